@@ -1,0 +1,151 @@
+/* pcop-b200 — C ABI of the B200-native product-convolution apply path.
+ *
+ * Drop-in boundary for the reference's assembled operator
+ * pcop::ProductConvolutionOperator (reference: proj/core/include/pcop/
+ * pc_operator.hpp:17-66).  Plain pointers and sizes only; no C++ or torch
+ * types.  Each entry point names the reference interface it replaces.
+ *
+ * Conventions kept from the reference:
+ *   - vectors are in domain lexicographic order, last axis fastest
+ *     (grid_function.hpp:11-13); batches are vector-major B x N;
+ *   - boxes are inclusive int64 [lo, hi] per axis (box.hpp:22-30);
+ *   - a grid function reads 0 outside its stored box (grid_function.hpp:41-43);
+ *   - shape / domain violations -> PCB_EINVAL, with the reference's
+ *     std::invalid_argument message text in pcb_last_error()
+ *     (pc_operator.cpp:34-37,46,59-60,86,101);
+ *   - the operator is immutable after pcb_create; calls on one handle are
+ *     serialized internally, so concurrent callers are safe
+ *     (pc_operator.hpp:15-16).
+ * There is no CPU fallback: every compute entry point runs sm_100a kernels
+ * and fails with PCB_ECUDA when no suitable device is present.
+ */
+#ifndef PCB_PCB_H
+#define PCB_PCB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define PCB_API __attribute__((visibility("default")))
+#else
+#define PCB_API
+#endif
+
+typedef enum pcb_status {
+    PCB_OK = 0,
+    PCB_EINVAL = 1,    /* std::invalid_argument in the reference */
+    PCB_ENOMEM = 2,
+    PCB_ECUDA = 3,     /* CUDA runtime / launch failure, or no sm_100 device */
+    PCB_ENCCL = 4,
+    PCB_EINTERNAL = 5
+} pcb_status;
+
+typedef enum pcb_mode {
+    PCB_MODE_AUTO = 0,   /* pick by the cost model (pcb_get_info reports the choice) */
+    PCB_MODE_GLOBAL = 1, /* common FFT grid over Omega, sum_k Phi_k . FFT(w_k f) accumulated in
+                            frequency space, one inverse FFT per vector */
+    PCB_MODE_LOCAL = 2   /* per-term FFT grid on the support-trimmed kernel box (the reference's own
+                            per-term padding rule, fft.cpp:64-70, on the nonzero box of phi_k^E) */
+} pcb_mode;
+
+typedef struct pcb_op pcb_op;
+
+typedef struct pcb_options {
+    int32_t device;        /* CUDA device ordinal; -1 = current device */
+    int32_t mode;          /* pcb_mode */
+    int32_t max_batch;     /* vectors per internal pass; 0 = default (16) */
+    int32_t shard_rank;    /* shard-by-k: this process owns terms of shard_rank ... */
+    int32_t shard_count;   /* ... out of shard_count (1 = unsharded); apply returns the partial sum */
+    int32_t reserved;
+    int64_t scratch_bytes; /* scratch budget for pipelined passes; 0 = default */
+} pcb_options;
+
+typedef struct pcb_info {
+    int32_t dim;
+    int32_t rank;           /* r, number of terms */
+    int32_t rank_active;    /* terms with a nonzero kernel window owned by this shard */
+    int32_t mode;           /* resolved pcb_mode */
+    int32_t n_groups;       /* distinct FFT shapes */
+    int32_t fft_size[3];    /* FFT shape of the largest group */
+    int64_t n_points;       /* N */
+    int64_t spectra_bytes;  /* device bytes of stored half spectra Phi_k */
+    int64_t device_bytes;   /* all device memory held by the handle */
+    double bytes_per_vector;  /* algorithmic HBM bytes per applied vector (spectra read once + f,g) */
+    double flops_per_vector;  /* nominal fp64 flops per applied vector */
+    int32_t launches_per_batch; /* kernels launched by one apply batch call */
+    int32_t reserved;
+} pcb_info;
+
+PCB_API void pcb_default_options(pcb_options* opt);
+PCB_API const char* pcb_last_error(void);
+
+/* Replaces ProductConvolutionOperator(domain, grid, weights, impulses)
+ * (pc_operator.hpp:20-22, pc_operator.cpp:26-38).  Term k: weight w_k on box
+ * [w_lo+k*dim, w_hi+k*dim] with values w_vals[k] (lexicographic), extended
+ * impulse phi_k^E on [phi_lo+k*dim, phi_hi+k*dim] with values phi_vals[k].
+ * points (r*dim, may be NULL) are the sample points p_k (informational).
+ * All host inputs are copied; the caller may free them on return.  Builds the
+ * spectra (K1) before returning. */
+PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t r,
+                              const int64_t* points, const int64_t* w_lo, const int64_t* w_hi,
+                              const double* const* w_vals, const int64_t* phi_lo, const int64_t* phi_hi,
+                              const double* const* phi_vals, const pcb_options* opt, pcb_op** out);
+PCB_API pcb_status pcb_destroy(pcb_op* op);
+PCB_API pcb_status pcb_get_info(const pcb_op* op, pcb_info* info);
+
+/* Replaces ProductConvolutionOperator::apply (pc_operator.cpp:45-56), batched
+ * (the reference's closest analogue is fft_convolve_batch, fft.cpp:164-181).
+ * F, G: host, B x N.  apply = B == 1. */
+PCB_API pcb_status pcb_apply_batch(pcb_op* op, int32_t B, const double* F, double* G);
+/* Replaces ProductConvolutionOperator::apply_adjoint (pc_operator.cpp:58-69). */
+PCB_API pcb_status pcb_apply_adjoint_batch(pcb_op* op, int32_t B, const double* F, double* G);
+/* Device-pointer variants: dF, dG on the handle's device, ordered on `stream`
+ * (a cudaStream_t; NULL = legacy default stream). */
+PCB_API pcb_status pcb_apply_batch_dev(pcb_op* op, int32_t B, const double* dF, double* dG, void* stream);
+PCB_API pcb_status pcb_apply_adjoint_batch_dev(pcb_op* op, int32_t B, const double* dF, double* dG,
+                                               void* stream);
+
+/* Replaces ProductConvolutionOperator::entry (pc_operator.cpp:84-96) for cnt
+ * (y, x) pairs (y, x: cnt*dim host int64).  Bit-identical to the reference's
+ * summation. */
+PCB_API pcb_status pcb_entries(pcb_op* op, int64_t cnt, const int64_t* y, const int64_t* x, double* out);
+/* Dense blocks for H-matrix conversion (reference caller: dense_block,
+ * hmatrix.cpp:138-150): block b has rows t_origin[b] + [0, block_shape) and
+ * cols s_origin[b] + [0, block_shape) (points lexicographic);
+ * out[b][i][j] row-major, nblk * prod(block_shape)^2 doubles. */
+PCB_API pcb_status pcb_blocks(pcb_op* op, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
+                              const int64_t* block_shape, double* out);
+PCB_API pcb_status pcb_blocks_dev(pcb_op* op, int32_t nblk, const int64_t* d_t_origin,
+                                  const int64_t* d_s_origin, const int64_t* block_shape, double* d_out,
+                                  void* stream);
+
+/* Randomized a-posteriori estimator (adaptivity.cpp:75-121): Ytilde_i =
+ * Atilde^* zeta_i for q probes Z (q x N), eta_abs = sqrt(sum ||Ytilde-Y||^2/q),
+ * eta_rel = ||Ytilde-Y||_F / ||Y||_F, eta_cells[c] over leaf box c.  ytilde
+ * may be NULL.  Host pointers. */
+PCB_API pcb_status pcb_probe_estimate(pcb_op* op, int32_t q, const double* Z, const double* Y, int32_t nleaf,
+                                      const int64_t* leaf_lo, const int64_t* leaf_hi, double* ytilde,
+                                      double* eta_cells, double* eta_abs, double* eta_rel);
+/* Device variant: dZ, dY, dYt (q x N, dYt required) on device; results to host. */
+PCB_API pcb_status pcb_probe_estimate_dev(pcb_op* op, int32_t q, const double* dZ, const double* dY, double* dYt,
+                                          int32_t nleaf, const int64_t* leaf_lo, const int64_t* leaf_hi,
+                                          double* eta_cells, double* eta_abs, double* eta_rel, void* stream);
+
+/* Number of kernels this library has launched in the process (all handles). */
+PCB_API long long pcb_launch_count(void);
+
+/* Host utilities reproducing the reference's random streams (libstdc++):
+ * std::mt19937_64(seed) + std::normal_distribution<double>(0,1)
+ * (adaptivity.cpp:19-23, test_pc_operator.cpp:13-18) and
+ * std::uniform_int_distribution<int64_t>(lo, hi). */
+PCB_API pcb_status pcb_normal_fill(uint64_t seed, int64_t count, double* out);
+PCB_API pcb_status pcb_uniform_int_fill(uint64_t seed, int64_t lo, int64_t hi, int64_t count, int64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PCB_PCB_H */

@@ -1,0 +1,766 @@
+// sm_100a fp64 kernels of the product-convolution apply path.
+//
+//   K1  spectra build      rows_fwd<RF_SPEC> -> [mid<MM_FWD_SPEC>] -> cols<CM_SPEC>
+//   K2  weight+pad+FFT     rows_fwd<RF_APPLY> (w_k . f gathered on the footprint, zero-padded,
+//                          R2C along the last axis) -> [mid<MM_FWD_APPLY>] (pruned: m rows in)
+//   K3  frequency MAC      cols<CM_APPLY_*> : pruned axis-0 FFT, x Phi_k, (global mode: accumulate
+//                          over k in registers), axis-0 inverse — all inside one CTA per column tile
+//   K4  inverse + crop     [mid<MM_INV_*>] -> rows_inv<RI_*> : C2R along the last axis, gathered
+//                          per output line over the contributing terms in ascending k, cropped to Omega
+//   K5  adjoint/probes     the same passes with conj(Phi_k) (rows_fwd<RF_ADJ>, cols<CM_ADJ_*>,
+//                          rows_inv<RI_ADJ>), plus probe_sums for eta
+//   K6  entry/block gather entries / blocks
+// Reference semantics: pc_operator.cpp:45-96, fft.cpp:64-162, adaptivity.cpp:75-121.
+#include <cstdio>
+
+#include "fft.cuh"
+#include "kernels.cuh"
+
+namespace pcb {
+
+namespace {
+
+constexpr int kPadShift = 4;  // one pad word per 16 shared-memory words
+
+__device__ __forceinline__ const double2* twtab(const double2* tw, int len) { return tw + (len - 8); }
+
+template <int LEN, int NL>
+constexpr int smem_words() {
+    return SmemLine<LEN, NL, kPadShift>::WORDS;
+}
+
+// number of lines of one item for the rows_fwd pass
+__device__ __forceinline__ int64_t rows_fwd_lines(const PassArgs& a, const TermDesc& t, int mode) {
+    if (mode == RF_APPLY) return a.D == 2 ? t.m[0] : (int64_t)t.m[0] * t.m[1];
+    if (mode == RF_ADJ) return a.D == 2 ? t.o_cnt[0] : (int64_t)t.o_cnt[0] * t.o_cnt[1];
+    return a.D == 2 ? a.P[0] : (int64_t)a.P[0] * a.P[1];
+}
+
+__device__ __forceinline__ int64_t imod(int64_t a, int64_t p) {
+    int64_t r = a % p;
+    return r < 0 ? r + p : r;
+}
+
+// ---------------------------------------------------------------------------
+// rows_fwd: R2C along the last axis (length P = 2N) via an N-point complex FFT
+// of z[j] = x[2j] + i x[2j+1] and the usual even/odd split.
+template <int N, int NL, int MODE>
+__global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_fwd(PassArgs a) {
+    constexpr int TPL = FftCfg<N>::TPL;
+    constexpr int R = FftCfg<N>::R;
+    constexpr int RF = FirstPos<N>::RF;
+    extern __shared__ double2 buf[];
+
+    const int item = blockIdx.y;
+    const bool gmode = (MODE == RF_ADJ) && a.global;
+    const int nvec = MODE == RF_SPEC ? 1 : a.B;
+    const int slot = gmode ? 0 : item / nvec;
+    const int vec = gmode ? item : item % nvec;
+    const TermDesc& td = gmode ? *a.gdesc : a.terms[a.slots[slot]];
+    const int64_t nlines = rows_fwd_lines(a, td, MODE);
+    const int64_t line0 = (int64_t)blockIdx.x * NL;
+    if (line0 >= nlines) return;
+
+    const int D = a.D;
+    const int ax = D - 1;  // real axis
+    const int lead1 = D == 3 ? 1 : 0;
+    // per-line lead coordinates and S row offset
+    auto line_info = [&](int64_t line, int64_t& src_off, int64_t& s_row, int& aux) {
+        // aux: APPLY -> w row; ADJ -> unused; SPEC -> validity of lead (1 valid)
+        int64_t c0, c1 = 0;
+        if (MODE == RF_APPLY) {
+            if (D == 3) { c0 = line / td.m[1]; c1 = line % td.m[1]; } else { c0 = line; }
+            const int64_t x0 = td.x_lo[0] + c0 - a.dom_lo[0];
+            const int64_t x1 = D == 3 ? td.x_lo[1] + c1 - a.dom_lo[1] : 0;
+            src_off = (int64_t)vec * a.N + (D == 3 ? (x0 * a.n[1] + x1) * a.n[2] : x0 * a.n[1]) +
+                      (td.x_lo[ax] - a.dom_lo[ax]);
+            aux = (int)(D == 3 ? c0 * td.m[1] + c1 : c0);
+            s_row = D == 3 ? (c0 * a.P[1] + c1) * a.W : c0 * a.W;
+        } else if (MODE == RF_ADJ) {
+            int64_t v0, v1 = 0;
+            if (D == 3) { v0 = td.o_lo[0] + line / td.o_cnt[1]; v1 = td.o_lo[1] + line % td.o_cnt[1]; }
+            else { v0 = td.o_lo[0] + line; }
+            const int64_t y0 = td.s[0] + v0 - a.dom_lo[0];
+            const int64_t y1 = D == 3 ? td.s[1] + v1 - a.dom_lo[1] : 0;
+            src_off = (int64_t)vec * a.N + (D == 3 ? (y0 * a.n[1] + y1) * a.n[2] : y0 * a.n[1]) +
+                      (td.s[ax] - a.dom_lo[ax]);
+            aux = 0;
+            s_row = D == 3 ? ((v0 - td.o_lo[0]) * a.P[1] + v1) * a.W : (v0 - td.o_lo[0]) * a.W;
+        } else {
+            int64_t t0, t1 = 0;
+            if (D == 3) { t0 = line / a.P[1]; t1 = line % a.P[1]; } else { t0 = line; }
+            // z_a = k_lo + ((t + c - k_lo) mod P), c = s - x_lo
+            const int64_t z0 = imod(t0 + td.s[0] - td.x_lo[0] - td.k_lo[0], a.P[0]);
+            const int64_t z1 = D == 3 ? imod(t1 + td.s[1] - td.x_lo[1] - td.k_lo[1], a.P[1]) : 0;
+            aux = (z0 < td.k_ext[0] && (D == 2 || z1 < td.k_ext[1])) ? 1 : 0;
+            src_off = td.phi_off + (D == 3 ? (z0 * td.k_ext[1] + z1) * td.k_ext[2] : z0 * td.k_ext[1]);
+            s_row = D == 3 ? (t0 * a.P[1] + t1) * a.W : t0 * a.W;
+        }
+    };
+
+    // phase 1: gather the real line into shared memory as z[j] = (x[2j], x[2j+1])
+    for (int idx = threadIdx.x; idx < NL * N; idx += blockDim.x) {
+        const int l = idx / N;
+        const int p = idx - l * N;
+        const int64_t line = line0 + l;
+        double2 z = czero();
+        if (line < nlines) {
+            int64_t src_off, s_row;
+            int aux;
+            line_info(line, src_off, s_row, aux);
+            double xv[2] = {0.0, 0.0};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int u = 2 * p + h;
+                if (MODE == RF_APPLY) {
+                    if (u < td.m[ax]) xv[h] = a.in[src_off + u] * a.w_pool[td.w_off + (int64_t)aux * td.m[ax] + u];
+                } else if (MODE == RF_ADJ) {
+                    if (u >= td.o_lo[ax] && u < td.o_lo[ax] + td.o_cnt[ax]) xv[h] = a.in[src_off + u];
+                } else {
+                    const int64_t zl = imod(u + td.s[ax] - td.x_lo[ax] - td.k_lo[ax], a.P[ax]);
+                    if (aux && zl < td.k_ext[ax]) xv[h] = a.phi_pool[src_off + zl];
+                }
+            }
+            z = make_double2(xv[0], xv[1]);
+        }
+        buf[sidx<NL, kPadShift>(p, l)] = z;
+    }
+    __syncthreads();
+
+    const int l = threadIdx.x % NL;
+    const int tl = threadIdx.x / NL;
+    double2 v[R];
+#pragma unroll
+    for (int b = 0; b < R / RF; ++b)
+#pragma unroll
+        for (int r = 0; r < RF; ++r) v[b * RF + r] = buf[sidx<NL, kPadShift>(FirstPos<N>::pos(tl, b, r), l)];
+    fft_fwd_order<N, -1, NL, kPadShift>(v, buf, l, tl, twtab(a.tw, N));
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int pos = N >= 16 ? tl + r * (N / 16) : r;
+        buf[sidx<NL, kPadShift>(pos, l)] = v[r];
+    }
+    __syncthreads();
+
+    // phase 3: even/odd split X[k] = A[k] + W^k B[k], k = 0..N
+    const double2* twP = twtab(a.tw, 2 * N);
+    double2* S_item = a.S + (int64_t)item * a.S_stride;
+    for (int idx = threadIdx.x; idx < NL * (N + 1); idx += blockDim.x) {
+        const int ll = idx / (N + 1);
+        const int k = idx - ll * (N + 1);
+        const int64_t line = line0 + ll;
+        if (line >= nlines) continue;
+        int64_t src_off, s_row;
+        int aux;
+        line_info(line, src_off, s_row, aux);
+        const double2 zk = buf[sidx<NL, kPadShift>(k & (N - 1), ll)];
+        const double2 zn = buf[sidx<NL, kPadShift>((N - k) & (N - 1), ll)];
+        const double2 A = make_double2(0.5 * (zk.x + zn.x), 0.5 * (zk.y - zn.y));
+        const double2 Bm = make_double2(0.5 * (zk.y + zn.y), -0.5 * (zk.x - zn.x));  // (zk - conj zn)/(2i)
+        S_item[s_row + k] = cadd(A, cmul(__ldg(&twP[k]), Bm));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// mid: complex FFT along axis 1 of 3D data [planes][P1][W], lines = columns c2.
+template <int P1, int NL, int MODE>
+__global__ void __launch_bounds__(NL * FftCfg<P1>::TPL) k_mid(PassArgs a) {
+    constexpr int R = FftCfg<P1>::R;
+    constexpr int RF = FirstPos<P1>::RF;
+    constexpr int RL = LastPos<P1>::RL;
+    extern __shared__ double2 buf[];
+    const bool fwd = MODE <= MM_FWD_SPEC;
+    const bool gmode = a.global && (MODE == MM_INV_APPLY || MODE == MM_FWD_ADJ);
+    const int nvec = MODE == MM_FWD_SPEC ? 1 : a.B;
+    const int item = blockIdx.z;
+    const int slot = gmode ? 0 : item / nvec;
+    const int vec = gmode ? item : item % nvec;
+    const TermDesc& td = gmode ? *a.gdesc : a.terms[a.slots[slot]];
+    int64_t planes;
+    int in_lo = 0, in_cnt = P1, keep_lo = 0, keep_cnt = P1;
+    if (MODE == MM_FWD_APPLY) { planes = td.m[0]; in_cnt = td.m[1]; }
+    else if (MODE == MM_FWD_ADJ) { planes = td.o_cnt[0]; in_lo = td.o_lo[1]; in_cnt = td.o_cnt[1]; }
+    else if (MODE == MM_FWD_SPEC) { planes = a.P[0]; }
+    else if (MODE == MM_INV_APPLY) { planes = td.o_cnt[0]; keep_lo = td.o_lo[1]; keep_cnt = td.o_cnt[1]; }
+    else { planes = td.m[0]; keep_cnt = td.m[1]; }
+    const int64_t plane = blockIdx.y;
+    if (plane >= planes) return;
+    const int l = threadIdx.x % NL;
+    const int tl = threadIdx.x / NL;
+    const int64_t c = (int64_t)blockIdx.x * NL + l;
+    const bool cvalid = c < a.W;
+    double2* base = (fwd ? a.S + (int64_t)item * a.S_stride : a.T + (int64_t)item * a.T_stride) +
+                    plane * (int64_t)a.P[1] * a.W + c;
+    double2 v[R];
+    if (fwd) {
+#pragma unroll
+        for (int b = 0; b < R / RF; ++b)
+#pragma unroll
+            for (int r = 0; r < RF; ++r) {
+                const int p = FirstPos<P1>::pos(tl, b, r);
+                v[b * RF + r] = (cvalid && p >= in_lo && p < in_lo + in_cnt) ? base[(int64_t)p * a.W] : czero();
+            }
+        fft_fwd_order<P1, -1, NL, kPadShift>(v, buf, l, tl, twtab(a.tw, P1));
+        if (cvalid) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int pos = P1 >= 16 ? tl + r * (P1 / 16) : r;
+                base[(int64_t)pos * a.W] = v[r];
+            }
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int pos = P1 >= 16 ? tl + r * (P1 / 16) : r;
+            v[r] = cvalid ? base[(int64_t)pos * a.W] : czero();
+        }
+        fft_rev_order<P1, +1, NL, kPadShift>(v, buf, l, tl, twtab(a.tw, P1));
+        if (cvalid) {
+#pragma unroll
+            for (int b = 0; b < R / RL; ++b)
+#pragma unroll
+                for (int r = 0; r < RL; ++r) {
+                    const int p = LastPos<P1>::pos(tl, b, r);
+                    if (p >= keep_lo && p < keep_lo + keep_cnt) base[(int64_t)(p - keep_lo) * a.W] = v[b * RL + r];
+                }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// cols: axis-0 pass with the frequency-domain product (K3).
+template <int P0, int NL, int MODE>
+__global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
+    constexpr int R = FftCfg<P0>::R;
+    constexpr int RF = FirstPos<P0>::RF;
+    constexpr int RL = LastPos<P0>::RL;
+    extern __shared__ double2 buf[];
+    const bool global = MODE == CM_APPLY_GLOBAL || MODE == CM_ADJ_GLOBAL;
+    const int nvec = MODE == CM_SPEC ? 1 : a.B;
+    const int item = blockIdx.y;
+    const int l = threadIdx.x % NL;
+    const int tl = threadIdx.x / NL;
+    const int64_t c0 = (int64_t)blockIdx.x * NL;
+    const int64_t c = c0 + l;
+    const bool cvalid = c < a.L;
+    const int64_t tile_off = (c0 / NL) * (int64_t)P0 * NL + l;  // spectrum tile-major offset
+    const double2* tw0 = twtab(a.tw, P0);
+
+    auto load_in = [&](const double2* src, int in_lo, int in_cnt, double2* v) {
+#pragma unroll
+        for (int b = 0; b < R / RF; ++b)
+#pragma unroll
+            for (int r = 0; r < RF; ++r) {
+                const int p = FirstPos<P0>::pos(tl, b, r);
+                v[b * RF + r] = (cvalid && p >= in_lo && p < in_lo + in_cnt) ? src[(int64_t)(p - in_lo) * a.L + c]
+                                                                              : czero();
+            }
+    };
+    auto store_out = [&](double2* dst, int keep_lo, int keep_cnt, const double2* v) {
+        if (!cvalid) return;
+#pragma unroll
+        for (int b = 0; b < R / RL; ++b)
+#pragma unroll
+            for (int r = 0; r < RL; ++r) {
+                const int p = LastPos<P0>::pos(tl, b, r);
+                if (p >= keep_lo && p < keep_lo + keep_cnt) dst[(int64_t)(p - keep_lo) * a.L + c] = v[b * RL + r];
+            }
+    };
+    auto fpos = [&](int r) { return P0 >= 16 ? tl + r * (P0 / 16) : r; };
+
+    double2 v[R];
+    if (MODE == CM_SPEC || MODE == CM_APPLY_LOCAL || MODE == CM_ADJ_LOCAL) {
+        const int slot = item / nvec;
+        const TermDesc& td = a.terms[a.slots[slot]];
+        const double2* S_item = a.S + (int64_t)item * a.S_stride;
+        if (MODE == CM_SPEC) load_in(S_item, 0, P0, v);
+        else if (MODE == CM_APPLY_LOCAL) load_in(S_item, 0, td.m[0], v);
+        else load_in(S_item, td.o_lo[0], td.o_cnt[0], v);
+        fft_fwd_order<P0, -1, NL, kPadShift>(v, buf, l, tl, tw0);
+        double2* spec = a.spec_pool + td.spec_off + tile_off;
+        if (MODE == CM_SPEC) {
+            if (cvalid) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) spec[(int64_t)fpos(r) * NL] = v[r];
+            }
+            return;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double2 ph = cvalid ? __ldg(&spec[(int64_t)fpos(r) * NL]) : czero();
+            v[r] = MODE == CM_APPLY_LOCAL ? cmul(v[r], ph) : cmulc(v[r], ph);
+        }
+        fft_rev_order<P0, +1, NL, kPadShift>(v, buf, l, tl, tw0);
+        double2* T_item = a.T + (int64_t)item * a.T_stride;
+        if (MODE == CM_APPLY_LOCAL) store_out(T_item, td.o_lo[0], td.o_cnt[0], v);
+        else store_out(T_item, 0, td.m[0], v);
+        return;
+    }
+
+    if (MODE == CM_APPLY_GLOBAL) {
+        const int vec = item;
+        double2 acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = czero();
+        for (int slot = 0; slot < a.n_slots; ++slot) {
+            const TermDesc& td = a.terms[a.slots[slot]];
+            const double2* S_item = a.S + ((int64_t)slot * a.B + vec) * a.S_stride;
+            load_in(S_item, 0, td.m[0], v);
+            fft_fwd_order<P0, -1, NL, kPadShift>(v, buf, l, tl, tw0);
+            const double2* spec = a.spec_pool + td.spec_off + tile_off;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double2 ph = cvalid ? __ldg(&spec[(int64_t)fpos(r) * NL]) : czero();
+                acc[r] = cadd(acc[r], cmul(v[r], ph));
+            }
+        }
+        fft_rev_order<P0, +1, NL, kPadShift>(acc, buf, l, tl, tw0);
+        const TermDesc& g = *a.gdesc;
+        store_out(a.T + (int64_t)vec * a.T_stride, g.o_lo[0], g.o_cnt[0], acc);
+        return;
+    }
+
+    // CM_ADJ_GLOBAL: one forward transform of g, one pruned inverse per term
+    {
+        const int vec = item;
+        const TermDesc& g = *a.gdesc;
+        double2 x[R];
+        load_in(a.S + (int64_t)vec * a.S_stride, g.o_lo[0], g.o_cnt[0], x);
+        fft_fwd_order<P0, -1, NL, kPadShift>(x, buf, l, tl, tw0);
+        for (int slot = 0; slot < a.n_slots; ++slot) {
+            const TermDesc& td = a.terms[a.slots[slot]];
+            const double2* spec = a.spec_pool + td.spec_off + tile_off;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double2 ph = cvalid ? __ldg(&spec[(int64_t)fpos(r) * NL]) : czero();
+                v[r] = cmulc(x[r], ph);
+            }
+            fft_rev_order<P0, +1, NL, kPadShift>(v, buf, l, tl, tw0);
+            store_out(a.T + ((int64_t)slot * a.B + vec) * a.T_stride, 0, td.m[0], v);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// rows_inv: C2R along the last axis for every T line contributing to one output
+// line (CSR, ascending k), cropped and accumulated in a fixed order.
+template <int N, int NL, int MODE>
+__global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_inv(PassArgs a) {
+    constexpr int R = FftCfg<N>::R;
+    constexpr int RL = LastPos<N>::RL;
+    extern __shared__ double2 buf[];
+    const int64_t line = blockIdx.x;
+    const int vec = blockIdx.y;
+    const int D = a.D;
+    const int ax = D - 1;
+    const int n_last = a.n[ax];
+    double* acc = reinterpret_cast<double*>(buf + smem_words<N, NL>());
+    double* xs = reinterpret_cast<double*>(buf);
+    for (int i = threadIdx.x; i < n_last; i += blockDim.x) acc[i] = 0.0;
+    const int64_t e_beg = a.line_ptr[line];
+    const int64_t e_end = a.line_ptr[line + 1];
+    const double2* twP = twtab(a.tw, 2 * N);
+    const int l = threadIdx.x % NL;
+    const int tl = threadIdx.x / NL;
+
+    for (int64_t e0 = e_beg; e0 < e_end; e0 += NL) {
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < NL * N; idx += blockDim.x) {
+            const int ll = idx / N;
+            const int k = idx - ll * N;
+            const int64_t e = e0 + ll;
+            double2 z = czero();
+            if (e < e_end) {
+                const GatherEntry en = a.entries[e];
+                const int64_t it = a.global ? vec : (int64_t)en.slot * a.B + vec;
+                const double2* row = a.T + it * a.T_stride + en.t_off;
+                const double2 xk = row[k];
+                const double2 xn = row[N - k];
+                const double2 E = make_double2(xk.x + xn.x, xk.y - xn.y);    // X[k] + conj X[N-k]
+                const double2 Dd = make_double2(xk.x - xn.x, xk.y + xn.y);   // X[k] - conj X[N-k]
+                const double2 O = cmulc(Dd, __ldg(&twP[k]));                 // * exp(+2 pi i k / P)
+                z = make_double2(E.x - O.y, E.y + O.x);                      // E + i O
+            }
+            buf[sidx<NL, kPadShift>(k, ll)] = z;
+        }
+        __syncthreads();
+        double2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int pos = N >= 16 ? tl + r * (N / 16) : r;
+            v[r] = buf[sidx<NL, kPadShift>(pos, l)];
+        }
+        fft_rev_order<N, +1, NL, kPadShift>(v, buf, l, tl, twtab(a.tw, N));
+        __syncthreads();
+#pragma unroll
+        for (int b = 0; b < R / RL; ++b)
+#pragma unroll
+            for (int r = 0; r < RL; ++r) {
+                const int p = LastPos<N>::pos(tl, b, r);
+                xs[(int64_t)l * 2 * N + 2 * p] = v[b * RL + r].x;
+                xs[(int64_t)l * 2 * N + 2 * p + 1] = v[b * RL + r].y;
+            }
+        __syncthreads();
+        const int ne = (int)((e_end - e0) < NL ? (e_end - e0) : NL);
+        for (int i = threadIdx.x; i < n_last; i += blockDim.x) {
+            double s = acc[i];
+            const int64_t yl = a.dom_lo[ax] + i;
+            for (int ll = 0; ll < ne; ++ll) {
+                const GatherEntry en = a.entries[e0 + ll];
+                const TermDesc& td = a.global ? *a.gdesc : a.terms[a.slots[en.slot]];
+                if (MODE == RI_APPLY) {
+                    const int64_t vv = yl - td.s[ax];
+                    if (vv >= td.o_lo[ax] && vv < td.o_lo[ax] + td.o_cnt[ax])
+                        s += xs[(int64_t)ll * 2 * N + vv] * a.scale;
+                } else {
+                    const int64_t u = yl - td.x_lo[ax];
+                    if (u >= 0 && u < td.m[ax])
+                        s += a.w_pool[td.w_off + (int64_t)en.w_row * td.m[ax] + u] * (xs[(int64_t)ll * 2 * N + u] * a.scale);
+                }
+            }
+            acc[i] = s;
+        }
+    }
+    __syncthreads();
+    double* g = a.out + (int64_t)vec * a.N + line * n_last;
+    for (int i = threadIdx.x; i < n_last; i += blockDim.x) g[i] = a.accumulate ? g[i] + acc[i] : acc[i];
+}
+
+// ---------------------------------------------------------------------------
+// K6: Atilde[y,x] = sum_{k: x in U_k} w_k[x] phi_k^E[y - x], k ascending, the
+// reference's operation order (pc_operator.cpp:84-96) with IEEE mul/add (no FMA
+// contraction) so the result is the reference's bit for bit.
+__device__ __forceinline__ double entry_value(const EntryArgs& a, const int64_t* y, const int64_t* x, bool& bad) {
+    const int D = a.D;
+    int64_t bl = 0;
+    for (int i = 0; i < D; ++i) {
+        const int64_t yi = y[i] - a.dom_lo[i], xi = x[i] - a.dom_lo[i];
+        if (yi < 0 || yi >= a.n[i] || xi < 0 || xi >= a.n[i]) {
+            bad = true;
+            return 0.0;
+        }
+        bl = bl * a.nb[i] + xi / a.bucket[i];
+    }
+    double sum = 0.0;
+    for (int64_t q = a.bucket_ptr[bl]; q < a.bucket_ptr[bl + 1]; ++q) {
+        const TermDesc& t = a.terms[a.bucket_terms[q]];
+        int64_t wl = 0, zl = 0;
+        bool inx = true, inz = true;
+        for (int i = 0; i < D; ++i) {
+            const int64_t u = x[i] - t.x_lo[i];
+            if (u < 0 || u >= t.m[i]) inx = false;
+            wl = wl * t.m[i] + u;
+            const int64_t z = y[i] - x[i] - t.k_lo[i];
+            if (z < 0 || z >= t.k_ext[i]) inz = false;
+            zl = zl * t.k_ext[i] + z;
+        }
+        if (!inx) continue;
+        const double wx = a.w_pool[t.w_off + wl];
+        if (wx == 0.0) continue;
+        const double ph = inz ? a.phi_pool[t.phi_off + zl] : 0.0;
+        sum = __dadd_rn(sum, __dmul_rn(wx, ph));
+    }
+    return sum;
+}
+
+__global__ void k_entries(EntryArgs a, int64_t cnt, const int64_t* __restrict__ y, const int64_t* __restrict__ x,
+                          double* __restrict__ out, int32_t* bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+        bool b = false;
+        const double v = entry_value(a, y + i * a.D, x + i * a.D, b);
+        out[i] = v;
+        if (b) atomicOr(bad, 1);
+    }
+}
+
+__global__ void k_blocks(EntryArgs a, int32_t nblk, const int64_t* __restrict__ t_origin,
+                         const int64_t* __restrict__ s_origin, const int32_t* __restrict__ bshape,
+                         double* __restrict__ out, int32_t* bad) {
+    const int D = a.D;
+    int64_t bs = 1;
+    for (int i = 0; i < D; ++i) bs *= bshape[i];
+    const int64_t total = (int64_t)nblk * bs * bs;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t blk = g / (bs * bs);
+        const int64_t rem = g - blk * bs * bs;
+        int64_t i = rem / bs, j = rem - (rem / bs) * bs;
+        int64_t y[3], x[3];
+        for (int d = D - 1; d >= 0; --d) {
+            y[d] = t_origin[blk * D + d] + i % bshape[d];
+            i /= bshape[d];
+            x[d] = s_origin[blk * D + d] + j % bshape[d];
+            j /= bshape[d];
+        }
+        bool b = false;
+        out[g] = entry_value(a, y, x, b);
+        if (b) atomicOr(bad, 1);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5 reductions: d2[box, probe] = sum_{p in box cap Omega} (Yt - Y)^2, y2[probe] = sum Y^2
+__global__ void k_probe_sums(int D, int32_t n0, int32_t n1, int32_t n2, int32_t nbox, const int64_t* __restrict__ blo,
+                             const int64_t* __restrict__ bhi, const double* __restrict__ Yt,
+                             const double* __restrict__ Y, double* d2, double* y2) {
+    const int box = blockIdx.x;  // box == nbox -> whole domain (also sums Y^2)
+    const int probe = blockIdx.y;
+    const int32_t n[3] = {n0, n1, D == 3 ? n2 : 1};
+    int64_t lo[3] = {0, 0, 0}, hi[3] = {n0 - 1, n1 - 1, n[2] - 1};
+    if (box < nbox) {
+        for (int i = 0; i < D; ++i) {
+            lo[i] = blo[box * D + i] > 0 ? blo[box * D + i] : 0;
+            hi[i] = bhi[box * D + i] < n[i] - 1 ? bhi[box * D + i] : n[i] - 1;
+        }
+    }
+    int64_t ext[3];
+    int64_t cnt = 1;
+    for (int i = 0; i < 3; ++i) {
+        ext[i] = hi[i] >= lo[i] ? hi[i] - lo[i] + 1 : 0;
+        cnt *= ext[i];
+    }
+    const int64_t N = (int64_t)n[0] * n[1] * n[2];
+    const double* yt = Yt + probe * N;
+    const double* yy = Y + probe * N;
+    double s = 0.0, sy = 0.0;
+    for (int64_t q = threadIdx.x; q < cnt; q += blockDim.x) {
+        const int64_t i2 = q % ext[2];
+        const int64_t r = q / ext[2];
+        const int64_t i1 = r % ext[1];
+        const int64_t i0 = r / ext[1];
+        const int64_t off = ((lo[0] + i0) * n[1] + lo[1] + i1) * n[2] + lo[2] + i2;
+        const double dv = yt[off] - yy[off];
+        s += dv * dv;
+        sy += yy[off] * yy[off];
+    }
+    __shared__ double red[2][256];
+    red[0][threadIdx.x] = s;
+    red[1][threadIdx.x] = sy;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            red[0][threadIdx.x] += red[0][threadIdx.x + w];
+            red[1][threadIdx.x] += red[1][threadIdx.x + w];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        d2[(int64_t)box * gridDim.y + probe] = red[0][0];
+        if (box == nbox) y2[probe] = red[1][0];
+    }
+}
+
+__global__ void k_zero(double* p, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// dispatch over the compile-time sizes
+
+template <typename K>
+cudaError_t launch_dyn(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const PassArgs& a) {
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    kernel<<<grid, block, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int LEN>
+constexpr int rows_nl() {
+    return LEN >= 1024 ? 1 : (1024 / LEN > 16 ? 16 : 1024 / LEN);
+}
+template <int P>
+constexpr int cols_nl() {
+    return P >= 1024 ? 2 : (2048 / P > 32 ? 32 : 2048 / P);
+}
+
+template <int N, int MODE>
+cudaError_t rows_fwd_n(const PassArgs& a, cudaStream_t st) {
+    constexpr int NL = rows_nl<N>();
+    int64_t maxlines;
+    if (MODE == RF_SPEC) maxlines = a.D == 2 ? a.P[0] : (int64_t)a.P[0] * a.P[1];
+    else maxlines = a.D == 2 ? a.n[0] + 0 : (int64_t)a.n[0] * a.n[1];
+    // lines per item never exceed max(m, o_cnt) <= P per axis; bound by P
+    if (MODE != RF_SPEC) maxlines = a.D == 2 ? a.P[0] : (int64_t)a.P[0] * a.P[1];
+    const int items = (MODE == RF_ADJ && a.global) ? a.B : a.n_slots * (MODE == RF_SPEC ? 1 : a.B);
+    dim3 grid((unsigned)((maxlines + NL - 1) / NL), (unsigned)items);
+    const size_t smem = sizeof(double2) * smem_words<N, NL>();
+    return launch_dyn(k_rows_fwd<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
+}
+
+template <int MODE>
+cudaError_t rows_fwd_mode(const PassArgs& a, cudaStream_t st) {
+    switch (a.P[a.D - 1] / 2) {
+        case 8: return rows_fwd_n<8, MODE>(a, st);
+        case 16: return rows_fwd_n<16, MODE>(a, st);
+        case 32: return rows_fwd_n<32, MODE>(a, st);
+        case 64: return rows_fwd_n<64, MODE>(a, st);
+        case 128: return rows_fwd_n<128, MODE>(a, st);
+        case 256: return rows_fwd_n<256, MODE>(a, st);
+        case 512: return rows_fwd_n<512, MODE>(a, st);
+        case 1024: return rows_fwd_n<1024, MODE>(a, st);
+        case 2048: return rows_fwd_n<2048, MODE>(a, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int P1, int MODE>
+cudaError_t mid_p(const PassArgs& a, cudaStream_t st) {
+    constexpr int NL = cols_nl<P1>();
+    const bool gmode = a.global && (MODE == MM_INV_APPLY || MODE == MM_FWD_ADJ);
+    const int items = gmode ? a.B : a.n_slots * (MODE == MM_FWD_SPEC ? 1 : a.B);
+    dim3 grid((unsigned)((a.W + NL - 1) / NL), (unsigned)a.P[0], (unsigned)items);
+    const size_t smem = sizeof(double2) * smem_words<P1, NL>();
+    return launch_dyn(k_mid<P1, NL, MODE>, grid, dim3(NL * FftCfg<P1>::TPL), smem, st, a);
+}
+
+template <int MODE>
+cudaError_t mid_mode(const PassArgs& a, cudaStream_t st) {
+    switch (a.P[1]) {
+        case 16: return mid_p<16, MODE>(a, st);
+        case 32: return mid_p<32, MODE>(a, st);
+        case 64: return mid_p<64, MODE>(a, st);
+        case 128: return mid_p<128, MODE>(a, st);
+        case 256: return mid_p<256, MODE>(a, st);
+        case 512: return mid_p<512, MODE>(a, st);
+        case 1024: return mid_p<1024, MODE>(a, st);
+        case 2048: return mid_p<2048, MODE>(a, st);
+        case 4096: return mid_p<4096, MODE>(a, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int P0, int MODE>
+cudaError_t cols_p(const PassArgs& a, cudaStream_t st) {
+    constexpr int NL = cols_nl<P0>();
+    if (a.nl_cols != NL) return cudaErrorInvalidValue;
+    const bool global = MODE == CM_APPLY_GLOBAL || MODE == CM_ADJ_GLOBAL;
+    const int items = global ? a.B : a.n_slots * (MODE == CM_SPEC ? 1 : a.B);
+    dim3 grid((unsigned)((a.L + NL - 1) / NL), (unsigned)items);
+    const size_t smem = sizeof(double2) * smem_words<P0, NL>();
+    return launch_dyn(k_cols<P0, NL, MODE>, grid, dim3(NL * FftCfg<P0>::TPL), smem, st, a);
+}
+
+template <int MODE>
+cudaError_t cols_mode(const PassArgs& a, cudaStream_t st) {
+    switch (a.P[0]) {
+        case 16: return cols_p<16, MODE>(a, st);
+        case 32: return cols_p<32, MODE>(a, st);
+        case 64: return cols_p<64, MODE>(a, st);
+        case 128: return cols_p<128, MODE>(a, st);
+        case 256: return cols_p<256, MODE>(a, st);
+        case 512: return cols_p<512, MODE>(a, st);
+        case 1024: return cols_p<1024, MODE>(a, st);
+        case 2048: return cols_p<2048, MODE>(a, st);
+        case 4096: return cols_p<4096, MODE>(a, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int N, int MODE>
+cudaError_t rows_inv_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
+    constexpr int NL = rows_nl<N>() > 8 ? 8 : rows_nl<N>();
+    dim3 grid((unsigned)n_lines, (unsigned)a.B);
+    const size_t smem = sizeof(double2) * smem_words<N, NL>() + sizeof(double) * (size_t)a.n[a.D - 1];
+    return launch_dyn(k_rows_inv<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
+}
+
+template <int MODE>
+cudaError_t rows_inv_mode(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
+    switch (a.P[a.D - 1] / 2) {
+        case 8: return rows_inv_n<8, MODE>(a, n_lines, st);
+        case 16: return rows_inv_n<16, MODE>(a, n_lines, st);
+        case 32: return rows_inv_n<32, MODE>(a, n_lines, st);
+        case 64: return rows_inv_n<64, MODE>(a, n_lines, st);
+        case 128: return rows_inv_n<128, MODE>(a, n_lines, st);
+        case 256: return rows_inv_n<256, MODE>(a, n_lines, st);
+        case 512: return rows_inv_n<512, MODE>(a, n_lines, st);
+        case 1024: return rows_inv_n<1024, MODE>(a, n_lines, st);
+        case 2048: return rows_inv_n<2048, MODE>(a, n_lines, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace
+
+int cols_tile_width(int P0) {
+    switch (P0) {
+        case 16: return cols_nl<16>();
+        case 32: return cols_nl<32>();
+        case 64: return cols_nl<64>();
+        case 128: return cols_nl<128>();
+        case 256: return cols_nl<256>();
+        case 512: return cols_nl<512>();
+        case 1024: return cols_nl<1024>();
+        case 2048: return cols_nl<2048>();
+        case 4096: return cols_nl<4096>();
+        default: return -1;
+    }
+}
+
+cudaError_t launch_rows_fwd(const PassArgs& a, int mode, cudaStream_t st) {
+    switch (mode) {
+        case RF_APPLY: return rows_fwd_mode<RF_APPLY>(a, st);
+        case RF_ADJ: return rows_fwd_mode<RF_ADJ>(a, st);
+        case RF_SPEC: return rows_fwd_mode<RF_SPEC>(a, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_mid(const PassArgs& a, int mode, cudaStream_t st) {
+    switch (mode) {
+        case MM_FWD_APPLY: return mid_mode<MM_FWD_APPLY>(a, st);
+        case MM_FWD_ADJ: return mid_mode<MM_FWD_ADJ>(a, st);
+        case MM_FWD_SPEC: return mid_mode<MM_FWD_SPEC>(a, st);
+        case MM_INV_APPLY: return mid_mode<MM_INV_APPLY>(a, st);
+        case MM_INV_ADJ: return mid_mode<MM_INV_ADJ>(a, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_cols(const PassArgs& a, int mode, cudaStream_t st) {
+    switch (mode) {
+        case CM_SPEC: return cols_mode<CM_SPEC>(a, st);
+        case CM_APPLY_LOCAL: return cols_mode<CM_APPLY_LOCAL>(a, st);
+        case CM_APPLY_GLOBAL: return cols_mode<CM_APPLY_GLOBAL>(a, st);
+        case CM_ADJ_LOCAL: return cols_mode<CM_ADJ_LOCAL>(a, st);
+        case CM_ADJ_GLOBAL: return cols_mode<CM_ADJ_GLOBAL>(a, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_rows_inv(const PassArgs& a, int mode, int64_t n_lines, cudaStream_t st) {
+    return mode == RI_APPLY ? rows_inv_mode<RI_APPLY>(a, n_lines, st) : rows_inv_mode<RI_ADJ>(a, n_lines, st);
+}
+
+cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, const int64_t* x, double* out,
+                           int32_t* bad, cudaStream_t st) {
+    if (cnt <= 0) return cudaSuccess;
+    const int64_t blocks = (cnt + 255) / 256;
+    k_entries<<<(unsigned)(blocks < 148 * 64 ? blocks : 148 * 64), 256, 0, st>>>(a, cnt, y, x, out, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
+                          const int32_t* bshape, double* out, int32_t* bad, cudaStream_t st) {
+    if (nblk <= 0) return cudaSuccess;
+    k_blocks<<<148 * 16, 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape, out, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_probe_sums(int D, const int32_t* n, int32_t nbox, const int64_t* box_lo, const int64_t* box_hi,
+                              int32_t q, const double* Yt, const double* Y, double* d2, double* y2, cudaStream_t st) {
+    dim3 grid((unsigned)(nbox + 1), (unsigned)q);
+    k_probe_sums<<<grid, 256, 0, st>>>(D, n[0], n[1], D == 3 ? n[2] : 1, nbox, box_lo, box_hi, Yt, Y, d2, y2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zero(double* p, int64_t n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_zero<<<148 * 8, 256, 0, st>>>(p, n);
+    return cudaGetLastError();
+}
+
+}  // namespace pcb

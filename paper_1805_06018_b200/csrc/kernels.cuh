@@ -1,0 +1,109 @@
+// Device-side descriptors shared by the host planner (plan.cpp) and the
+// kernels (kernels.cu).  Plain structs, passed by value or through device
+// arrays; no torch types anywhere.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pcb {
+
+// One product-convolution term k, in FFT index space (reference:
+// pc_operator.cpp:49-54; SURVEY.md 8(a) "GPU restatement").
+//   input window   X_k = footprint(w_k) cap Omega, x = x_lo + u, u in [0, m)
+//   output         y = s + v, v kept in [o_lo, o_lo + o_cnt)  (apply)
+//   kernel         trimmed phi_k^E box K = [k_lo, k_lo + k_ext), placed at
+//                  t = (z - c) mod P with c = s - x_lo
+// Apply: g[s+v] += IFFT( FFT_P(phi placed) . FFT_P(w f on X) )[v] / prod P.
+// Adjoint (same spectra, conjugated): out[x_lo+u] += w[u] IFFT(conj(Phi) FFT(g[s+.]))[u].
+struct TermDesc {
+    int64_t x_lo[3];
+    int64_t s[3];
+    int64_t k_lo[3];
+    int32_t m[3];
+    int32_t o_lo[3];
+    int32_t o_cnt[3];
+    int32_t k_ext[3];
+    int64_t w_off;     // doubles: w_k on X_k, row-major [m0][m1][m2]
+    int64_t phi_off;   // doubles: phi_k^E on K, row-major
+    int64_t spec_off;  // double2: spectrum, tile-major [L/NL][P0][NL]
+};
+
+// rows_inv gather list entry: one C2R line of T contributing to one output line
+struct GatherEntry {
+    int32_t slot;     // term slot within the launch chunk
+    int32_t w_row;    // adjoint: row of w_k (lead index) multiplying the line
+    int64_t t_off;    // double2 offset of the line inside the item's T buffer
+};
+
+// Everything one pipeline pass needs.  D in {2, 3}: axes 0..D-1, last axis is
+// the R2C/C2R axis (contiguous in memory, reference layout "last axis
+// fastest", grid_function.hpp:11-13).
+struct PassArgs {
+    int D;
+    int64_t dom_lo[3];
+    int32_t n[3];          // domain extents
+    int32_t P[3];          // FFT sizes (P[D-1] is the real axis)
+    int32_t W;             // padded half-spectrum row: roundup(P_last/2+1, 4)
+    int64_t L;             // lines of the axis-0 pass: W (2D) or P1*W (3D)
+    int32_t nl_cols;       // spectrum tile width
+    const TermDesc* terms; // device
+    const int32_t* slots;  // device: term ids of this chunk
+    int32_t n_slots;
+    int32_t B;             // vectors in this call
+    int32_t global;        // 1: spectral accumulation over all slots (one T per vector)
+    int32_t accumulate;    // rows_inv: add into g instead of overwrite
+    const double* in;      // B x N input vectors (vector-major)
+    double* out;           // B x N output vectors
+    int64_t N;             // points per vector
+    double2* S;            // forward scratch, per item stride S_stride
+    int64_t S_stride;
+    double2* T;            // inverse scratch, per item stride T_stride
+    int64_t T_stride;
+    const double* w_pool;
+    const double* phi_pool;
+    double2* spec_pool;
+    const double2* tw;     // twiddle tables: length L at tw + (L - 8)
+    const TermDesc* gdesc; // global-mode pseudo term (s = dom_lo, o = [0,n))
+    const int64_t* line_ptr;      // rows_inv CSR over output lines
+    const GatherEntry* entries;
+    double scale;          // 1 / prod P
+};
+
+enum RowsFwdMode { RF_APPLY = 0, RF_ADJ = 1, RF_SPEC = 2 };
+enum ColsMode { CM_SPEC = 0, CM_APPLY_LOCAL = 1, CM_APPLY_GLOBAL = 2, CM_ADJ_LOCAL = 3, CM_ADJ_GLOBAL = 4 };
+enum MidMode { MM_FWD_APPLY = 0, MM_FWD_ADJ = 1, MM_FWD_SPEC = 2, MM_INV_APPLY = 3, MM_INV_ADJ = 4 };
+enum RowsInvMode { RI_APPLY = 0, RI_ADJ = 1 };
+
+// launchers (kernels.cu); return cudaGetLastError()
+cudaError_t launch_rows_fwd(const PassArgs& a, int mode, cudaStream_t st);
+cudaError_t launch_mid(const PassArgs& a, int mode, cudaStream_t st);
+cudaError_t launch_cols(const PassArgs& a, int mode, cudaStream_t st);
+cudaError_t launch_rows_inv(const PassArgs& a, int mode, int64_t n_lines, cudaStream_t st);
+int cols_tile_width(int P0);
+
+// entry / block gather (K6)
+struct EntryArgs {
+    int D;
+    int64_t dom_lo[3];
+    int32_t n[3];
+    const TermDesc* terms;
+    const double* w_pool;
+    const double* phi_pool;
+    int32_t bucket[3];          // bucket edge per axis
+    int32_t nb[3];              // buckets per axis
+    const int64_t* bucket_ptr;  // CSR over buckets (lexicographic)
+    const int32_t* bucket_terms;
+};
+cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, const int64_t* x, double* out,
+                           int32_t* bad, cudaStream_t st);
+cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
+                          const int32_t* bshape, double* out, int32_t* bad, cudaStream_t st);
+
+// estimator reductions (K5): per (box, probe) sums of (Yt - Y)^2 and Y^2
+cudaError_t launch_probe_sums(int D, const int32_t* n, int32_t nbox, const int64_t* box_lo, const int64_t* box_hi,
+                              int32_t q, const double* Yt, const double* Y, double* d2, double* y2, cudaStream_t st);
+
+cudaError_t launch_zero(double* p, int64_t n, cudaStream_t st);
+
+}  // namespace pcb

@@ -1,0 +1,109 @@
+"""ctypes binding of the C ABI (include/pcb/pcb.h) — the only way Python reaches the kernels.
+
+The product path has no fallback: if ``lib/libpcop_b200.so`` is missing, ``load()`` raises; if no
+sm_100 device is present, ``pcb_create`` fails with PCB_ECUDA.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "libpcop_b200.so")
+
+i32 = ctypes.c_int32
+i64 = ctypes.c_int64
+dbl = ctypes.c_double
+vp = ctypes.c_void_p
+P_i64 = ctypes.POINTER(i64)
+P_dbl = ctypes.POINTER(dbl)
+
+STATUS = {0: "PCB_OK", 1: "PCB_EINVAL", 2: "PCB_ENOMEM", 3: "PCB_ECUDA", 4: "PCB_ENCCL", 5: "PCB_EINTERNAL"}
+MODES = {"auto": 0, "global": 1, "local": 2}
+MODE_NAMES = {v: k for k, v in MODES.items()}
+
+# every symbol include/pcb/pcb.h declares
+EXPORTS = ["pcb_default_options", "pcb_last_error", "pcb_create", "pcb_destroy", "pcb_get_info", "pcb_apply_batch",
+           "pcb_apply_adjoint_batch", "pcb_apply_batch_dev", "pcb_apply_adjoint_batch_dev", "pcb_entries",
+           "pcb_blocks", "pcb_blocks_dev", "pcb_probe_estimate", "pcb_probe_estimate_dev", "pcb_launch_count",
+           "pcb_normal_fill", "pcb_uniform_int_fill"]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("device", i32), ("mode", i32), ("max_batch", i32), ("shard_rank", i32), ("shard_count", i32),
+                ("reserved", i32), ("scratch_bytes", i64)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("dim", i32), ("rank", i32), ("rank_active", i32), ("mode", i32), ("n_groups", i32),
+                ("fft_size", i32 * 3), ("n_points", i64), ("spectra_bytes", i64), ("device_bytes", i64),
+                ("bytes_per_vector", dbl), ("flops_per_vector", dbl), ("launches_per_batch", i32),
+                ("reserved", i32)]
+
+    def as_dict(self) -> dict:
+        return {"dim": self.dim, "rank": self.rank, "rank_active": self.rank_active,
+                "mode": MODE_NAMES.get(self.mode, self.mode), "n_groups": self.n_groups,
+                "fft_size": [self.fft_size[i] for i in range(self.dim)], "n_points": self.n_points,
+                "spectra_bytes": self.spectra_bytes, "device_bytes": self.device_bytes,
+                "bytes_per_vector": self.bytes_per_vector, "flops_per_vector": self.flops_per_vector,
+                "launches_per_batch": self.launches_per_batch}
+
+
+class PcbError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.msg = msg
+
+
+_lib = None
+
+
+def load():
+    """Load the in-tree library (built by ``__graft_entry__.build()`` / ``python -m paper_1805_06018_b200.build``)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise FileNotFoundError(f"{LIB_PATH} is not built; run `python -m paper_1805_06018_b200.build` "
+                                "(there is no CPU fallback for the apply path)")
+    L = ctypes.CDLL(LIB_PATH)
+    L.pcb_default_options.argtypes = [ctypes.POINTER(Options)]
+    L.pcb_default_options.restype = None
+    L.pcb_last_error.restype = ctypes.c_char_p
+    L.pcb_create.argtypes = [i32, P_i64, P_i64, i32, P_i64, P_i64, P_i64, ctypes.POINTER(vp), P_i64, P_i64,
+                             ctypes.POINTER(vp), ctypes.POINTER(Options), ctypes.POINTER(vp)]
+    L.pcb_destroy.argtypes = [vp]
+    L.pcb_get_info.argtypes = [vp, ctypes.POINTER(Info)]
+    for n in ("pcb_apply_batch", "pcb_apply_adjoint_batch"):
+        getattr(L, n).argtypes = [vp, i32, vp, vp]
+    for n in ("pcb_apply_batch_dev", "pcb_apply_adjoint_batch_dev"):
+        getattr(L, n).argtypes = [vp, i32, vp, vp, vp]
+    L.pcb_entries.argtypes = [vp, i64, vp, vp, vp]
+    L.pcb_blocks.argtypes = [vp, i32, vp, vp, P_i64, vp]
+    L.pcb_blocks_dev.argtypes = [vp, i32, vp, vp, P_i64, vp, vp]
+    L.pcb_probe_estimate.argtypes = [vp, i32, vp, vp, i32, vp, vp, vp, vp, P_dbl, P_dbl]
+    L.pcb_probe_estimate_dev.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, vp, P_dbl, P_dbl, vp]
+    L.pcb_launch_count.restype = ctypes.c_longlong
+    L.pcb_normal_fill.argtypes = [ctypes.c_uint64, i64, vp]
+    L.pcb_uniform_int_fill.argtypes = [ctypes.c_uint64, i64, i64, i64, vp]
+    for n in EXPORTS:
+        if n not in ("pcb_default_options", "pcb_last_error", "pcb_launch_count"):
+            getattr(L, n).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise PcbError(rc, load().pcb_last_error().decode())
+
+
+def default_options() -> Options:
+    o = Options()
+    load().pcb_default_options(ctypes.byref(o))
+    return o
+
+
+def launch_count() -> int:
+    return int(load().pcb_launch_count())

@@ -1,0 +1,221 @@
+"""Python mirror of ``pcop::ProductConvolutionOperator`` over the C ABI.
+
+Same names, argument meaning and error behaviour as the reference
+(proj/core/include/pcop/pc_operator.hpp:17-66):
+
+* ``ProductConvolutionOperator(domain, weights, impulses)`` — pc_operator.cpp:26-38
+  (``ValueError`` for a weight/impulse count mismatch, like std::invalid_argument);
+* ``apply(f)`` / ``apply_adjoint(f)`` — pc_operator.cpp:45-69 (``ValueError`` "shape mismatch");
+* ``entry(y, x)`` — pc_operator.cpp:84-96 (``ValueError`` "index outside the domain");
+* ``apply_batch`` / ``apply_adjoint_batch`` — batched forms (fft_convolve_batch analogue, fft.cpp:164-181);
+* ``entries`` / ``blocks`` — vectorised entry gather for H-matrix conversion (hmatrix.cpp:138-150);
+* ``probe_estimate`` — the randomized estimator's adjoint samples and eta (adaptivity.cpp:75-121).
+
+All compute runs in the sm_100a kernels of ``lib/libpcop_b200.so``; numpy arrays are host
+buffers, and the ``*_dev`` methods take device pointers (e.g. ``torch.Tensor.data_ptr()``).
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Iterable, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import lib as _L
+
+
+def _i64arr(vals) -> ctypes.Array:
+    vals = [int(v) for v in vals]
+    return (_L.i64 * max(1, len(vals)))(*vals)
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class ProductConvolutionOperator:
+    """Immutable assembled operator; kernels, spectra and scratch live on one B200."""
+
+    def __init__(self, domain: Tuple[Sequence[int], Sequence[int]], weights: Sequence, impulses: Sequence,
+                 points: Optional[Sequence[Sequence[int]]] = None, mode: str = "auto", max_batch: int = 16,
+                 shard: Tuple[int, int] = (0, 1), device: int = -1, scratch_bytes: int = 0):
+        """domain = (lo, hi) inclusive; weights / impulses: objects with ``.lo`` and ``.values``
+        (``inputs.Field``) or (lo, values) pairs."""
+        if len(weights) != len(impulses):
+            raise ValueError("PCOp: one weight per impulse required")
+        L = _L.load()
+        lo, hi = [int(v) for v in domain[0]], [int(v) for v in domain[1]]
+        self.dim = len(lo)
+        self.domain = (tuple(lo), tuple(hi))
+        self.shape = tuple(h - l + 1 for l, h in zip(lo, hi))
+        self.n_points = int(np.prod(self.shape))
+        r = len(weights)
+        self.rank = r
+
+        def unpack(f):
+            if hasattr(f, "values"):
+                return tuple(int(v) for v in f.lo), np.ascontiguousarray(f.values, dtype=np.float64)
+            return tuple(int(v) for v in f[0]), np.ascontiguousarray(f[1], dtype=np.float64)
+
+        keep = []
+        w_lo, w_hi, p_lo, p_hi, w_ptr, p_ptr = [], [], [], [], [], []
+        for w, e in zip(weights, impulses):
+            wl, wv = unpack(w)
+            el, ev = unpack(e)
+            if wv.ndim != self.dim or ev.ndim != self.dim:
+                raise ValueError("IndexBox: dim mismatch")
+            keep += [wv, ev]
+            w_lo += wl
+            w_hi += [l + s - 1 for l, s in zip(wl, wv.shape)]
+            p_lo += el
+            p_hi += [l + s - 1 for l, s in zip(el, ev.shape)]
+            w_ptr.append(wv.ctypes.data)
+            p_ptr.append(ev.ctypes.data)
+        pts = None
+        if points is not None:
+            pts = _i64arr([c for p in points for c in p])
+        opt = _L.default_options()
+        opt.mode = _L.MODES[mode]
+        opt.max_batch = int(max_batch)
+        opt.shard_rank, opt.shard_count = int(shard[0]), int(shard[1])
+        opt.device = int(device)
+        opt.scratch_bytes = int(scratch_bytes)
+        PP = _L.vp * max(1, r)
+        h = _L.vp()
+        rc = L.pcb_create(self.dim, _i64arr(lo), _i64arr(hi), r, pts, _i64arr(w_lo), _i64arr(w_hi),
+                          PP(*w_ptr), _i64arr(p_lo), _i64arr(p_hi), PP(*p_ptr), ctypes.byref(opt), ctypes.byref(h))
+        if rc == 1:
+            raise ValueError(L.pcb_last_error().decode())
+        _L.check(rc)
+        self._h = h
+        info = _L.Info()
+        _L.check(L.pcb_get_info(self._h, ctypes.byref(info)))
+        self.info = info.as_dict()
+
+    @classmethod
+    def from_inputs(cls, inp, **kw) -> "ProductConvolutionOperator":
+        return cls((inp.dom_lo, inp.dom_hi), inp.weights, inp.impulses, points=inp.points, **kw)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _L.load().pcb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # --- apply -------------------------------------------------------------
+    def _vecs(self, F, what: str) -> np.ndarray:
+        F = np.ascontiguousarray(F, dtype=np.float64)
+        if F.ndim == 1:
+            if F.size != self.n_points:
+                raise ValueError(f"PCOp::{what}: shape mismatch")
+            return F.reshape(1, -1)
+        F = F.reshape(F.shape[0], -1)
+        if F.shape[1] != self.n_points:
+            raise ValueError(f"PCOp::{what}: shape mismatch")
+        return F
+
+    def apply_batch(self, F: np.ndarray) -> np.ndarray:
+        F = self._vecs(F, "apply")
+        G = np.empty_like(F)
+        self._rc(_L.load().pcb_apply_batch(self._h, F.shape[0], _ptr(F), _ptr(G)))
+        return G
+
+    def apply_adjoint_batch(self, F: np.ndarray) -> np.ndarray:
+        F = self._vecs(F, "apply_adjoint")
+        G = np.empty_like(F)
+        self._rc(_L.load().pcb_apply_adjoint_batch(self._h, F.shape[0], _ptr(F), _ptr(G)))
+        return G
+
+    def apply(self, f: np.ndarray) -> np.ndarray:
+        f = np.asarray(f, dtype=np.float64)
+        if f.size != self.n_points:
+            raise ValueError("PCOp::apply: shape mismatch")
+        return self.apply_batch(f.reshape(1, -1))[0]
+
+    def apply_adjoint(self, f: np.ndarray) -> np.ndarray:
+        f = np.asarray(f, dtype=np.float64)
+        if f.size != self.n_points:
+            raise ValueError("PCOp::apply_adjoint: shape mismatch")
+        return self.apply_adjoint_batch(f.reshape(1, -1))[0]
+
+    def apply_batch_dev(self, B: int, dF: int, dG: int, stream: int = 0, adjoint: bool = False) -> None:
+        fn = _L.load().pcb_apply_adjoint_batch_dev if adjoint else _L.load().pcb_apply_batch_dev
+        self._rc(fn(self._h, int(B), dF, dG, stream or None))
+
+    # --- entries -----------------------------------------------------------
+    def entry(self, y: Sequence[int], x: Sequence[int]) -> float:
+        return float(self.entries(np.asarray([y]), np.asarray([x]))[0])
+
+    def entries(self, y: np.ndarray, x: np.ndarray) -> np.ndarray:
+        y = np.ascontiguousarray(y, dtype=np.int64).reshape(-1, self.dim)
+        x = np.ascontiguousarray(x, dtype=np.int64).reshape(-1, self.dim)
+        if y.shape != x.shape:
+            raise ValueError("entries: y and x must have the same count")
+        out = np.empty(y.shape[0])
+        self._rc(_L.load().pcb_entries(self._h, y.shape[0], _ptr(y), _ptr(x), _ptr(out)))
+        return out
+
+    def blocks(self, t_origin: np.ndarray, s_origin: np.ndarray, block_shape: Sequence[int]) -> np.ndarray:
+        t = np.ascontiguousarray(t_origin, dtype=np.int64).reshape(-1, self.dim)
+        s = np.ascontiguousarray(s_origin, dtype=np.int64).reshape(-1, self.dim)
+        bs = int(np.prod(block_shape))
+        out = np.empty((t.shape[0], bs, bs))
+        self._rc(_L.load().pcb_blocks(self._h, t.shape[0], _ptr(t), _ptr(s), _i64arr(block_shape), _ptr(out)))
+        return out
+
+    def blocks_dev(self, nblk: int, d_t: int, d_s: int, block_shape: Sequence[int], d_out: int, stream: int = 0):
+        self._rc(_L.load().pcb_blocks_dev(self._h, int(nblk), d_t, d_s, _i64arr(block_shape), d_out, stream or None))
+
+    # --- estimator ---------------------------------------------------------
+    def probe_estimate(self, Z: np.ndarray, Y: np.ndarray, leaves: Iterable = (), want_ytilde: bool = False):
+        Z = self._vecs(Z, "apply_adjoint")
+        Y = self._vecs(Y, "apply_adjoint")
+        leaves = list(leaves)
+        lo = np.ascontiguousarray([l for l, _ in leaves], dtype=np.int64).reshape(-1)
+        hi = np.ascontiguousarray([h for _, h in leaves], dtype=np.int64).reshape(-1)
+        cells = np.zeros(max(1, len(leaves)))
+        yt = np.empty_like(Z) if want_ytilde else None
+        ea, er = _L.dbl(), _L.dbl()
+        self._rc(_L.load().pcb_probe_estimate(self._h, Z.shape[0], _ptr(Z), _ptr(Y), len(leaves),
+                                              _ptr(lo) if len(leaves) else None, _ptr(hi) if len(leaves) else None,
+                                              _ptr(yt) if yt is not None else None, _ptr(cells),
+                                              ctypes.byref(ea), ctypes.byref(er)))
+        return yt, cells[: len(leaves)], ea.value, er.value
+
+    def probe_estimate_dev(self, q: int, dZ: int, dY: int, dYt: int, leaves: Iterable = (), stream: int = 0):
+        leaves = list(leaves)
+        lo = np.ascontiguousarray([l for l, _ in leaves], dtype=np.int64).reshape(-1)
+        hi = np.ascontiguousarray([h for _, h in leaves], dtype=np.int64).reshape(-1)
+        cells = np.zeros(max(1, len(leaves)))
+        ea, er = _L.dbl(), _L.dbl()
+        self._rc(_L.load().pcb_probe_estimate_dev(self._h, int(q), dZ, dY, dYt, len(leaves),
+                                                  _ptr(lo) if len(leaves) else None,
+                                                  _ptr(hi) if len(leaves) else None, _ptr(cells),
+                                                  ctypes.byref(ea), ctypes.byref(er), stream or None))
+        return cells[: len(leaves)], ea.value, er.value
+
+    # --- errors ------------------------------------------------------------
+    @staticmethod
+    def _rc(rc: int) -> None:
+        if rc == 1:
+            raise ValueError(_L.load().pcb_last_error().decode())
+        _L.check(rc)
+
+
+def normal_vectors(seed: int, count: int, n: int) -> np.ndarray:
+    """count x n draws of std::mt19937_64(seed) + std::normal_distribution<double> (adaptivity.cpp:19-23)."""
+    out = np.empty(count * n)
+    _L.check(_L.load().pcb_normal_fill(ctypes.c_uint64(seed), count * n, _ptr(out)))
+    return out.reshape(count, n)
+
+
+def uniform_ints(seed: int, lo: int, hi: int, count: int) -> np.ndarray:
+    """std::mt19937_64(seed) + std::uniform_int_distribution<int64_t>(lo, hi)."""
+    out = np.empty(count, dtype=np.int64)
+    _L.check(_L.load().pcb_uniform_int_fill(ctypes.c_uint64(seed), lo, hi, count, _ptr(out)))
+    return out
