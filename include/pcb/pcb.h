@@ -137,6 +137,14 @@ PCB_API pcb_status pcb_probe_estimate_dev(pcb_op* op, int32_t q, const double* d
 /* Number of kernels this library has launched in the process (all handles). */
 PCB_API long long pcb_launch_count(void);
 
+/* Per-kernel timing: between pcb_profile_begin and pcb_profile_end every
+ * kernel launch of this handle is bracketed by CUDA events on its launching
+ * stream.  pcb_profile_end returns, per kernel name (names: max_kernels x 32
+ * chars), the summed event time in ms and the launch count. */
+PCB_API pcb_status pcb_profile_begin(pcb_op* op);
+PCB_API pcb_status pcb_profile_end(pcb_op* op, int32_t max_kernels, char* names, double* ms_total,
+                                   int32_t* launches, int32_t* n_kernels);
+
 /* Host utilities reproducing the reference's random streams (libstdc++):
  * std::mt19937_64(seed) + std::normal_distribution<double>(0,1)
  * (adaptivity.cpp:19-23, test_pc_operator.cpp:13-18) and

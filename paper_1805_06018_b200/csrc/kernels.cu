@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_fwd(PassArgs a) {
     };
 
     // phase 1: gather the real line into shared memory as z[j] = (x[2j], x[2j+1])
+#pragma unroll 4
     for (int idx = threadIdx.x; idx < NL * N; idx += blockDim.x) {
         const int l = idx / N;
         const int p = idx - l * N;
@@ -344,43 +345,82 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
 
 // ---------------------------------------------------------------------------
 // rows_inv: C2R along the last axis for every T line contributing to one output
-// line (CSR, ascending k), cropped and accumulated in a fixed order.
+// line (CSR, ascending k), cropped and accumulated in a fixed order.  Entry
+// metadata is staged in shared memory per batch of NL lines; thread t owns the
+// output positions p = t mod blockDim, so contributions to one position are
+// added by one thread in ascending entry order (deterministic, no atomics).
 template <int N, int NL, int MODE>
 __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_inv(PassArgs a) {
     constexpr int R = FftCfg<N>::R;
     constexpr int RL = LastPos<N>::RL;
+    constexpr int NT = NL * FftCfg<N>::TPL;
+    constexpr int XS = 2 * N + 1;  // padded real line stride: conflict-free column writes
     extern __shared__ double2 buf[];
-    const int64_t line = blockIdx.x;
+    const int64_t aline = blockIdx.x;
     const int vec = blockIdx.y;
     const int D = a.D;
     const int ax = D - 1;
-    const int n_last = a.n[ax];
-    double* acc = reinterpret_cast<double*>(buf + smem_words<N, NL>());
-    double* xs = reinterpret_cast<double*>(buf);
-    for (int i = threadIdx.x; i < n_last; i += blockDim.x) acc[i] = 0.0;
-    const int64_t e_beg = a.line_ptr[line];
-    const int64_t e_end = a.line_ptr[line + 1];
+    const int64_t line = a.line_id[aline];
+    const int ulo = a.line_rng[2 * aline], uhi = a.line_rng[2 * aline + 1];
+    double* xs = reinterpret_cast<double*>(buf);  // NL x XS doubles <= smem_words double2
+    double* acc = reinterpret_cast<double*>(buf + smem_words<N, NL>());  // [ulo, uhi)
+    int* m_lo = reinterpret_cast<int*>(acc + a.n[ax]);
+    int* m_hi = m_lo + NL;
+    int* m_sh = m_hi + NL;
+    int64_t* m_w = reinterpret_cast<int64_t*>(m_sh + NL + (NL & 1));
+    int64_t* m_row = m_w + NL;
+    const int64_t e_beg = a.line_ptr[aline];
+    const int64_t e_end = a.line_ptr[aline + 1];
     const double2* twP = twtab(a.tw, 2 * N);
     const int l = threadIdx.x % NL;
     const int tl = threadIdx.x / NL;
+    for (int i = ulo + threadIdx.x; i < uhi; i += NT) acc[i - ulo] = 0.0;
 
     for (int64_t e0 = e_beg; e0 < e_end; e0 += NL) {
+        const int ne = (int)((e_end - e0) < NL ? (e_end - e0) : NL);
         __syncthreads();
-        for (int idx = threadIdx.x; idx < NL * N; idx += blockDim.x) {
+        if (threadIdx.x < NL) {
+            const int ll = threadIdx.x;
+            int lo = 0, hi = 0, sh = 0;
+            int64_t wrow = -1, trow = -1;
+            if (ll < ne) {
+                const GatherEntry en = a.entries[e0 + ll];
+                const TermDesc& td = a.global ? *a.gdesc : a.terms[a.slots[en.slot]];
+                const int64_t it = a.global ? vec : (int64_t)en.slot * a.B + vec;
+                trow = it * a.T_stride + en.t_off;
+                if (MODE == RI_APPLY) {
+                    sh = (int)(td.s[ax] - a.dom_lo[ax]);  // v = p - sh in [o_lo, o_lo + o_cnt)
+                    lo = sh + td.o_lo[ax];
+                    hi = lo + td.o_cnt[ax];
+                } else {
+                    sh = (int)(td.x_lo[ax] - a.dom_lo[ax]);
+                    lo = sh;
+                    hi = sh + td.m[ax];
+                    wrow = td.w_off + (int64_t)en.w_row * td.m[ax];
+                }
+                lo = lo < ulo ? ulo : lo;
+                hi = hi > uhi ? uhi : hi;
+            }
+            m_lo[ll] = lo;
+            m_hi[ll] = hi;
+            m_sh[ll] = sh;
+            m_w[ll] = wrow;
+            m_row[ll] = trow;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int idx = threadIdx.x; idx < NL * N; idx += NT) {
             const int ll = idx / N;
             const int k = idx - ll * N;
-            const int64_t e = e0 + ll;
             double2 z = czero();
-            if (e < e_end) {
-                const GatherEntry en = a.entries[e];
-                const int64_t it = a.global ? vec : (int64_t)en.slot * a.B + vec;
-                const double2* row = a.T + it * a.T_stride + en.t_off;
+            if (ll < ne) {
+                const double2* row = a.T + m_row[ll];
                 const double2 xk = row[k];
                 const double2 xn = row[N - k];
-                const double2 E = make_double2(xk.x + xn.x, xk.y - xn.y);    // X[k] + conj X[N-k]
-                const double2 Dd = make_double2(xk.x - xn.x, xk.y + xn.y);   // X[k] - conj X[N-k]
-                const double2 O = cmulc(Dd, __ldg(&twP[k]));                 // * exp(+2 pi i k / P)
-                z = make_double2(E.x - O.y, E.y + O.x);                      // E + i O
+                const double2 E = make_double2(xk.x + xn.x, xk.y - xn.y);   // X[k] + conj X[N-k]
+                const double2 Dd = make_double2(xk.x - xn.x, xk.y + xn.y);  // X[k] - conj X[N-k]
+                const double2 O = cmulc(Dd, __ldg(&twP[k]));                // * exp(+2 pi i k / P)
+                z = make_double2(E.x - O.y, E.y + O.x);                     // E + i O
             }
             buf[sidx<NL, kPadShift>(k, ll)] = z;
         }
@@ -398,33 +438,25 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_inv(PassArgs a) {
 #pragma unroll
             for (int r = 0; r < RL; ++r) {
                 const int p = LastPos<N>::pos(tl, b, r);
-                xs[(int64_t)l * 2 * N + 2 * p] = v[b * RL + r].x;
-                xs[(int64_t)l * 2 * N + 2 * p + 1] = v[b * RL + r].y;
+                xs[l * XS + 2 * p] = v[b * RL + r].x;
+                xs[l * XS + 2 * p + 1] = v[b * RL + r].y;
             }
         __syncthreads();
-        const int ne = (int)((e_end - e0) < NL ? (e_end - e0) : NL);
-        for (int i = threadIdx.x; i < n_last; i += blockDim.x) {
-            double s = acc[i];
-            const int64_t yl = a.dom_lo[ax] + i;
-            for (int ll = 0; ll < ne; ++ll) {
-                const GatherEntry en = a.entries[e0 + ll];
-                const TermDesc& td = a.global ? *a.gdesc : a.terms[a.slots[en.slot]];
-                if (MODE == RI_APPLY) {
-                    const int64_t vv = yl - td.s[ax];
-                    if (vv >= td.o_lo[ax] && vv < td.o_lo[ax] + td.o_cnt[ax])
-                        s += xs[(int64_t)ll * 2 * N + vv] * a.scale;
-                } else {
-                    const int64_t u = yl - td.x_lo[ax];
-                    if (u >= 0 && u < td.m[ax])
-                        s += a.w_pool[td.w_off + (int64_t)en.w_row * td.m[ax] + u] * (xs[(int64_t)ll * 2 * N + u] * a.scale);
-                }
+        for (int ll = 0; ll < ne; ++ll) {
+            const int lo = m_lo[ll], hi = m_hi[ll];
+            const double* x = xs + ll * XS - m_sh[ll];
+            int p = lo + (int)((threadIdx.x + NT - (unsigned)(lo % NT)) % NT);
+            if (MODE == RI_APPLY) {
+                for (; p < hi; p += NT) acc[p - ulo] += x[p] * a.scale;
+            } else {
+                const double* w = a.w_pool + m_w[ll] - m_sh[ll];
+                for (; p < hi; p += NT) acc[p - ulo] += w[p] * (x[p] * a.scale);
             }
-            acc[i] = s;
         }
     }
     __syncthreads();
-    double* g = a.out + (int64_t)vec * a.N + line * n_last;
-    for (int i = threadIdx.x; i < n_last; i += blockDim.x) g[i] = a.accumulate ? g[i] + acc[i] : acc[i];
+    double* g = a.out + (int64_t)vec * a.N + line * a.n[ax];
+    for (int i = ulo + threadIdx.x; i < uhi; i += NT) g[i] = a.accumulate ? g[i] + acc[i - ulo] : acc[i - ulo];
 }
 
 // ---------------------------------------------------------------------------
@@ -568,8 +600,8 @@ cudaError_t launch_dyn(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_
 }
 
 template <int LEN>
-constexpr int rows_nl() {
-    return LEN >= 1024 ? 1 : (1024 / LEN > 16 ? 16 : 1024 / LEN);
+constexpr int rows_nl() {  // lines per CTA for the last-axis passes: ~128 threads
+    return LEN >= 2048 ? 1 : (2048 / LEN > 32 ? 32 : 2048 / LEN);
 }
 template <int P>
 constexpr int cols_nl() {
@@ -661,9 +693,11 @@ cudaError_t cols_mode(const PassArgs& a, cudaStream_t st) {
 
 template <int N, int MODE>
 cudaError_t rows_inv_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
-    constexpr int NL = rows_nl<N>() > 8 ? 8 : rows_nl<N>();
+    constexpr int NL = rows_nl<N>();
     dim3 grid((unsigned)n_lines, (unsigned)a.B);
-    const size_t smem = sizeof(double2) * smem_words<N, NL>() + sizeof(double) * (size_t)a.n[a.D - 1];
+    static_assert(NL * (2 * N + 1) <= 2 * smem_words<N, NL>(), "xs must fit the FFT buffer");
+    const size_t smem = sizeof(double2) * smem_words<N, NL>() + sizeof(double) * (size_t)a.n[a.D - 1] +
+                        (3 * NL + 1) * sizeof(int) + 2 * NL * sizeof(int64_t) + 16;
     return launch_dyn(k_rows_inv<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
 }
 

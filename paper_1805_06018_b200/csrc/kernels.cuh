@@ -65,7 +65,9 @@ struct PassArgs {
     double2* spec_pool;
     const double2* tw;     // twiddle tables: length L at tw + (L - 8)
     const TermDesc* gdesc; // global-mode pseudo term (s = dom_lo, o = [0,n))
-    const int64_t* line_ptr;      // rows_inv CSR over output lines
+    const int64_t* line_ptr;      // rows_inv CSR over the chunk's active output lines
+    const int64_t* line_id;       // output line of each active line
+    const int32_t* line_rng;      // [2*i], [2*i+1]: union of the entries' last-axis ranges
     const GatherEntry* entries;
     double scale;          // 1 / prod P
 };

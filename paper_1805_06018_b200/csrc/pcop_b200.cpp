@@ -108,11 +108,17 @@ struct HBox {
     bool empty = false;
 };
 
+struct Csr {  // rows_inv gather list over the active output lines of one chunk
+    int64_t n_lines = 0;
+    DevBuf<int64_t> ptr, ids;
+    DevBuf<int32_t> rng;
+    DevBuf<GatherEntry> en;
+};
+
 struct Chunk {
     int first = 0, count = 0;
     DevBuf<int32_t> slots;
-    DevBuf<int64_t> lp_apply, lp_adj;
-    DevBuf<GatherEntry> en_apply, en_adj;
+    Csr apply, adj;
 };
 
 struct Group {
@@ -162,6 +168,14 @@ struct pcb_op {
     pcb::DevBuf<int32_t> st_flag, st_shape;
     cudaStream_t stream = nullptr;
     pcb_info info{};
+    // per-kernel event profiling (pcb_profile_begin / pcb_profile_end)
+    bool prof = false;
+    struct Rec {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> ev_pool;
 };
 
 namespace pcb {
@@ -231,6 +245,31 @@ void launch_ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(PCB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+cudaEvent_t take_event(pcb_op* op) {
+    if (!op->ev_pool.empty()) {
+        cudaEvent_t e = op->ev_pool.back();
+        op->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    PCB_CK(cudaEventCreate(&e));
+    return e;
+}
+
+// launch with optional per-kernel CUDA-event bracketing on the launching stream
+template <typename Fn>
+void launch(pcb_op* op, cudaStream_t st, const char* what, Fn&& fn) {
+    if (!op->prof) {
+        launch_ck(fn(), what);
+        return;
+    }
+    cudaEvent_t a = take_event(op), b = take_event(op);
+    PCB_CK(cudaEventRecord(a, st));
+    launch_ck(fn(), what);
+    PCB_CK(cudaEventRecord(b, st));
+    op->recs.push_back({what, a, b});
+}
+
 // ---------------------------------------------------------------------------
 // planning
 
@@ -278,20 +317,54 @@ void build_csr(pcb_op* op, Group& g, Chunk& c, bool global) {
             ap[ln].push_back(e);
         }
     }
-    auto flatten = [&](std::vector<std::vector<GatherEntry>>& lists, DevBuf<int64_t>& lp, DevBuf<GatherEntry>& en) {
-        std::vector<int64_t> hp(n_lines + 1, 0);
+    // range of an entry along the last axis (domain-relative), for the per-line union
+    const int ax = D - 1;
+    auto rng_of = [&](const GatherEntry& e, bool adjoint, int& lo, int& hi) {
+        const TermDesc& t = global && !adjoint ? op->gdesc : op->terms[g.terms[c.first + e.slot]];
+        if (!adjoint) {
+            lo = (int)(t.s[ax] - op->dom_lo[ax]) + t.o_lo[ax];
+            hi = lo + t.o_cnt[ax];
+        } else {
+            lo = (int)(t.x_lo[ax] - op->dom_lo[ax]);
+            hi = lo + t.m[ax];
+        }
+        lo = std::max(lo, 0);
+        hi = std::min(hi, op->n[ax]);
+    };
+    auto flatten = [&](std::vector<std::vector<GatherEntry>>& lists, Csr& out, bool adjoint) {
+        std::vector<int64_t> hp, ids;
+        std::vector<int32_t> rg;
         std::vector<GatherEntry> he;
         for (int64_t ln = 0; ln < n_lines; ++ln) {
-            hp[ln] = (int64_t)he.size();
+            if (lists[ln].empty()) continue;
+            int ulo = INT32_MAX, uhi = INT32_MIN;
+            for (const GatherEntry& e : lists[ln]) {
+                int lo, hi;
+                rng_of(e, adjoint, lo, hi);
+                ulo = std::min(ulo, lo);
+                uhi = std::max(uhi, hi);
+            }
+            hp.push_back((int64_t)he.size());
+            ids.push_back(ln);
+            rg.push_back(ulo);
+            rg.push_back(std::max(ulo, uhi));
             he.insert(he.end(), lists[ln].begin(), lists[ln].end());
         }
-        hp[n_lines] = (int64_t)he.size();
-        lp.upload(hp);
+        hp.push_back((int64_t)he.size());
+        out.n_lines = (int64_t)ids.size();
+        out.ptr.upload(hp);
+        if (ids.empty()) {
+            ids.push_back(0);
+            rg.push_back(0);
+            rg.push_back(0);
+        }
         if (he.empty()) he.push_back(GatherEntry{});
-        en.upload(he);
+        out.ids.upload(ids);
+        out.rng.upload(rg);
+        out.en.upload(he);
     };
-    flatten(ap, c.lp_apply, c.en_apply);
-    flatten(ad, c.lp_adj, c.en_adj);
+    flatten(ap, c.apply, false);
+    flatten(ad, c.adj, true);
 }
 
 void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t r, const int64_t* w_lo,
@@ -722,14 +795,18 @@ void run_batch(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG
     const int D = op->D;
     const int64_t n_lines = D == 2 ? op->n[0] : (int64_t)op->n[0] * op->n[1];
     if (op->groups.empty()) {
-        launch_ck(launch_zero(dG, (int64_t)B * op->N, st), "zero");
+        launch(op, st, "zero", [&] { return launch_zero(dG, (int64_t)B * op->N, st); });
         return;
     }
+    const bool global = op->mode == PCB_MODE_GLOBAL;
     for (int b0 = 0; b0 < B;) {
-        bool first = true;
         int bmax = B - b0;
         for (const Group& g : op->groups) bmax = std::min(bmax, g.vb);
         const int bn = bmax;
+        // local mode (and every adjoint): rows_inv accumulates only the lines its terms touch
+        const bool zero_first = !global || adjoint;
+        if (zero_first)
+            PCB_CK(cudaMemsetAsync(dG + (int64_t)b0 * op->N, 0, (size_t)bn * op->N * sizeof(double), st));
         for (const Group& g : op->groups) {
             for (const Chunk& c : g.chunks) {
                 PassArgs a = base_args(op, g);
@@ -738,33 +815,39 @@ void run_batch(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG
                 a.B = bn;
                 a.in = dF + (int64_t)b0 * op->N;
                 a.out = dG + (int64_t)b0 * op->N;
-                a.accumulate = first ? 0 : 1;
-                const bool global = op->mode == PCB_MODE_GLOBAL;
+                a.accumulate = zero_first ? 1 : 0;
                 if (!adjoint) {
                     a.S_stride = g.S_apply;
                     a.T_stride = g.T_apply;
                     a.global = global;
-                    launch_ck(launch_rows_fwd(a, RF_APPLY, st), "rows_fwd(apply)");
-                    if (D == 3) launch_ck(launch_mid(a, MM_FWD_APPLY, st), "mid(fwd apply)");
-                    launch_ck(launch_cols(a, global ? CM_APPLY_GLOBAL : CM_APPLY_LOCAL, st), "cols(apply)");
-                    if (D == 3) launch_ck(launch_mid(a, MM_INV_APPLY, st), "mid(inv apply)");
-                    a.line_ptr = c.lp_apply.p;
-                    a.entries = c.en_apply.p;
-                    launch_ck(launch_rows_inv(a, RI_APPLY, n_lines, st), "rows_inv(apply)");
+                    launch(op, st, "rows_fwd(apply)", [&] { return launch_rows_fwd(a, RF_APPLY, st); });
+                    if (D == 3) launch(op, st, "mid(fwd apply)", [&] { return launch_mid(a, MM_FWD_APPLY, st); });
+                    launch(op, st, global ? "cols(apply,global)" : "cols(apply,local)", [&] { return launch_cols(a, global ? CM_APPLY_GLOBAL : CM_APPLY_LOCAL, st); });
+                    if (D == 3) launch(op, st, "mid(inv apply)", [&] { return launch_mid(a, MM_INV_APPLY, st); });
+                    a.line_ptr = c.apply.ptr.p;
+                    a.line_id = c.apply.ids.p;
+                    a.line_rng = c.apply.rng.p;
+                    a.entries = c.apply.en.p;
+                    if (c.apply.n_lines > 0)
+                        launch(op, st, "rows_inv(apply)",
+                               [&] { return launch_rows_inv(a, RI_APPLY, c.apply.n_lines, st); });
                 } else {
                     a.S_stride = g.S_adj;
                     a.T_stride = g.T_adj;
                     a.global = global;
-                    launch_ck(launch_rows_fwd(a, RF_ADJ, st), "rows_fwd(adjoint)");
-                    if (D == 3) launch_ck(launch_mid(a, MM_FWD_ADJ, st), "mid(fwd adjoint)");
-                    launch_ck(launch_cols(a, global ? CM_ADJ_GLOBAL : CM_ADJ_LOCAL, st), "cols(adjoint)");
+                    launch(op, st, "rows_fwd(adjoint)", [&] { return launch_rows_fwd(a, RF_ADJ, st); });
+                    if (D == 3) launch(op, st, "mid(fwd adjoint)", [&] { return launch_mid(a, MM_FWD_ADJ, st); });
+                    launch(op, st, global ? "cols(adjoint,global)" : "cols(adjoint,local)", [&] { return launch_cols(a, global ? CM_ADJ_GLOBAL : CM_ADJ_LOCAL, st); });
                     a.global = 0;
-                    if (D == 3) launch_ck(launch_mid(a, MM_INV_ADJ, st), "mid(inv adjoint)");
-                    a.line_ptr = c.lp_adj.p;
-                    a.entries = c.en_adj.p;
-                    launch_ck(launch_rows_inv(a, RI_ADJ, n_lines, st), "rows_inv(adjoint)");
+                    if (D == 3) launch(op, st, "mid(inv adjoint)", [&] { return launch_mid(a, MM_INV_ADJ, st); });
+                    a.line_ptr = c.adj.ptr.p;
+                    a.line_id = c.adj.ids.p;
+                    a.line_rng = c.adj.rng.p;
+                    a.entries = c.adj.en.p;
+                    if (c.adj.n_lines > 0)
+                        launch(op, st, "rows_inv(adjoint)",
+                               [&] { return launch_rows_inv(a, RI_ADJ, c.adj.n_lines, st); });
                 }
-                first = false;
             }
         }
         b0 += bn;
@@ -872,6 +955,11 @@ PCB_API pcb_status pcb_destroy(pcb_op* op) {
         cudaStreamSynchronize(op->stream);
         cudaStreamDestroy(op->stream);
     }
+    for (auto& r : op->recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : op->ev_pool) cudaEventDestroy(e);
     delete op;
     return PCB_OK;
 }
@@ -980,7 +1068,9 @@ static void blocks_common(pcb_op* op, int32_t nblk, const int64_t* d_t, const in
     op->st_flag.ensure(1);
     PCB_CK(cudaMemcpyAsync(op->st_shape.p, bs, sizeof(bs), cudaMemcpyHostToDevice, st));
     PCB_CK(cudaMemsetAsync(op->st_flag.p, 0, 4, st));
-    launch_ck(launch_blocks(entry_args(op), nblk, d_t, d_s, op->st_shape.p, d_out, op->st_flag.p, st), "blocks");
+    launch(op, st, "blocks", [&] {
+        return launch_blocks(entry_args(op), nblk, d_t, d_s, op->st_shape.p, d_out, op->st_flag.p, st);
+    });
     if (host_check) {
         int32_t bad = 0;
         PCB_CK(cudaMemcpyAsync(&bad, op->st_flag.p, 4, cudaMemcpyDeviceToHost, st));
@@ -1055,9 +1145,10 @@ static void estimate_common(pcb_op* op, int32_t q, const double* dZ, const doubl
         PCB_CK(cudaMemcpyAsync(op->st_i64a.p, blo.data(), blo.size() * 8, cudaMemcpyHostToDevice, st));
         PCB_CK(cudaMemcpyAsync(op->st_i64b.p, bhi.data(), bhi.size() * 8, cudaMemcpyHostToDevice, st));
     }
-    launch_ck(launch_probe_sums(op->D, op->n, nleaf, op->st_i64a.p, op->st_i64b.p, q, dYt, dY, op->st_aux.p,
-                                op->st_aux.p + nd2, st),
-              "probe_sums");
+    launch(op, st, "probe_sums", [&] {
+        return launch_probe_sums(op->D, op->n, nleaf, op->st_i64a.p, op->st_i64b.p, q, dYt, dY, op->st_aux.p,
+                                 op->st_aux.p + nd2, st);
+    });
     std::vector<double> h(nd2 + q);
     PCB_CK(cudaMemcpyAsync(h.data(), op->st_aux.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
     PCB_CK(cudaStreamSynchronize(st));
@@ -1114,6 +1205,51 @@ PCB_API pcb_status pcb_probe_estimate_dev(pcb_op* op, int32_t q, const double* d
         set_device(op);
         estimate_common(op, q, dZ, dY, dYt, nleaf, leaf_lo, leaf_hi, eta_cells, eta_abs, eta_rel,
                         (cudaStream_t)stream);
+    });
+}
+
+PCB_API pcb_status pcb_profile_begin(pcb_op* op) {
+    if (!op) {
+        set_err("null handle");
+        return PCB_EINVAL;
+    }
+    std::lock_guard<std::mutex> lk(op->mu);
+    op->prof = true;
+    return PCB_OK;
+}
+
+PCB_API pcb_status pcb_profile_end(pcb_op* op, int32_t max_kernels, char* names, double* ms_total, int32_t* launches,
+                                   int32_t* n_kernels) {
+    if (!op || !n_kernels) {
+        set_err("null argument");
+        return PCB_EINVAL;
+    }
+    std::lock_guard<std::mutex> lk(op->mu);
+    return guarded([&] {
+        set_device(op);
+        std::vector<std::string> order;
+        std::map<std::string, std::pair<double, int>> acc;
+        for (auto& r : op->recs) {
+            PCB_CK(cudaEventSynchronize(r.b));
+            float ms = 0.f;
+            PCB_CK(cudaEventElapsedTime(&ms, r.a, r.b));
+            if (!acc.count(r.name)) order.push_back(r.name);
+            acc[r.name].first += ms;
+            acc[r.name].second += 1;
+            op->ev_pool.push_back(r.a);
+            op->ev_pool.push_back(r.b);
+        }
+        op->recs.clear();
+        op->prof = false;
+        *n_kernels = (int32_t)order.size();
+        for (int32_t i = 0; i < (int32_t)order.size() && i < max_kernels; ++i) {
+            if (names) {
+                std::memset(names + 32 * i, 0, 32);
+                std::strncpy(names + 32 * i, order[i].c_str(), 31);
+            }
+            if (ms_total) ms_total[i] = acc[order[i]].first;
+            if (launches) launches[i] = acc[order[i]].second;
+        }
     });
 }
 

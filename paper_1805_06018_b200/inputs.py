@@ -36,7 +36,7 @@ from __future__ import annotations
 
 import math
 from dataclasses import dataclass, field
-from typing import Callable, List, Sequence, Tuple
+from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -314,7 +314,7 @@ def extend_lattice_impulse(blur: BlurSpec, dom_lo, dom_hi, nodes, k: int, full_b
 
 
 def lattice_operator(name: str, blur: BlurSpec, nodes: Sequence[Sequence[int]], full_box: bool = False,
-                     extend: bool = True) -> OperatorInputs:
+                     extend: bool = True, ks: Optional[Sequence[int]] = None) -> OperatorInputs:
     d = blur.dim
     n = blur.n
     dom_lo = (0,) * d
@@ -322,7 +322,7 @@ def lattice_operator(name: str, blur: BlurSpec, nodes: Sequence[Sequence[int]], 
     pts = lattice_points(nodes)
     sizes = [len(a) for a in nodes]
     weights, imps = [], []
-    for k in range(len(pts)):
+    for k in (range(len(pts)) if ks is None else ks):
         idx = lattice_index(nodes, k)
         weights.append(tent_weight(nodes, idx))
         if extend:
@@ -332,6 +332,8 @@ def lattice_operator(name: str, blur: BlurSpec, nodes: Sequence[Sequence[int]], 
             lo = tuple(dom_lo[a] - p[a] for a in range(d))
             hi = tuple(dom_hi[a] - p[a] for a in range(d))
             imps.append(Field(lo, impulse_on(blur, dom_lo, dom_hi, p, lo, hi)))
+    if ks is not None:
+        pts = [pts[k] for k in ks]
     return OperatorInputs(name, dom_lo, dom_hi, pts, weights, imps,
                           {"nodes": [list(a) for a in nodes], "lattice": sizes})
 
@@ -345,24 +347,26 @@ CONFIGS = {
     "c2": dict(desc="2D 512^2, r=64 (8x8 tents), sigma0=6, B=16, seed 1", B=16, seed=1),
     "c3": dict(desc="2D 1024^2, r=256 (graded 16x16 tents), anisotropic sigma, B=64 probes, seed 2", B=64, seed=2),
     "c4": dict(desc="3D 128^3, r=512 (8x8x8 tents), sigma=2(1+.5 sin sin), B=8, seed 4", B=8, seed=4),
+    "c5": dict(desc="c2 operator, 4096 dense 8x8-patch blocks (64x64), origins mt19937_64(3) in [0,504]", B=0, seed=3),
 }
 
 
-def make_config(name: str, full_box: bool = False) -> OperatorInputs:
-    if name == "c1":
-        nodes = [uniform_nodes(128, 3)] * 2
-        op = lattice_operator("c1", blur_c1(128, 3.0), nodes, full_box)
-    elif name == "c2":
-        nodes = [uniform_nodes(512, 7)] * 2
-        op = lattice_operator("c2", blur_c1(512, 6.0), nodes, full_box)
-    elif name == "c3":
-        nodes = [graded_nodes(1024, 10, 5)] * 2
-        op = lattice_operator("c3", blur_c3(1024), nodes, full_box)
-    elif name == "c4":
-        nodes = [uniform_nodes(128, 7)] * 3
-        op = lattice_operator("c4", blur_c4(128), nodes, full_box)
-    else:
-        raise ValueError(f"unknown config {name!r}")
+def config_spec(name: str):
+    """(blur, nodes) of a BASELINE.json configuration."""
+    if name in ("c1",):
+        return blur_c1(128, 3.0), [uniform_nodes(128, 3)] * 2
+    if name in ("c2", "c5"):
+        return blur_c1(512, 6.0), [uniform_nodes(512, 7)] * 2
+    if name == "c3":
+        return blur_c3(1024), [graded_nodes(1024, 10, 5)] * 2
+    if name == "c4":
+        return blur_c4(128), [uniform_nodes(128, 7)] * 3
+    raise ValueError(f"unknown config {name!r}")
+
+
+def make_config(name: str, full_box: bool = False, ks: Optional[Sequence[int]] = None) -> OperatorInputs:
+    blur, nodes = config_spec(name)
+    op = lattice_operator(name, blur, nodes, full_box, ks=ks)
     op.meta.update(CONFIGS[name])
     return op
 

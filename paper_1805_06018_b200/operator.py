@@ -199,6 +199,24 @@ class ProductConvolutionOperator:
                                                   ctypes.byref(ea), ctypes.byref(er), stream or None))
         return cells[: len(leaves)], ea.value, er.value
 
+    # --- per-kernel profile ------------------------------------------------
+    def profile_begin(self) -> None:
+        _L.check(_L.load().pcb_profile_begin(self._h))
+
+    def profile_end(self) -> dict:
+        """{kernel name: (total ms, launches)} for launches since profile_begin (CUDA events)."""
+        mx = 64
+        names = ctypes.create_string_buffer(32 * mx)
+        ms = np.zeros(mx)
+        cnt = np.zeros(mx, dtype=np.int32)
+        n = _L.i32()
+        _L.check(_L.load().pcb_profile_end(self._h, mx, names, _ptr(ms), _ptr(cnt), ctypes.byref(n)))
+        out = {}
+        for i in range(min(n.value, mx)):
+            nm = names.raw[32 * i: 32 * (i + 1)].split(b"\0", 1)[0].decode()
+            out[nm] = (float(ms[i]), int(cnt[i]))
+        return out
+
     # --- errors ------------------------------------------------------------
     @staticmethod
     def _rc(rc: int) -> None:
