@@ -109,10 +109,11 @@ def fft_convolve(psi: GF, f: GF) -> GF:
     if psi.values.size == 0 or f.values.size == 0:
         raise ValueError("fft_convolve: empty input")  # fft.cpp:146
     shape = conv_padded_shape(psi.box, f.box)
-    A = np.fft.fftn(psi.values, s=shape)
-    B = np.fft.fftn(f.values, s=shape)
+    axes = list(range(len(shape)))
+    A = np.fft.fftn(psi.values, s=shape, axes=axes)
+    B = np.fft.fftn(f.values, s=shape, axes=axes)
     out_box = minkowski_sum(psi.box, f.box)
-    full = np.fft.ifftn(A * B).real
+    full = np.fft.ifftn(A * B, axes=axes).real
     return GF(out_box[0], full[tuple(slice(0, h - l + 1) for l, h in zip(*out_box))].copy())
 
 

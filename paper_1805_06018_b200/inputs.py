@@ -85,6 +85,19 @@ class OperatorInputs:
     def rank(self) -> int:
         return len(self.weights)
 
+    def checksum(self) -> str:
+        """sha256 over the domain, boxes and values (pins golden fixtures to their inputs)."""
+        import hashlib
+
+        h = hashlib.sha256()
+        h.update(repr((tuple(self.dom_lo), tuple(self.dom_hi))).encode())
+        for w, e in zip(self.weights, self.impulses):
+            h.update(repr(tuple(w.lo)).encode())
+            h.update(np.ascontiguousarray(w.values).tobytes())
+            h.update(repr(tuple(e.lo)).encode())
+            h.update(np.ascontiguousarray(e.values).tobytes())
+        return h.hexdigest()
+
     def subset(self, ks: Sequence[int]) -> "OperatorInputs":
         return OperatorInputs(self.name, self.dom_lo, self.dom_hi, [self.points[k] for k in ks],
                               [self.weights[k] for k in ks], [self.impulses[k] for k in ks],

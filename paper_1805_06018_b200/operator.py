@@ -114,7 +114,7 @@ class ProductConvolutionOperator:
             if F.size != self.n_points:
                 raise ValueError(f"PCOp::{what}: shape mismatch")
             return F.reshape(1, -1)
-        F = F.reshape(F.shape[0], -1)
+        F = F.reshape(F.shape[0], -1) if F.shape[0] > 0 else F.reshape(0, int(np.prod(F.shape[1:])))
         if F.shape[1] != self.n_points:
             raise ValueError(f"PCOp::{what}: shape mismatch")
         return F

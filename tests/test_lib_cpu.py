@@ -1,0 +1,94 @@
+"""The C-ABI library without a GPU: it builds, loads, exports every declared symbol, has no CPU
+fallback, and its host utilities reproduce the reference's random streams."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    with open(os.path.join(ROOT, "include", "pcb", "pcb.h")) as f:
+        src = f.read()
+    return sorted(set(re.findall(r"PCB_API\s+[\w\s\*]+?\b(pcb_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ["pcb_create", "pcb_destroy", "pcb_apply_batch", "pcb_apply_adjoint_batch", "pcb_entries",
+              "pcb_blocks", "pcb_probe_estimate", "pcb_last_error"]:
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(pcb_lib):
+    from paper_1805_06018_b200 import lib
+
+    for s in declared_symbols():
+        assert hasattr(pcb_lib, s), f"{s} declared in include/pcb/pcb.h but not exported"
+    assert sorted(lib.EXPORTS) == declared_symbols()
+
+
+def test_shared_object_is_sm100a(pcb_lib):
+    import subprocess
+
+    from paper_1805_06018_b200 import lib
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_cpu_fallback(pcb_lib):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    from paper_1805_06018_b200 import inputs, lib
+    from paper_1805_06018_b200.operator import ProductConvolutionOperator
+
+    with pytest.raises(lib.PcbError) as e:
+        ProductConvolutionOperator.from_inputs(inputs.small_lattice(n=12, m=2))
+    assert e.value.code == 3  # PCB_ECUDA
+    assert "no CPU fallback" in e.value.msg
+
+
+def test_count_mismatch_is_invalid_argument(pcb_lib):  # pc_operator.cpp:34-35
+    from paper_1805_06018_b200 import inputs
+    from paper_1805_06018_b200.operator import ProductConvolutionOperator
+
+    inp = inputs.small_lattice(n=12, m=2)
+    with pytest.raises(ValueError, match="one weight per impulse"):
+        ProductConvolutionOperator((inp.dom_lo, inp.dom_hi), inp.weights, inp.impulses[:-1])
+
+
+def test_normal_fill_is_the_reference_stream(pcb_lib):
+    """std::mt19937_64 + std::normal_distribution<double> (adaptivity.cpp:19-23): deterministic,
+    vector b = draws [bN, (b+1)N); first values pinned (libstdc++ polar method)."""
+    from paper_1805_06018_b200.operator import normal_vectors
+
+    a = normal_vectors(0, 2, 5)
+    b = normal_vectors(0, 1, 10).reshape(2, 5)
+    assert np.array_equal(a, b)
+    assert np.allclose(a[0], [0.10191856, -0.48132337, -0.68060303, 0.06498795, -1.09611891], atol=1e-8)
+    assert abs(normal_vectors(1, 1, 200000).std() - 1.0) < 0.01
+
+
+def test_uniform_int_fill_range(pcb_lib):
+    from paper_1805_06018_b200.operator import uniform_ints
+
+    v = uniform_ints(3, 0, 504, 4096 * 4)
+    assert v.min() >= 0 and v.max() <= 504
+    assert np.array_equal(v, uniform_ints(3, 0, 504, 4096 * 4))
+
+
+def test_bad_arguments_rejected_without_device(pcb_lib):
+    from paper_1805_06018_b200 import lib
+
+    L = lib.load()
+    assert L.pcb_normal_fill(ctypes.c_uint64(0), -1, None) == 1
+    assert L.pcb_uniform_int_fill(ctypes.c_uint64(0), 5, 1, 3, None) == 1
+    assert L.pcb_destroy(None) == 0
+    assert L.pcb_apply_batch(None, 1, None, None) == 1
