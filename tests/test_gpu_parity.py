@@ -283,3 +283,19 @@ def test_single_kernel_exactness_c1_geometry(gpu):
     for mode in MODES:
         op = ProductConvolutionOperator.from_inputs(inp, mode=mode)
         assert rel(op.apply(f), truth) <= 1e-12
+
+
+def test_cpp_host_example(gpu, tmp_path):
+    """The C++ host side (include/pcb/operator.hpp) linked against the in-tree library."""
+    import subprocess
+
+    from paper_1805_06018_b200 import lib
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "apply_example")
+    libdir = os.path.dirname(lib.LIB_PATH)
+    subprocess.run(["g++", "-std=c++17", "-O2", f"-I{root}/include", os.path.join(root, "tests", "cpp", "apply_example.cpp"),
+                    f"-L{libdir}", "-lpcop_b200", f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK" in r.stdout

@@ -92,3 +92,17 @@ def test_bad_arguments_rejected_without_device(pcb_lib):
     assert L.pcb_uniform_int_fill(ctypes.c_uint64(0), 5, 1, 3, None) == 1
     assert L.pcb_destroy(None) == 0
     assert L.pcb_apply_batch(None, 1, None, None) == 1
+
+
+def test_cpp_header_compiles():
+    """include/pcb/operator.hpp + pcb.h compile as plain C++17 and C (no CUDA headers needed)."""
+    import subprocess
+
+    src = os.path.join(ROOT, "tests", "cpp", "apply_example.cpp")
+    r = subprocess.run(["g++", "-std=c++17", "-fsyntax-only", "-Wall", "-Wextra", f"-I{ROOT}/include", src],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run(["gcc", "-std=c99", "-fsyntax-only", "-x", "c", f"-I{ROOT}/include", "-"],
+                       input='#include "pcb/pcb.h"\nint main(void){pcb_options o; pcb_default_options(&o); return 0;}\n',
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
