@@ -20,13 +20,18 @@ namespace pcb {
 
 namespace {
 
-constexpr int kPadShift = 4;  // one pad word per 16 shared-memory words
+// one pad word per 2^PSH shared-memory (16-byte) words: with lines interleaved [L][NL], a pass
+// that walks one line (k fastest) strides NL words, and NL + NL/2^PSH must be odd-ish for the
+// 8 lanes of a 128-bit quarter-warp to hit distinct bank groups (NL = 2, 4, 8: 2^3; 16: 2^4; 32: 2^5)
+constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
+template <int NL>
+constexpr int PSH = ilog2c(NL) > 3 ? ilog2c(NL) : 3;
 
 __device__ __forceinline__ const double2* twtab(const double2* tw, int len) { return tw + (len - 8); }
 
 template <int LEN, int NL>
 constexpr int smem_words() {
-    return SmemLine<LEN, NL, kPadShift>::WORDS;
+    return SmemLine<LEN, NL, PSH<NL>>::WORDS;
 }
 
 // number of lines of one item for the rows_fwd pass
@@ -42,14 +47,39 @@ __device__ __forceinline__ int64_t imod(int64_t a, int64_t p) {
 }
 
 // ---------------------------------------------------------------------------
+// async global -> shared copies (LDGSTS): the gathers below issue all their loads back to back
+// and wait once, instead of stalling on each dependent load.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+// ---------------------------------------------------------------------------
 // rows_fwd: R2C along the last axis (length P = 2N) via an N-point complex FFT
-// of z[j] = x[2j] + i x[2j+1] and the usual even/odd split.
+// of z[j] = x[2j] + i x[2j+1] and the usual even/odd split.  APPLY gathers
+// w_k . f on the footprint window, ADJ gathers g on the output window (both
+// staged through shared memory with cp.async), SPEC places the trimmed kernel.
 template <int N, int NL, int MODE>
 __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_fwd(PassArgs a) {
-    constexpr int TPL = FftCfg<N>::TPL;
     constexpr int R = FftCfg<N>::R;
     constexpr int RF = FirstPos<N>::RF;
+    constexpr int NT = NL * FftCfg<N>::TPL;
+    constexpr int PS = PSH<NL>;
     extern __shared__ double2 buf[];
+    // layout: buf [smem_words] | line meta
+    int64_t* m_src = reinterpret_cast<int64_t*>(buf + smem_words<N, NL>());
+    int64_t* m_row = m_src + NL;
+    int64_t* m_w = m_row + NL;
+    int* m_lo = reinterpret_cast<int*>(m_w + NL);  // valid positions [m_lo, m_hi) along the line
+    int* m_hi = m_lo + NL;
 
     const int item = blockIdx.y;
     const bool gmode = (MODE == RF_ADJ) && a.global;
@@ -60,71 +90,81 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_fwd(PassArgs a) {
     const int64_t nlines = rows_fwd_lines(a, td, MODE);
     const int64_t line0 = (int64_t)blockIdx.x * NL;
     if (line0 >= nlines) return;
-
     const int D = a.D;
     const int ax = D - 1;  // real axis
-    const int lead1 = D == 3 ? 1 : 0;
-    // per-line lead coordinates and S row offset
-    auto line_info = [&](int64_t line, int64_t& src_off, int64_t& s_row, int& aux) {
-        // aux: APPLY -> w row; ADJ -> unused; SPEC -> validity of lead (1 valid)
-        int64_t c0, c1 = 0;
-        if (MODE == RF_APPLY) {
-            if (D == 3) { c0 = line / td.m[1]; c1 = line % td.m[1]; } else { c0 = line; }
-            const int64_t x0 = td.x_lo[0] + c0 - a.dom_lo[0];
-            const int64_t x1 = D == 3 ? td.x_lo[1] + c1 - a.dom_lo[1] : 0;
-            src_off = (int64_t)vec * a.N + (D == 3 ? (x0 * a.n[1] + x1) * a.n[2] : x0 * a.n[1]) +
-                      (td.x_lo[ax] - a.dom_lo[ax]);
-            aux = (int)(D == 3 ? c0 * td.m[1] + c1 : c0);
-            s_row = D == 3 ? (c0 * a.P[1] + c1) * a.W : c0 * a.W;
-        } else if (MODE == RF_ADJ) {
-            int64_t v0, v1 = 0;
-            if (D == 3) { v0 = td.o_lo[0] + line / td.o_cnt[1]; v1 = td.o_lo[1] + line % td.o_cnt[1]; }
-            else { v0 = td.o_lo[0] + line; }
-            const int64_t y0 = td.s[0] + v0 - a.dom_lo[0];
-            const int64_t y1 = D == 3 ? td.s[1] + v1 - a.dom_lo[1] : 0;
-            src_off = (int64_t)vec * a.N + (D == 3 ? (y0 * a.n[1] + y1) * a.n[2] : y0 * a.n[1]) +
-                      (td.s[ax] - a.dom_lo[ax]);
-            aux = 0;
-            s_row = D == 3 ? ((v0 - td.o_lo[0]) * a.P[1] + v1) * a.W : (v0 - td.o_lo[0]) * a.W;
-        } else {
-            int64_t t0, t1 = 0;
-            if (D == 3) { t0 = line / a.P[1]; t1 = line % a.P[1]; } else { t0 = line; }
-            // z_a = k_lo + ((t + c - k_lo) mod P), c = s - x_lo
-            const int64_t z0 = imod(t0 + td.s[0] - td.x_lo[0] - td.k_lo[0], a.P[0]);
-            const int64_t z1 = D == 3 ? imod(t1 + td.s[1] - td.x_lo[1] - td.k_lo[1], a.P[1]) : 0;
-            aux = (z0 < td.k_ext[0] && (D == 2 || z1 < td.k_ext[1])) ? 1 : 0;
-            src_off = td.phi_off + (D == 3 ? (z0 * td.k_ext[1] + z1) * td.k_ext[2] : z0 * td.k_ext[1]);
-            s_row = D == 3 ? (t0 * a.P[1] + t1) * a.W : t0 * a.W;
-        }
-    };
 
-    // phase 1: gather the real line into shared memory as z[j] = (x[2j], x[2j+1])
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < NL * N; idx += blockDim.x) {
-        const int l = idx / N;
-        const int p = idx - l * N;
-        const int64_t line = line0 + l;
-        double2 z = czero();
+    // phase 0: per-line source / destination offsets
+    if (threadIdx.x < NL) {
+        const int ll = threadIdx.x;
+        const int64_t line = line0 + ll;
+        int64_t src = 0, row = -1, woff = 0;
+        int lo = 0, hi = 0;
         if (line < nlines) {
-            int64_t src_off, s_row;
-            int aux;
-            line_info(line, src_off, s_row, aux);
-            double xv[2] = {0.0, 0.0};
+            if (MODE == RF_APPLY) {
+                int64_t c0 = line, c1 = 0;
+                if (D == 3) { c0 = line / td.m[1]; c1 = line % td.m[1]; }
+                const int64_t x0 = td.x_lo[0] + c0 - a.dom_lo[0];
+                const int64_t x1 = D == 3 ? td.x_lo[1] + c1 - a.dom_lo[1] : 0;
+                src = (int64_t)vec * a.N + (D == 3 ? (x0 * a.n[1] + x1) * a.n[2] : x0 * a.n[1]) +
+                      (td.x_lo[ax] - a.dom_lo[ax]);
+                woff = td.w_off + (D == 3 ? c0 * td.m[1] + c1 : c0) * (int64_t)td.m[ax];
+                row = D == 3 ? (c0 * a.P[1] + c1) * a.W : c0 * a.W;
+                lo = 0;
+                hi = td.m[ax];
+            } else if (MODE == RF_ADJ) {
+                int64_t v0 = td.o_lo[0] + line, v1 = 0;
+                if (D == 3) { v0 = td.o_lo[0] + line / td.o_cnt[1]; v1 = td.o_lo[1] + line % td.o_cnt[1]; }
+                const int64_t y0 = td.s[0] + v0 - a.dom_lo[0];
+                const int64_t y1 = D == 3 ? td.s[1] + v1 - a.dom_lo[1] : 0;
+                src = (int64_t)vec * a.N + (D == 3 ? (y0 * a.n[1] + y1) * a.n[2] : y0 * a.n[1]) +
+                      (td.s[ax] - a.dom_lo[ax]);
+                row = D == 3 ? ((v0 - td.o_lo[0]) * a.P[1] + v1) * a.W : (v0 - td.o_lo[0]) * a.W;
+                lo = td.o_lo[ax];
+                hi = td.o_lo[ax] + td.o_cnt[ax];
+            } else {
+                int64_t t0 = line, t1 = 0;
+                if (D == 3) { t0 = line / a.P[1]; t1 = line % a.P[1]; }
+                // z_a = k_lo + ((t + c - k_lo) mod P), c = s - x_lo
+                const int64_t z0 = imod(t0 + td.s[0] - td.x_lo[0] - td.k_lo[0], a.P[0]);
+                const int64_t z1 = D == 3 ? imod(t1 + td.s[1] - td.x_lo[1] - td.k_lo[1], a.P[1]) : 0;
+                const bool ok = z0 < td.k_ext[0] && (D == 2 || z1 < td.k_ext[1]);
+                src = td.phi_off + (D == 3 ? (z0 * td.k_ext[1] + z1) * td.k_ext[2] : z0 * td.k_ext[1]);
+                row = D == 3 ? (t0 * a.P[1] + t1) * a.W : t0 * a.W;
+                lo = 0;
+                hi = ok ? 2 * N : 0;
+            }
+        }
+        m_src[ll] = src;
+        m_row[ll] = row;
+        m_w[ll] = woff;
+        m_lo[ll] = lo;
+        m_hi[ll] = hi;
+    }
+    __syncthreads();
+
+    // phase 1: z[j] = (x[2j], x[2j+1]) gathered straight into the interleaved FFT buffer
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < NL * N; idx += NT) {
+        const int ll = idx / N;
+        const int p = idx - ll * N;
+        const int lo = m_lo[ll], hi = m_hi[ll];
+        const int64_t src = m_src[ll];
+        double xv[2];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int u = 2 * p + h;
-                if (MODE == RF_APPLY) {
-                    if (u < td.m[ax]) xv[h] = a.in[src_off + u] * a.w_pool[td.w_off + (int64_t)aux * td.m[ax] + u];
-                } else if (MODE == RF_ADJ) {
-                    if (u >= td.o_lo[ax] && u < td.o_lo[ax] + td.o_cnt[ax]) xv[h] = a.in[src_off + u];
-                } else {
+        for (int h = 0; h < 2; ++h) {
+            const int u = 2 * p + h;
+            double x = 0.0;
+            if (u >= lo && u < hi) {
+                if (MODE == RF_APPLY) x = __ldg(&a.in[src + u]) * __ldg(&a.w_pool[m_w[ll] + u]);
+                else if (MODE == RF_ADJ) x = __ldg(&a.in[src + u]);
+                else {
                     const int64_t zl = imod(u + td.s[ax] - td.x_lo[ax] - td.k_lo[ax], a.P[ax]);
-                    if (aux && zl < td.k_ext[ax]) xv[h] = a.phi_pool[src_off + zl];
+                    if (zl < td.k_ext[ax]) x = a.phi_pool[src + zl];
                 }
             }
-            z = make_double2(xv[0], xv[1]);
+            xv[h] = x;
         }
-        buf[sidx<NL, kPadShift>(p, l)] = z;
+        buf[sidx<NL, PS>(p, ll)] = make_double2(xv[0], xv[1]);
     }
     __syncthreads();
 
@@ -134,32 +174,29 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_fwd(PassArgs a) {
 #pragma unroll
     for (int b = 0; b < R / RF; ++b)
 #pragma unroll
-        for (int r = 0; r < RF; ++r) v[b * RF + r] = buf[sidx<NL, kPadShift>(FirstPos<N>::pos(tl, b, r), l)];
-    fft_fwd_order<N, -1, NL, kPadShift>(v, buf, l, tl, twtab(a.tw, N));
+        for (int r = 0; r < RF; ++r) v[b * RF + r] = buf[sidx<NL, PS>(FirstPos<N>::pos(tl, b, r), l)];
+    fft_fwd_order<N, -1, NL, PS>(v, buf, l, tl, twtab(a.tw, N));
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int pos = N >= 16 ? tl + r * (N / 16) : r;
-        buf[sidx<NL, kPadShift>(pos, l)] = v[r];
+        buf[sidx<NL, PS>(pos, l)] = v[r];
     }
     __syncthreads();
 
     // phase 3: even/odd split X[k] = A[k] + W^k B[k], k = 0..N
     const double2* twP = twtab(a.tw, 2 * N);
     double2* S_item = a.S + (int64_t)item * a.S_stride;
-    for (int idx = threadIdx.x; idx < NL * (N + 1); idx += blockDim.x) {
+    for (int idx = threadIdx.x; idx < NL * (N + 1); idx += NT) {
         const int ll = idx / (N + 1);
         const int k = idx - ll * (N + 1);
-        const int64_t line = line0 + ll;
-        if (line >= nlines) continue;
-        int64_t src_off, s_row;
-        int aux;
-        line_info(line, src_off, s_row, aux);
-        const double2 zk = buf[sidx<NL, kPadShift>(k & (N - 1), ll)];
-        const double2 zn = buf[sidx<NL, kPadShift>((N - k) & (N - 1), ll)];
+        const int64_t row = m_row[ll];
+        if (row < 0) continue;
+        const double2 zk = buf[sidx<NL, PS>(k & (N - 1), ll)];
+        const double2 zn = buf[sidx<NL, PS>((N - k) & (N - 1), ll)];
         const double2 A = make_double2(0.5 * (zk.x + zn.x), 0.5 * (zk.y - zn.y));
         const double2 Bm = make_double2(0.5 * (zk.y + zn.y), -0.5 * (zk.x - zn.x));  // (zk - conj zn)/(2i)
-        S_item[s_row + k] = cadd(A, cmul(__ldg(&twP[k]), Bm));
+        S_item[row + k] = cadd(A, cmul(__ldg(&twP[k]), Bm));
     }
 }
 
@@ -202,7 +239,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P1>::TPL) k_mid(PassArgs a) {
                 const int p = FirstPos<P1>::pos(tl, b, r);
                 v[b * RF + r] = (cvalid && p >= in_lo && p < in_lo + in_cnt) ? base[(int64_t)p * a.W] : czero();
             }
-        fft_fwd_order<P1, -1, NL, kPadShift>(v, buf, l, tl, twtab(a.tw, P1));
+        fft_fwd_order<P1, -1, NL, PSH<NL>>(v, buf, l, tl, twtab(a.tw, P1));
         if (cvalid) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -216,7 +253,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P1>::TPL) k_mid(PassArgs a) {
             const int pos = P1 >= 16 ? tl + r * (P1 / 16) : r;
             v[r] = cvalid ? base[(int64_t)pos * a.W] : czero();
         }
-        fft_rev_order<P1, +1, NL, kPadShift>(v, buf, l, tl, twtab(a.tw, P1));
+        fft_rev_order<P1, +1, NL, PSH<NL>>(v, buf, l, tl, twtab(a.tw, P1));
         if (cvalid) {
 #pragma unroll
             for (int b = 0; b < R / RL; ++b)
@@ -278,7 +315,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
         if (MODE == CM_SPEC) load_in(S_item, 0, P0, v);
         else if (MODE == CM_APPLY_LOCAL) load_in(S_item, 0, td.m[0], v);
         else load_in(S_item, td.o_lo[0], td.o_cnt[0], v);
-        fft_fwd_order<P0, -1, NL, kPadShift>(v, buf, l, tl, tw0);
+        fft_fwd_order<P0, -1, NL, PSH<NL>>(v, buf, l, tl, tw0);
         double2* spec = a.spec_pool + td.spec_off + tile_off;
         if (MODE == CM_SPEC) {
             if (cvalid) {
@@ -292,7 +329,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
             const double2 ph = cvalid ? __ldg(&spec[(int64_t)fpos(r) * NL]) : czero();
             v[r] = MODE == CM_APPLY_LOCAL ? cmul(v[r], ph) : cmulc(v[r], ph);
         }
-        fft_rev_order<P0, +1, NL, kPadShift>(v, buf, l, tl, tw0);
+        fft_rev_order<P0, +1, NL, PSH<NL>>(v, buf, l, tl, tw0);
         double2* T_item = a.T + (int64_t)item * a.T_stride;
         if (MODE == CM_APPLY_LOCAL) store_out(T_item, td.o_lo[0], td.o_cnt[0], v);
         else store_out(T_item, 0, td.m[0], v);
@@ -308,7 +345,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
             const TermDesc& td = a.terms[a.slots[slot]];
             const double2* S_item = a.S + ((int64_t)slot * a.B + vec) * a.S_stride;
             load_in(S_item, 0, td.m[0], v);
-            fft_fwd_order<P0, -1, NL, kPadShift>(v, buf, l, tl, tw0);
+            fft_fwd_order<P0, -1, NL, PSH<NL>>(v, buf, l, tl, tw0);
             const double2* spec = a.spec_pool + td.spec_off + tile_off;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -316,7 +353,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
                 acc[r] = cadd(acc[r], cmul(v[r], ph));
             }
         }
-        fft_rev_order<P0, +1, NL, kPadShift>(acc, buf, l, tl, tw0);
+        fft_rev_order<P0, +1, NL, PSH<NL>>(acc, buf, l, tl, tw0);
         const TermDesc& g = *a.gdesc;
         store_out(a.T + (int64_t)vec * a.T_stride, g.o_lo[0], g.o_cnt[0], acc);
         return;
@@ -328,7 +365,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
         const TermDesc& g = *a.gdesc;
         double2 x[R];
         load_in(a.S + (int64_t)vec * a.S_stride, g.o_lo[0], g.o_cnt[0], x);
-        fft_fwd_order<P0, -1, NL, kPadShift>(x, buf, l, tl, tw0);
+        fft_fwd_order<P0, -1, NL, PSH<NL>>(x, buf, l, tl, tw0);
         for (int slot = 0; slot < a.n_slots; ++slot) {
             const TermDesc& td = a.terms[a.slots[slot]];
             const double2* spec = a.spec_pool + td.spec_off + tile_off;
@@ -337,7 +374,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
                 const double2 ph = cvalid ? __ldg(&spec[(int64_t)fpos(r) * NL]) : czero();
                 v[r] = cmulc(x[r], ph);
             }
-            fft_rev_order<P0, +1, NL, kPadShift>(v, buf, l, tl, tw0);
+            fft_rev_order<P0, +1, NL, PSH<NL>>(v, buf, l, tl, tw0);
             store_out(a.T + ((int64_t)slot * a.B + vec) * a.T_stride, 0, td.m[0], v);
         }
     }
@@ -362,8 +399,12 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_inv(PassArgs a) {
     const int ax = D - 1;
     const int64_t line = a.line_id[aline];
     const int ulo = a.line_rng[2 * aline], uhi = a.line_rng[2 * aline + 1];
+    // layout: buf [smem_words] (FFT; reused as xs) | stage [NL][N+1] | acc [n_last] | meta
     double* xs = reinterpret_cast<double*>(buf);  // NL x XS doubles <= smem_words double2
-    double* acc = reinterpret_cast<double*>(buf + smem_words<N, NL>());  // [ulo, uhi)
+    constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
+                                                                          : (NL * (2 * N + 1) + 1) / 2;
+    double2* stage = buf + BUFW;
+    double* acc = reinterpret_cast<double*>(stage + NL * (N + 1));  // [ulo, uhi)
     int* m_lo = reinterpret_cast<int*>(acc + a.n[ax]);
     int* m_hi = m_lo + NL;
     int* m_sh = m_hi + NL;
@@ -408,30 +449,36 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_inv(PassArgs a) {
             m_row[ll] = trow;
         }
         __syncthreads();
-#pragma unroll 4
+        // stage the NL half-spectrum rows (N+1 complex each) with async copies
+        for (int idx = threadIdx.x; idx < ne * (N + 1); idx += NT) {
+            const int ll = idx / (N + 1);
+            const int k = idx - ll * (N + 1);
+            cp_async16(&stage[idx], a.T + m_row[ll] + k);
+        }
+        cp_async_wait_all();
+        __syncthreads();
         for (int idx = threadIdx.x; idx < NL * N; idx += NT) {
             const int ll = idx / N;
             const int k = idx - ll * N;
             double2 z = czero();
             if (ll < ne) {
-                const double2* row = a.T + m_row[ll];
-                const double2 xk = row[k];
-                const double2 xn = row[N - k];
+                const double2 xk = stage[ll * (N + 1) + k];
+                const double2 xn = stage[ll * (N + 1) + N - k];
                 const double2 E = make_double2(xk.x + xn.x, xk.y - xn.y);   // X[k] + conj X[N-k]
                 const double2 Dd = make_double2(xk.x - xn.x, xk.y + xn.y);  // X[k] - conj X[N-k]
                 const double2 O = cmulc(Dd, __ldg(&twP[k]));                // * exp(+2 pi i k / P)
                 z = make_double2(E.x - O.y, E.y + O.x);                     // E + i O
             }
-            buf[sidx<NL, kPadShift>(k, ll)] = z;
+            buf[sidx<NL, PSH<NL>>(k, ll)] = z;
         }
         __syncthreads();
         double2 v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int pos = N >= 16 ? tl + r * (N / 16) : r;
-            v[r] = buf[sidx<NL, kPadShift>(pos, l)];
+            v[r] = buf[sidx<NL, PSH<NL>>(pos, l)];
         }
-        fft_rev_order<N, +1, NL, kPadShift>(v, buf, l, tl, twtab(a.tw, N));
+        fft_rev_order<N, +1, NL, PSH<NL>>(v, buf, l, tl, twtab(a.tw, N));
         __syncthreads();
 #pragma unroll
         for (int b = 0; b < R / RL; ++b)
@@ -618,7 +665,7 @@ cudaError_t rows_fwd_n(const PassArgs& a, cudaStream_t st) {
     if (MODE != RF_SPEC) maxlines = a.D == 2 ? a.P[0] : (int64_t)a.P[0] * a.P[1];
     const int items = (MODE == RF_ADJ && a.global) ? a.B : a.n_slots * (MODE == RF_SPEC ? 1 : a.B);
     dim3 grid((unsigned)((maxlines + NL - 1) / NL), (unsigned)items);
-    const size_t smem = sizeof(double2) * smem_words<N, NL>();
+    const size_t smem = sizeof(double2) * smem_words<N, NL>() + NL * (3 * sizeof(int64_t) + 2 * sizeof(int));
     return launch_dyn(k_rows_fwd<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
 }
 
@@ -695,9 +742,11 @@ template <int N, int MODE>
 cudaError_t rows_inv_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
     constexpr int NL = rows_nl<N>();
     dim3 grid((unsigned)n_lines, (unsigned)a.B);
-    static_assert(NL * (2 * N + 1) <= 2 * smem_words<N, NL>(), "xs must fit the FFT buffer");
-    const size_t smem = sizeof(double2) * smem_words<N, NL>() + sizeof(double) * (size_t)a.n[a.D - 1] +
-                        (3 * NL + 1) * sizeof(int) + 2 * NL * sizeof(int64_t) + 16;
+    constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
+                                                                          : (NL * (2 * N + 1) + 1) / 2;
+    const size_t smem = sizeof(double2) * (BUFW + NL * (N + 1)) +
+                        sizeof(double) * (size_t)a.n[a.D - 1] + (3 * NL + 1) * sizeof(int) +
+                        2 * NL * sizeof(int64_t) + 16;
     return launch_dyn(k_rows_inv<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
 }
 

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -157,7 +158,10 @@ struct pcb_op {
     pcb::DevBuf<double> w_pool, phi_pool;
     pcb::DevBuf<double2> spec_pool, tw;
     std::vector<pcb::Group> groups;
-    pcb::DevBuf<double2> S, T;
+    pcb::DevBuf<double2> S, T, T2;  // T2: second inverse buffer of the two-stream local pipeline
+    cudaStream_t sA = nullptr, sB = nullptr;
+    bool pipeline = false;  // two-stream local pipeline (PCB_PIPELINE=1 enables; measured no gain on c3)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_cols[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
     // entry gather
     int32_t bucket[3] = {1, 1, 1}, nb[3] = {1, 1, 1};
     pcb::DevBuf<int64_t> bucket_ptr;
@@ -651,8 +655,11 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             g.S_adj = (int64_t)g.o0max * plane;
             g.T_adj = (int64_t)g.m0max * plane;
             const int64_t per_item = 16 * (std::max(g.S_apply, g.S_adj) + std::max(g.T_apply, g.T_adj));
-            int per_chunk = (int)std::max<int64_t>(1, budget / std::max<int64_t>(1, per_item * mb));
+            int per_chunk = (int)std::max<int64_t>(1, budget / std::max<int64_t>(1, (op->pipeline ? 2 : 1) * per_item * mb));
             per_chunk = std::min<int>(per_chunk, std::max(1, 65535 / mb));
+            // at least two chunks per group so the two-stream pipeline has something to overlap
+            if (op->pipeline) per_chunk = std::min<int>(per_chunk, std::max<int>(1, ((int)g.terms.size() + 1) / 2));
+            if (const char* e = getenv("PCB_CHUNK_TERMS")) per_chunk = std::max(1, atoi(e));
             g.vb = mb;
             for (int f = 0; f < (int)g.terms.size(); f += per_chunk) {
                 g.chunks.emplace_back();
@@ -685,6 +692,10 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     op->T.alloc((size_t)std::max<int64_t>(T_need, 1));
     PCB_CK(cudaMemset(op->S.p, 0, op->S.bytes()));
     PCB_CK(cudaMemset(op->T.p, 0, op->T.bytes()));
+    if (mode == PCB_MODE_LOCAL && op->pipeline) {
+        op->T2.alloc((size_t)std::max<int64_t>(T_need, 1));
+        PCB_CK(cudaMemset(op->T2.p, 0, op->T2.bytes()));
+    }
 
     // device descriptors and pools
     op->d_terms.upload(op->terms.empty() ? std::vector<TermDesc>(1) : op->terms);
@@ -790,68 +801,114 @@ void build_spectra(pcb_op* op) {
     }
 }
 
-// one apply / adjoint batch on device pointers
+// one apply / adjoint batch on device pointers.
+// GLOBAL: one chunk per vector block, on the caller's stream.
+// LOCAL: chunks of terms flow through a two-stream pipeline forked from the caller's stream:
+//   stream A: rows_fwd(i) -> [mid] -> cols(i) -> [mid_inv] (writes T[i % 2]) -> event cols[i % 2]
+//   stream B: wait cols[i % 2] -> rows_inv(i) (reads T[i % 2], accumulates into g) -> event done[i % 2]
+// stream A waits done[i % 2] before overwriting T[i % 2] again; rows_inv launches stay in chunk
+// order on stream B, so the accumulation order (and the result) is fixed.
 void run_batch(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG, cudaStream_t st) {
     const int D = op->D;
-    const int64_t n_lines = D == 2 ? op->n[0] : (int64_t)op->n[0] * op->n[1];
     if (op->groups.empty()) {
         launch(op, st, "zero", [&] { return launch_zero(dG, (int64_t)B * op->N, st); });
         return;
     }
     const bool global = op->mode == PCB_MODE_GLOBAL;
-    for (int b0 = 0; b0 < B;) {
-        int bmax = B - b0;
-        for (const Group& g : op->groups) bmax = std::min(bmax, g.vb);
-        const int bn = bmax;
-        // local mode (and every adjoint): rows_inv accumulates only the lines its terms touch
-        const bool zero_first = !global || adjoint;
-        if (zero_first)
-            PCB_CK(cudaMemsetAsync(dG + (int64_t)b0 * op->N, 0, (size_t)bn * op->N * sizeof(double), st));
+    auto pass_args = [&](const Group& g, const Chunk& c, int b0, int bn, double2* T) {
+        PassArgs a = base_args(op, g);
+        a.slots = c.slots.p;
+        a.n_slots = c.count;
+        a.B = bn;
+        a.in = dF + (int64_t)b0 * op->N;
+        a.out = dG + (int64_t)b0 * op->N;
+        a.T = T;
+        a.S_stride = adjoint ? g.S_adj : g.S_apply;
+        a.T_stride = adjoint ? g.T_adj : g.T_apply;
+        return a;
+    };
+    auto front = [&](PassArgs a, cudaStream_t s) {  // K2 + K3 (+ 3-D middle passes)
+        a.global = global;
+        if (!adjoint) {
+            launch(op, s, "rows_fwd(apply)", [&] { return launch_rows_fwd(a, RF_APPLY, s); });
+            if (D == 3) launch(op, s, "mid(fwd apply)", [&] { return launch_mid(a, MM_FWD_APPLY, s); });
+            launch(op, s, global ? "cols(apply,global)" : "cols(apply,local)",
+                   [&] { return launch_cols(a, global ? CM_APPLY_GLOBAL : CM_APPLY_LOCAL, s); });
+            if (D == 3) launch(op, s, "mid(inv apply)", [&] { return launch_mid(a, MM_INV_APPLY, s); });
+        } else {
+            launch(op, s, "rows_fwd(adjoint)", [&] { return launch_rows_fwd(a, RF_ADJ, s); });
+            if (D == 3) launch(op, s, "mid(fwd adjoint)", [&] { return launch_mid(a, MM_FWD_ADJ, s); });
+            launch(op, s, global ? "cols(adjoint,global)" : "cols(adjoint,local)",
+                   [&] { return launch_cols(a, global ? CM_ADJ_GLOBAL : CM_ADJ_LOCAL, s); });
+            a.global = 0;
+            if (D == 3) launch(op, s, "mid(inv adjoint)", [&] { return launch_mid(a, MM_INV_ADJ, s); });
+        }
+    };
+    auto back = [&](PassArgs a, const Chunk& c, cudaStream_t s, bool accumulate) {  // K4
+        const Csr& csr = adjoint ? c.adj : c.apply;
+        a.global = global && !adjoint;
+        a.accumulate = accumulate ? 1 : 0;
+        a.line_ptr = csr.ptr.p;
+        a.line_id = csr.ids.p;
+        a.line_rng = csr.rng.p;
+        a.entries = csr.en.p;
+        if (csr.n_lines > 0)
+            launch(op, s, adjoint ? "rows_inv(adjoint)" : "rows_inv(apply)",
+                   [&] { return launch_rows_inv(a, adjoint ? RI_ADJ : RI_APPLY, csr.n_lines, s); });
+    };
+
+    if (global) {
+        const Group& g = op->groups[0];
+        const Chunk& c = g.chunks[0];
+        for (int b0 = 0; b0 < B; b0 += g.vb) {
+            const int bn = std::min(g.vb, B - b0);
+            if (adjoint)
+                PCB_CK(cudaMemsetAsync(dG + (int64_t)b0 * op->N, 0, (size_t)bn * op->N * sizeof(double), st));
+            PassArgs a = pass_args(g, c, b0, bn, op->T.p);
+            front(a, st);
+            back(a, c, st, adjoint);
+        }
+        return;
+    }
+
+    // LOCAL: fork the two pipeline streams off the caller's stream
+    PCB_CK(cudaEventRecord(op->ev_fork, st));
+    PCB_CK(cudaStreamWaitEvent(op->sA, op->ev_fork, 0));
+    PCB_CK(cudaStreamWaitEvent(op->sB, op->ev_fork, 0));
+    PCB_CK(cudaMemsetAsync(dG, 0, (size_t)B * op->N * sizeof(double), op->sB));
+    int64_t i = 0;
+    int vb = op->max_batch;
+    for (const Group& g : op->groups) vb = std::min(vb, g.vb);
+    for (int b0 = 0; b0 < B; b0 += vb) {
+        const int bn = std::min(vb, B - b0);
         for (const Group& g : op->groups) {
             for (const Chunk& c : g.chunks) {
-                PassArgs a = base_args(op, g);
-                a.slots = c.slots.p;
-                a.n_slots = c.count;
-                a.B = bn;
-                a.in = dF + (int64_t)b0 * op->N;
-                a.out = dG + (int64_t)b0 * op->N;
-                a.accumulate = zero_first ? 1 : 0;
-                if (!adjoint) {
-                    a.S_stride = g.S_apply;
-                    a.T_stride = g.T_apply;
-                    a.global = global;
-                    launch(op, st, "rows_fwd(apply)", [&] { return launch_rows_fwd(a, RF_APPLY, st); });
-                    if (D == 3) launch(op, st, "mid(fwd apply)", [&] { return launch_mid(a, MM_FWD_APPLY, st); });
-                    launch(op, st, global ? "cols(apply,global)" : "cols(apply,local)", [&] { return launch_cols(a, global ? CM_APPLY_GLOBAL : CM_APPLY_LOCAL, st); });
-                    if (D == 3) launch(op, st, "mid(inv apply)", [&] { return launch_mid(a, MM_INV_APPLY, st); });
-                    a.line_ptr = c.apply.ptr.p;
-                    a.line_id = c.apply.ids.p;
-                    a.line_rng = c.apply.rng.p;
-                    a.entries = c.apply.en.p;
-                    if (c.apply.n_lines > 0)
-                        launch(op, st, "rows_inv(apply)",
-                               [&] { return launch_rows_inv(a, RI_APPLY, c.apply.n_lines, st); });
+                const int par = (int)(i & 1);
+                double2* T = (par && op->pipeline) ? op->T2.p : op->T.p;
+                if (i >= 2 && op->pipeline) PCB_CK(cudaStreamWaitEvent(op->sA, op->ev_done[par], 0));
+                PassArgs a = pass_args(g, c, b0, bn, T);
+                front(a, op->sA);
+                if (op->pipeline) {
+                    PCB_CK(cudaEventRecord(op->ev_cols[par], op->sA));
+                    PCB_CK(cudaStreamWaitEvent(op->sB, op->ev_cols[par], 0));
+                    back(a, c, op->sB, true);
+                    PCB_CK(cudaEventRecord(op->ev_done[par], op->sB));
                 } else {
-                    a.S_stride = g.S_adj;
-                    a.T_stride = g.T_adj;
-                    a.global = global;
-                    launch(op, st, "rows_fwd(adjoint)", [&] { return launch_rows_fwd(a, RF_ADJ, st); });
-                    if (D == 3) launch(op, st, "mid(fwd adjoint)", [&] { return launch_mid(a, MM_FWD_ADJ, st); });
-                    launch(op, st, global ? "cols(adjoint,global)" : "cols(adjoint,local)", [&] { return launch_cols(a, global ? CM_ADJ_GLOBAL : CM_ADJ_LOCAL, st); });
-                    a.global = 0;
-                    if (D == 3) launch(op, st, "mid(inv adjoint)", [&] { return launch_mid(a, MM_INV_ADJ, st); });
-                    a.line_ptr = c.adj.ptr.p;
-                    a.line_id = c.adj.ids.p;
-                    a.line_rng = c.adj.rng.p;
-                    a.entries = c.adj.en.p;
-                    if (c.adj.n_lines > 0)
-                        launch(op, st, "rows_inv(adjoint)",
-                               [&] { return launch_rows_inv(a, RI_ADJ, c.adj.n_lines, st); });
+                    if (i == 0) {
+                        PCB_CK(cudaEventRecord(op->ev_done[0], op->sB));
+                        PCB_CK(cudaStreamWaitEvent(op->sA, op->ev_done[0], 0));
+                    }
+                    back(a, c, op->sA, true);
                 }
+                ++i;
             }
         }
-        b0 += bn;
     }
+    // join: the caller's stream waits for both pipeline streams
+    PCB_CK(cudaEventRecord(op->ev_join, op->sA));
+    PCB_CK(cudaStreamWaitEvent(st, op->ev_join, 0));
+    PCB_CK(cudaEventRecord(op->ev_join, op->sB));
+    PCB_CK(cudaStreamWaitEvent(st, op->ev_join, 0));
 }
 
 EntryArgs entry_args(pcb_op* op) {
@@ -930,7 +987,13 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
         PCB_CK(cudaGetDeviceProperties(&prop, op->device));
         if (prop.major < 10) fail(PCB_ECUDA, "pcop-b200 kernels are built for sm_100a (Blackwell B200)");
         op->max_batch = opt.max_batch > 0 ? opt.max_batch : 16;
+        if (const char* e = getenv("PCB_PIPELINE")) op->pipeline = atoi(e) != 0;
         PCB_CK(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
+        PCB_CK(cudaStreamCreateWithFlags(&op->sA, cudaStreamNonBlocking));
+        PCB_CK(cudaStreamCreateWithFlags(&op->sB, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&op->ev_fork, &op->ev_join, &op->ev_cols[0], &op->ev_cols[1], &op->ev_done[0],
+                               &op->ev_done[1]})
+            PCB_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         make_twiddles(op);
         plan(op, dim, dom_lo, dom_hi, r, w_lo, w_hi, w_vals, phi_lo, phi_hi, phi_vals, opt);
         build_spectra(op);
@@ -940,8 +1003,7 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
         op->info.device_bytes = (int64_t)dev;
     });
     if (st != PCB_OK) {
-        if (op->stream) cudaStreamDestroy(op->stream);
-        delete op;
+        pcb_destroy(op);
         return st;
     }
     *out = op;
@@ -960,6 +1022,13 @@ PCB_API pcb_status pcb_destroy(pcb_op* op) {
         cudaEventDestroy(r.b);
     }
     for (auto e : op->ev_pool) cudaEventDestroy(e);
+    for (cudaStream_t s : {op->sA, op->sB})
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    for (cudaEvent_t e : {op->ev_fork, op->ev_join, op->ev_cols[0], op->ev_cols[1], op->ev_done[0], op->ev_done[1]})
+        if (e) cudaEventDestroy(e);
     delete op;
     return PCB_OK;
 }

@@ -1,6 +1,6 @@
 #!/bin/bash
 # development loop: parity quick check + c3/c4 bench lines
-timeout 300 python scripts/quick_parity.py 2>&1 | tail -12
+[ -z "$NOPARITY" ] && timeout 300 python scripts/quick_parity.py 2>&1 | tail -12
 for args in "$@"; do
   timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline $args 2>&1 | tail -2 | python -c "
 import sys, json
