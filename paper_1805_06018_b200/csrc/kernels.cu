@@ -392,24 +392,19 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_inv(PassArgs a) {
     constexpr int RL = LastPos<N>::RL;
     constexpr int NT = NL * FftCfg<N>::TPL;
     constexpr int XS = 2 * N + 1;  // padded real line stride: conflict-free column writes
+    constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
+                                                                          : (NL * (2 * N + 1) + 1) / 2;
     extern __shared__ double2 buf[];
     const int64_t aline = blockIdx.x;
     const int vec = blockIdx.y;
-    const int D = a.D;
-    const int ax = D - 1;
+    const int ax = a.D - 1;
     const int64_t line = a.line_id[aline];
     const int ulo = a.line_rng[2 * aline], uhi = a.line_rng[2 * aline + 1];
-    // layout: buf [smem_words] (FFT; reused as xs) | stage [NL][N+1] | acc [n_last] | meta
-    double* xs = reinterpret_cast<double*>(buf);  // NL x XS doubles <= smem_words double2
-    constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
-                                                                          : (NL * (2 * N + 1) + 1) / 2;
+    // layout: buf [BUFW] (FFT; reused as xs) | stage [NL][N+1] | acc [n_last] | meta [NL]
+    double* xs = reinterpret_cast<double*>(buf);
     double2* stage = buf + BUFW;
-    double* acc = reinterpret_cast<double*>(stage + NL * (N + 1));  // [ulo, uhi)
-    int* m_lo = reinterpret_cast<int*>(acc + a.n[ax]);
-    int* m_hi = m_lo + NL;
-    int* m_sh = m_hi + NL;
-    int64_t* m_w = reinterpret_cast<int64_t*>(m_sh + NL + (NL & 1));
-    int64_t* m_row = m_w + NL;
+    double* acc = reinterpret_cast<double*>(stage + NL * (N + 1));
+    GatherEntry* meta = reinterpret_cast<GatherEntry*>(acc + a.n[ax] + (a.n[ax] & 1));
     const int64_t e_beg = a.line_ptr[aline];
     const int64_t e_end = a.line_ptr[aline + 1];
     const double2* twP = twtab(a.tw, 2 * N);
@@ -419,41 +414,14 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_inv(PassArgs a) {
 
     for (int64_t e0 = e_beg; e0 < e_end; e0 += NL) {
         const int ne = (int)((e_end - e0) < NL ? (e_end - e0) : NL);
+        __syncthreads();  // previous batch finished with meta / xs
+        if (threadIdx.x < ne) meta[threadIdx.x] = a.entries[e0 + threadIdx.x];
         __syncthreads();
-        if (threadIdx.x < NL) {
-            const int ll = threadIdx.x;
-            int lo = 0, hi = 0, sh = 0;
-            int64_t wrow = -1, trow = -1;
-            if (ll < ne) {
-                const GatherEntry en = a.entries[e0 + ll];
-                const TermDesc& td = a.global ? *a.gdesc : a.terms[a.slots[en.slot]];
-                const int64_t it = a.global ? vec : (int64_t)en.slot * a.B + vec;
-                trow = it * a.T_stride + en.t_off;
-                if (MODE == RI_APPLY) {
-                    sh = (int)(td.s[ax] - a.dom_lo[ax]);  // v = p - sh in [o_lo, o_lo + o_cnt)
-                    lo = sh + td.o_lo[ax];
-                    hi = lo + td.o_cnt[ax];
-                } else {
-                    sh = (int)(td.x_lo[ax] - a.dom_lo[ax]);
-                    lo = sh;
-                    hi = sh + td.m[ax];
-                    wrow = td.w_off + (int64_t)en.w_row * td.m[ax];
-                }
-                lo = lo < ulo ? ulo : lo;
-                hi = hi > uhi ? uhi : hi;
-            }
-            m_lo[ll] = lo;
-            m_hi[ll] = hi;
-            m_sh[ll] = sh;
-            m_w[ll] = wrow;
-            m_row[ll] = trow;
-        }
-        __syncthreads();
-        // stage the NL half-spectrum rows (N+1 complex each) with async copies
         for (int idx = threadIdx.x; idx < ne * (N + 1); idx += NT) {
             const int ll = idx / (N + 1);
             const int k = idx - ll * (N + 1);
-            cp_async16(&stage[idx], a.T + m_row[ll] + k);
+            const int64_t it = a.global ? vec : (int64_t)meta[ll].slot * a.B + vec;
+            cp_async16(&stage[idx], a.T + it * a.T_stride + meta[ll].t_off + k);
         }
         cp_async_wait_all();
         __syncthreads();
@@ -481,22 +449,22 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_inv(PassArgs a) {
         fft_rev_order<N, +1, NL, PSH<NL>>(v, buf, l, tl, twtab(a.tw, N));
         __syncthreads();
 #pragma unroll
-        for (int b = 0; b < R / RL; ++b)
+        for (int bb = 0; bb < R / RL; ++bb)
 #pragma unroll
             for (int r = 0; r < RL; ++r) {
-                const int p = LastPos<N>::pos(tl, b, r);
-                xs[l * XS + 2 * p] = v[b * RL + r].x;
-                xs[l * XS + 2 * p + 1] = v[b * RL + r].y;
+                const int p = LastPos<N>::pos(tl, bb, r);
+                xs[l * XS + 2 * p] = v[bb * RL + r].x;
+                xs[l * XS + 2 * p + 1] = v[bb * RL + r].y;
             }
         __syncthreads();
         for (int ll = 0; ll < ne; ++ll) {
-            const int lo = m_lo[ll], hi = m_hi[ll];
-            const double* x = xs + ll * XS - m_sh[ll];
+            const int lo = meta[ll].lo, hi = meta[ll].hi;
+            const double* x = xs + ll * XS - meta[ll].sh;
             int p = lo + (int)((threadIdx.x + NT - (unsigned)(lo % NT)) % NT);
             if (MODE == RI_APPLY) {
                 for (; p < hi; p += NT) acc[p - ulo] += x[p] * a.scale;
             } else {
-                const double* w = a.w_pool + m_w[ll] - m_sh[ll];
+                const double* w = a.w_pool + meta[ll].w_off;
                 for (; p < hi; p += NT) acc[p - ulo] += w[p] * (x[p] * a.scale);
             }
         }
@@ -744,9 +712,8 @@ cudaError_t rows_inv_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
     dim3 grid((unsigned)n_lines, (unsigned)a.B);
     constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
                                                                           : (NL * (2 * N + 1) + 1) / 2;
-    const size_t smem = sizeof(double2) * (BUFW + NL * (N + 1)) +
-                        sizeof(double) * (size_t)a.n[a.D - 1] + (3 * NL + 1) * sizeof(int) +
-                        2 * NL * sizeof(int64_t) + 16;
+    const size_t smem = sizeof(double2) * (BUFW + NL * (N + 1)) + sizeof(double) * ((size_t)a.n[a.D - 1] + 1) +
+                        NL * sizeof(GatherEntry) + 16;
     return launch_dyn(k_rows_inv<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
 }
 

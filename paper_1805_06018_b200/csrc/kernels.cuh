@@ -29,11 +29,14 @@ struct TermDesc {
     int64_t spec_off;  // double2: spectrum, tile-major [L/NL][P0][NL]
 };
 
-// rows_inv gather list entry: one C2R line of T contributing to one output line
+// rows_inv gather list entry: one C2R line of T contributing to one output line.
+// Self-contained (precomputed at create) so the gather issues no dependent loads.
 struct GatherEntry {
-    int32_t slot;     // term slot within the launch chunk
-    int32_t w_row;    // adjoint: row of w_k (lead index) multiplying the line
+    int32_t slot;     // term slot within the launch chunk (T item = slot * B + vec)
+    int32_t lo, hi;   // output positions [lo, hi) along the last axis (domain-relative, clipped)
+    int32_t sh;       // line index of output position p is p - sh
     int64_t t_off;    // double2 offset of the line inside the item's T buffer
+    int64_t w_off;    // adjoint: w_pool offset of the multiplying w row shifted by -sh; else -1
 };
 
 // Everything one pipeline pass needs.  D in {2, 3}: axes 0..D-1, last axis is

@@ -283,6 +283,23 @@ void build_csr(pcb_op* op, Group& g, Chunk& c, bool global) {
     auto line_of = [&](int64_t c0, int64_t c1) {  // absolute coordinates of the lead axes
         return D == 2 ? c0 - op->dom_lo[0] : (c0 - op->dom_lo[0]) * op->n[1] + (c1 - op->dom_lo[1]);
     };
+    const int ax = D - 1;
+    // entry's output range along the last axis (domain-relative) and its line shift
+    auto finish = [&](GatherEntry& e, const TermDesc& t, bool adjoint, int64_t w_row) {
+        if (!adjoint) {
+            e.sh = (int)(t.s[ax] - op->dom_lo[ax]);
+            e.lo = e.sh + t.o_lo[ax];
+            e.hi = e.lo + t.o_cnt[ax];
+            e.w_off = -1;
+        } else {
+            e.sh = (int)(t.x_lo[ax] - op->dom_lo[ax]);
+            e.lo = e.sh;
+            e.hi = e.sh + t.m[ax];
+            e.w_off = t.w_off + w_row * t.m[ax] - e.sh;
+        }
+        e.lo = std::max(e.lo, 0);
+        e.hi = std::min(e.hi, op->n[ax]);
+    };
     std::vector<std::vector<GatherEntry>> ap(n_lines), ad(n_lines);
     for (int i = 0; i < c.count; ++i) {
         const TermDesc& t = op->terms[g.terms[c.first + i]];
@@ -292,8 +309,8 @@ void build_csr(pcb_op* op, Group& g, Chunk& c, bool global) {
             for (int u1 = 0; u1 < c1n; ++u1) {
                 GatherEntry e{};
                 e.slot = i;
-                e.w_row = D == 3 ? u0 * t.m[1] + u1 : u0;
                 e.t_off = (int64_t)u0 * g.L + (D == 3 ? (int64_t)u1 * g.W : 0);
+                finish(e, t, true, D == 3 ? u0 * t.m[1] + u1 : u0);
                 ad[line_of(t.x_lo[0] + u0, D == 3 ? t.x_lo[1] + u1 : 0)].push_back(e);
             }
         if (!global) {
@@ -302,8 +319,8 @@ void build_csr(pcb_op* op, Group& g, Chunk& c, bool global) {
                 for (int j1 = 0; j1 < o1n; ++j1) {
                     GatherEntry e{};
                     e.slot = i;
-                    e.w_row = 0;
                     e.t_off = (int64_t)j0 * g.L + (D == 3 ? (int64_t)j1 * g.W : 0);
+                    finish(e, t, false, 0);
                     const int64_t y0 = t.s[0] + t.o_lo[0] + j0;
                     const int64_t y1 = D == 3 ? t.s[1] + t.o_lo[1] + j1 : 0;
                     ap[line_of(y0, y1)].push_back(e);
@@ -314,28 +331,14 @@ void build_csr(pcb_op* op, Group& g, Chunk& c, bool global) {
         for (int64_t ln = 0; ln < n_lines; ++ln) {
             GatherEntry e{};
             e.slot = 0;
-            e.w_row = 0;
             const int64_t j0 = D == 2 ? ln : ln / op->n[1];
             const int64_t j1 = D == 2 ? 0 : ln % op->n[1];
             e.t_off = j0 * g.L + j1 * g.W;
+            finish(e, op->gdesc, false, 0);
             ap[ln].push_back(e);
         }
     }
-    // range of an entry along the last axis (domain-relative), for the per-line union
-    const int ax = D - 1;
-    auto rng_of = [&](const GatherEntry& e, bool adjoint, int& lo, int& hi) {
-        const TermDesc& t = global && !adjoint ? op->gdesc : op->terms[g.terms[c.first + e.slot]];
-        if (!adjoint) {
-            lo = (int)(t.s[ax] - op->dom_lo[ax]) + t.o_lo[ax];
-            hi = lo + t.o_cnt[ax];
-        } else {
-            lo = (int)(t.x_lo[ax] - op->dom_lo[ax]);
-            hi = lo + t.m[ax];
-        }
-        lo = std::max(lo, 0);
-        hi = std::min(hi, op->n[ax]);
-    };
-    auto flatten = [&](std::vector<std::vector<GatherEntry>>& lists, Csr& out, bool adjoint) {
+    auto flatten = [&](std::vector<std::vector<GatherEntry>>& lists, Csr& out) {
         std::vector<int64_t> hp, ids;
         std::vector<int32_t> rg;
         std::vector<GatherEntry> he;
@@ -343,10 +346,8 @@ void build_csr(pcb_op* op, Group& g, Chunk& c, bool global) {
             if (lists[ln].empty()) continue;
             int ulo = INT32_MAX, uhi = INT32_MIN;
             for (const GatherEntry& e : lists[ln]) {
-                int lo, hi;
-                rng_of(e, adjoint, lo, hi);
-                ulo = std::min(ulo, lo);
-                uhi = std::max(uhi, hi);
+                ulo = std::min(ulo, e.lo);
+                uhi = std::max(uhi, e.hi);
             }
             hp.push_back((int64_t)he.size());
             ids.push_back(ln);
@@ -367,8 +368,8 @@ void build_csr(pcb_op* op, Group& g, Chunk& c, bool global) {
         out.rng.upload(rg);
         out.en.upload(he);
     };
-    flatten(ap, c.apply, false);
-    flatten(ad, c.adj, true);
+    flatten(ap, c.apply);
+    flatten(ad, c.adj);
 }
 
 void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t r, const int64_t* w_lo,
