@@ -160,6 +160,8 @@ struct pcb_op {
     std::vector<pcb::Group> groups;
     pcb::DevBuf<double2> S, T, T2;  // T2: second inverse buffer of the two-stream local pipeline
     cudaStream_t sA = nullptr, sB = nullptr;
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // host-buffer calls: copy streams
+    cudaEvent_t ev_io[8] = {};
     bool pipeline = false;  // two-stream local pipeline (PCB_PIPELINE=1 enables; measured no gain on c3)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_cols[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
     // entry gather
@@ -1023,7 +1025,9 @@ PCB_API pcb_status pcb_destroy(pcb_op* op) {
         cudaEventDestroy(r.b);
     }
     for (auto e : op->ev_pool) cudaEventDestroy(e);
-    for (cudaStream_t s : {op->sA, op->sB})
+    for (cudaEvent_t e : op->ev_io)
+        if (e) cudaEventDestroy(e);
+    for (cudaStream_t s : {op->sA, op->sB, op->s_h2d, op->s_d2h})
         if (s) {
             cudaStreamSynchronize(s);
             cudaStreamDestroy(s);
@@ -1079,9 +1083,25 @@ static pcb_status apply_host_common(pcb_op* op, bool adjoint, int32_t B, const d
         const size_t cnt = (size_t)B * (size_t)op->N;
         op->st_in.ensure(cnt);
         op->st_out.ensure(cnt);
-        PCB_CK(cudaMemcpyAsync(op->st_in.p, F, cnt * sizeof(double), cudaMemcpyHostToDevice, op->stream));
-        run_batch(op, adjoint, B, op->st_in.p, op->st_out.p, op->stream);
-        PCB_CK(cudaMemcpyAsync(G, op->st_out.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, op->stream));
+        // sub-batches overlap H2D(j+1) and D2H(j-1) with the kernels of sub-batch j
+        const int nsub = B >= 8 ? 4 : (B >= 2 ? 2 : 1);
+        if (!op->s_h2d) {
+            PCB_CK(cudaStreamCreateWithFlags(&op->s_h2d, cudaStreamNonBlocking));
+            PCB_CK(cudaStreamCreateWithFlags(&op->s_d2h, cudaStreamNonBlocking));
+            for (int j = 0; j < 8; ++j) PCB_CK(cudaEventCreateWithFlags(&op->ev_io[j], cudaEventDisableTiming));
+        }
+        for (int j = 0; j < nsub; ++j) {
+            const int b0 = (int)((int64_t)B * j / nsub), b1 = (int)((int64_t)B * (j + 1) / nsub);
+            const size_t off = (size_t)b0 * op->N, n = (size_t)(b1 - b0) * op->N;
+            PCB_CK(cudaMemcpyAsync(op->st_in.p + off, F + off, n * sizeof(double), cudaMemcpyHostToDevice, op->s_h2d));
+            PCB_CK(cudaEventRecord(op->ev_io[2 * (j & 1)], op->s_h2d));
+            PCB_CK(cudaStreamWaitEvent(op->stream, op->ev_io[2 * (j & 1)], 0));
+            run_batch(op, adjoint, b1 - b0, op->st_in.p + off, op->st_out.p + off, op->stream);
+            PCB_CK(cudaEventRecord(op->ev_io[2 * (j & 1) + 1], op->stream));
+            PCB_CK(cudaStreamWaitEvent(op->s_d2h, op->ev_io[2 * (j & 1) + 1], 0));
+            PCB_CK(cudaMemcpyAsync(G + off, op->st_out.p + off, n * sizeof(double), cudaMemcpyDeviceToHost, op->s_d2h));
+        }
+        PCB_CK(cudaStreamSynchronize(op->s_d2h));
         PCB_CK(cudaStreamSynchronize(op->stream));
     });
 }
