@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_fwd(PassArgs a) {
                 src = (int64_t)vec * a.N + (D == 3 ? (x0 * a.n[1] + x1) * a.n[2] : x0 * a.n[1]) +
                       (td.x_lo[ax] - a.dom_lo[ax]);
                 woff = td.w_off + (D == 3 ? c0 * td.m[1] + c1 : c0) * (int64_t)td.m[ax];
-                row = D == 3 ? (c0 * a.P[1] + c1) * a.W : c0 * a.W;
+                row = D == 3 ? (c0 * td.P1 + c1) * a.W : c0 * a.W;
                 lo = 0;
                 hi = td.m[ax];
             } else if (MODE == RF_ADJ) {
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_fwd(PassArgs a) {
                 const int64_t y1 = D == 3 ? td.s[1] + v1 - a.dom_lo[1] : 0;
                 src = (int64_t)vec * a.N + (D == 3 ? (y0 * a.n[1] + y1) * a.n[2] : y0 * a.n[1]) +
                       (td.s[ax] - a.dom_lo[ax]);
-                row = D == 3 ? ((v0 - td.o_lo[0]) * a.P[1] + v1) * a.W : (v0 - td.o_lo[0]) * a.W;
+                row = D == 3 ? ((v0 - td.o_lo[0]) * td.P1 + v1) * a.W : (v0 - td.o_lo[0]) * a.W;
                 lo = td.o_lo[ax];
                 hi = td.o_lo[ax] + td.o_cnt[ax];
             } else {
@@ -142,39 +142,37 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_fwd(PassArgs a) {
     }
     __syncthreads();
 
-    // phase 1: z[j] = (x[2j], x[2j+1]) gathered straight into the interleaved FFT buffer
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < NL * N; idx += NT) {
-        const int ll = idx / N;
-        const int p = idx - ll * N;
-        const int lo = m_lo[ll], hi = m_hi[ll];
-        const int64_t src = m_src[ll];
-        double xv[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int u = 2 * p + h;
-            double x = 0.0;
-            if (u >= lo && u < hi) {
-                if (MODE == RF_APPLY) x = __ldg(&a.in[src + u]) * __ldg(&a.w_pool[m_w[ll] + u]);
-                else if (MODE == RF_ADJ) x = __ldg(&a.in[src + u]);
-                else {
-                    const int64_t zl = imod(u + td.s[ax] - td.x_lo[ax] - td.k_lo[ax], a.P[ax]);
-                    if (zl < td.k_ext[ax]) x = a.phi_pool[src + zl];
-                }
-            }
-            xv[h] = x;
-        }
-        buf[sidx<NL, PS>(p, ll)] = make_double2(xv[0], xv[1]);
-    }
-    __syncthreads();
-
+    // phase 1: z[j] = (x[2j], x[2j+1]) gathered straight into the first-stage registers
     const int l = threadIdx.x % NL;
     const int tl = threadIdx.x / NL;
     double2 v[R];
+    {
+        const int lo = m_lo[l], hi = m_hi[l];
+        const int64_t src = m_src[l];
+        const int64_t wsrc = m_w[l];
 #pragma unroll
-    for (int b = 0; b < R / RF; ++b)
+        for (int b = 0; b < R / RF; ++b)
 #pragma unroll
-        for (int r = 0; r < RF; ++r) v[b * RF + r] = buf[sidx<NL, PS>(FirstPos<N>::pos(tl, b, r), l)];
+            for (int r = 0; r < RF; ++r) {
+                const int p = FirstPos<N>::pos(tl, b, r);
+                double xv[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int u = 2 * p + h;
+                    double x = 0.0;
+                    if (u >= lo && u < hi) {
+                        if (MODE == RF_APPLY) x = __ldg(&a.in[src + u]) * __ldg(&a.w_pool[wsrc + u]);
+                        else if (MODE == RF_ADJ) x = __ldg(&a.in[src + u]);
+                        else {
+                            const int64_t zl = imod(u + td.s[ax] - td.x_lo[ax] - td.k_lo[ax], a.P[ax]);
+                            if (zl < td.k_ext[ax]) x = a.phi_pool[src + zl];
+                        }
+                    }
+                    xv[h] = x;
+                }
+                v[b * RF + r] = make_double2(xv[0], xv[1]);
+            }
+    }
     fft_fwd_order<N, -1, NL, PS>(v, buf, l, tl, twtab(a.tw, N));
     __syncthreads();
 #pragma unroll
@@ -186,7 +184,7 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_fwd(PassArgs a) {
 
     // phase 3: even/odd split X[k] = A[k] + W^k B[k], k = 0..N
     const double2* twP = twtab(a.tw, 2 * N);
-    double2* S_item = a.S + (int64_t)item * a.S_stride;
+    double2* S_item = MODE == RF_SPEC ? a.S + (int64_t)item * a.S_stride : a.S + td.s_pool + vec * td.s_vst;
     for (int idx = threadIdx.x; idx < NL * (N + 1); idx += NT) {
         const int ll = idx / (N + 1);
         const int k = idx - ll * (N + 1);
@@ -228,7 +226,8 @@ __global__ void __launch_bounds__(NL * FftCfg<P1>::TPL) k_mid(PassArgs a) {
     const int tl = threadIdx.x / NL;
     const int64_t c = (int64_t)blockIdx.x * NL + l;
     const bool cvalid = c < a.W;
-    double2* base = (fwd ? a.S + (int64_t)item * a.S_stride : a.T + (int64_t)item * a.T_stride) +
+    double2* base = (MODE == MM_FWD_SPEC ? a.S + (int64_t)item * a.S_stride
+                                         : fwd ? a.S + td.s_pool + vec * td.s_vst : a.T + td.t_pool + vec * td.t_vst) +
                     plane * (int64_t)a.P[1] * a.W + c;
     double2 v[R];
     if (fwd) {
@@ -311,7 +310,8 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
     if (MODE == CM_SPEC || MODE == CM_APPLY_LOCAL || MODE == CM_ADJ_LOCAL) {
         const int slot = item / nvec;
         const TermDesc& td = a.terms[a.slots[slot]];
-        const double2* S_item = a.S + (int64_t)item * a.S_stride;
+        const int vec = item % nvec;
+        const double2* S_item = MODE == CM_SPEC ? a.S + (int64_t)item * a.S_stride : a.S + td.s_pool + vec * td.s_vst;
         if (MODE == CM_SPEC) load_in(S_item, 0, P0, v);
         else if (MODE == CM_APPLY_LOCAL) load_in(S_item, 0, td.m[0], v);
         else load_in(S_item, td.o_lo[0], td.o_cnt[0], v);
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
             v[r] = MODE == CM_APPLY_LOCAL ? cmul(v[r], ph) : cmulc(v[r], ph);
         }
         fft_rev_order<P0, +1, NL, PSH<NL>>(v, buf, l, tl, tw0);
-        double2* T_item = a.T + (int64_t)item * a.T_stride;
+        double2* T_item = a.T + td.t_pool + vec * td.t_vst;
         if (MODE == CM_APPLY_LOCAL) store_out(T_item, td.o_lo[0], td.o_cnt[0], v);
         else store_out(T_item, 0, td.m[0], v);
         return;
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
         for (int r = 0; r < R; ++r) acc[r] = czero();
         for (int slot = 0; slot < a.n_slots; ++slot) {
             const TermDesc& td = a.terms[a.slots[slot]];
-            const double2* S_item = a.S + ((int64_t)slot * a.B + vec) * a.S_stride;
+            const double2* S_item = a.S + td.s_pool + vec * td.s_vst;
             load_in(S_item, 0, td.m[0], v);
             fft_fwd_order<P0, -1, NL, PSH<NL>>(v, buf, l, tl, tw0);
             const double2* spec = a.spec_pool + td.spec_off + tile_off;
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
         }
         fft_rev_order<P0, +1, NL, PSH<NL>>(acc, buf, l, tl, tw0);
         const TermDesc& g = *a.gdesc;
-        store_out(a.T + (int64_t)vec * a.T_stride, g.o_lo[0], g.o_cnt[0], acc);
+        store_out(a.T + g.t_pool + vec * g.t_vst, g.o_lo[0], g.o_cnt[0], acc);
         return;
     }
 
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
         const int vec = item;
         const TermDesc& g = *a.gdesc;
         double2 x[R];
-        load_in(a.S + (int64_t)vec * a.S_stride, g.o_lo[0], g.o_cnt[0], x);
+        load_in(a.S + g.s_pool + vec * g.s_vst, g.o_lo[0], g.o_cnt[0], x);
         fft_fwd_order<P0, -1, NL, PSH<NL>>(x, buf, l, tl, tw0);
         for (int slot = 0; slot < a.n_slots; ++slot) {
             const TermDesc& td = a.terms[a.slots[slot]];
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
                 v[r] = cmulc(x[r], ph);
             }
             fft_rev_order<P0, +1, NL, PSH<NL>>(v, buf, l, tl, tw0);
-            store_out(a.T + ((int64_t)slot * a.B + vec) * a.T_stride, 0, td.m[0], v);
+            store_out(a.T + td.t_pool + vec * td.t_vst, 0, td.m[0], v);
         }
     }
 }
@@ -420,8 +420,7 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_inv(PassArgs a) {
         for (int idx = threadIdx.x; idx < ne * (N + 1); idx += NT) {
             const int ll = idx / (N + 1);
             const int k = idx - ll * (N + 1);
-            const int64_t it = a.global ? vec : (int64_t)meta[ll].slot * a.B + vec;
-            cp_async16(&stage[idx], a.T + it * a.T_stride + meta[ll].t_off + k);
+            cp_async16(&stage[idx], a.T + meta[ll].t_off + vec * meta[ll].t_vst + k);
         }
         cp_async_wait_all();
         __syncthreads();
@@ -461,11 +460,12 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_inv(PassArgs a) {
             const int lo = meta[ll].lo, hi = meta[ll].hi;
             const double* x = xs + ll * XS - meta[ll].sh;
             int p = lo + (int)((threadIdx.x + NT - (unsigned)(lo % NT)) % NT);
+            const double sc = meta[ll].scale;
             if (MODE == RI_APPLY) {
-                for (; p < hi; p += NT) acc[p - ulo] += x[p] * a.scale;
+                for (; p < hi; p += NT) acc[p - ulo] += x[p] * sc;
             } else {
                 const double* w = a.w_pool + meta[ll].w_off;
-                for (; p < hi; p += NT) acc[p - ulo] += w[p] * (x[p] * a.scale);
+                for (; p < hi; p += NT) acc[p - ulo] += w[p] * (x[p] * sc);
             }
         }
     }
@@ -626,11 +626,7 @@ constexpr int cols_nl() {
 template <int N, int MODE>
 cudaError_t rows_fwd_n(const PassArgs& a, cudaStream_t st) {
     constexpr int NL = rows_nl<N>();
-    int64_t maxlines;
-    if (MODE == RF_SPEC) maxlines = a.D == 2 ? a.P[0] : (int64_t)a.P[0] * a.P[1];
-    else maxlines = a.D == 2 ? a.n[0] + 0 : (int64_t)a.n[0] * a.n[1];
-    // lines per item never exceed max(m, o_cnt) <= P per axis; bound by P
-    if (MODE != RF_SPEC) maxlines = a.D == 2 ? a.P[0] : (int64_t)a.P[0] * a.P[1];
+    const int64_t maxlines = MODE == RF_SPEC ? (a.D == 2 ? a.P[0] : (int64_t)a.P[0] * a.P[1]) : a.lines_max;
     const int items = (MODE == RF_ADJ && a.global) ? a.B : a.n_slots * (MODE == RF_SPEC ? 1 : a.B);
     dim3 grid((unsigned)((maxlines + NL - 1) / NL), (unsigned)items);
     const size_t smem = sizeof(double2) * smem_words<N, NL>() + NL * (3 * sizeof(int64_t) + 2 * sizeof(int));

@@ -27,16 +27,23 @@ struct TermDesc {
     int64_t w_off;     // doubles: w_k on X_k, row-major [m0][m1][m2]
     int64_t phi_off;   // doubles: phi_k^E on K, row-major
     int64_t spec_off;  // double2: spectrum, tile-major [L/NL][P0][NL]
+    // scratch pools (double2): this term's forward (S) / inverse (T) region for vector 0 and the
+    // per-vector stride; rows of a region are planes of P1 * W (3-D) or W (2-D) values
+    int64_t s_pool, s_vst, t_pool, t_vst;
+    int32_t P1;        // axis-1 FFT size of the term (3-D plane stride); 1 in 2-D
+    int32_t pad_;
 };
 
 // rows_inv gather list entry: one C2R line of T contributing to one output line.
 // Self-contained (precomputed at create) so the gather issues no dependent loads.
 struct GatherEntry {
-    int32_t slot;     // term slot within the launch chunk (T item = slot * B + vec)
     int32_t lo, hi;   // output positions [lo, hi) along the last axis (domain-relative, clipped)
     int32_t sh;       // line index of output position p is p - sh
-    int64_t t_off;    // double2 offset of the line inside the item's T buffer
+    int32_t pad_;
+    int64_t t_off;    // double2 offset of the line in the T pool for vector 0
+    int64_t t_vst;    // ... plus t_vst per vector
     int64_t w_off;    // adjoint: w_pool offset of the multiplying w row shifted by -sh; else -1
+    double scale;     // 1 / prod P of the entry's term (its group's FFT size)
 };
 
 // Everything one pipeline pass needs.  D in {2, 3}: axes 0..D-1, last axis is
@@ -47,8 +54,9 @@ struct PassArgs {
     int64_t dom_lo[3];
     int32_t n[3];          // domain extents
     int32_t P[3];          // FFT sizes (P[D-1] is the real axis)
-    int32_t W;             // padded half-spectrum row: roundup(P_last/2+1, 4)
+    int32_t W;             // padded half-spectrum row: roundup(P_last/2+1, 8)
     int64_t L;             // lines of the axis-0 pass: W (2D) or P1*W (3D)
+    int32_t lines_max;     // rows_fwd: max lines of one item over the launch's terms
     int32_t nl_cols;       // spectrum tile width
     const TermDesc* terms; // device
     const int32_t* slots;  // device: term ids of this chunk
@@ -59,10 +67,9 @@ struct PassArgs {
     const double* in;      // B x N input vectors (vector-major)
     double* out;           // B x N output vectors
     int64_t N;             // points per vector
-    double2* S;            // forward scratch, per item stride S_stride
-    int64_t S_stride;
-    double2* T;            // inverse scratch, per item stride T_stride
-    int64_t T_stride;
+    double2* S;            // forward scratch pool (term regions: TermDesc::s_pool / s_vst)
+    int64_t S_stride;      // spectra build only: per-term stride of the full P0 x L transform
+    double2* T;            // inverse scratch pool (TermDesc::t_pool / t_vst)
     const double* w_pool;
     const double* phi_pool;
     double2* spec_pool;

@@ -109,31 +109,35 @@ struct HBox {
     bool empty = false;
 };
 
-struct Csr {  // rows_inv gather list over the active output lines of one chunk
+struct Csr {  // rows_inv gather list over the active output lines of one class
     int64_t n_lines = 0;
     DevBuf<int64_t> ptr, ids;
     DevBuf<int32_t> rng;
     DevBuf<GatherEntry> en;
 };
 
-struct Chunk {
-    int first = 0, count = 0;
-    DevBuf<int32_t> slots;
-    Csr apply, adj;
-};
-
+// Terms with the same full FFT shape: the axis-0 (cols) and axis-1 (mid) passes and the spectra.
 struct Group {
     int P[3] = {1, 1, 1};
     int W = 0;
-    int64_t L = 0;
-    int nl = 0;
-    int64_t Lt = 0;  // L rounded up to the spectrum tile width
+    int64_t L = 0;   // axis-0 lines: W (2-D) or P1 * W (3-D)
+    int nl = 0;      // spectrum tile width
+    int64_t Lt = 0;  // L rounded up to the tile width
     std::vector<int> terms;
-    int m0max = 0, o0max = 0;
-    // per-item strides (double2) for each pass family
-    int64_t S_apply = 0, T_apply = 0, S_adj = 0, T_adj = 0, S_spec = 0;
-    int vb = 1;  // vectors per pass
-    std::vector<Chunk> chunks;
+    DevBuf<int32_t> slots;
+};
+
+// Terms with the same last-axis length: the row passes (R2C / gathered C2R) run per class, so
+// the gather sees every term of the class at once (one read-modify-write of g per class).
+struct Class {
+    int P_last = 0;
+    int W = 0;
+    std::vector<int> terms;
+    std::vector<int> groups;
+    DevBuf<int32_t> slots;
+    int lines_apply = 1, lines_adj = 1;  // max rows_fwd lines per item
+    int P0max = 1, P1max = 1;
+    Csr apply, adj;
 };
 
 std::atomic<long long> g_launches{0};
@@ -158,12 +162,11 @@ struct pcb_op {
     pcb::DevBuf<double> w_pool, phi_pool;
     pcb::DevBuf<double2> spec_pool, tw;
     std::vector<pcb::Group> groups;
-    pcb::DevBuf<double2> S, T, T2;  // T2: second inverse buffer of the two-stream local pipeline
-    cudaStream_t sA = nullptr, sB = nullptr;
+    std::vector<pcb::Class> classes;
+    int vb = 1;                 // vectors per pass (scratch pools are sized for vb vectors)
+    pcb::DevBuf<double2> S, T;  // scratch pools
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // host-buffer calls: copy streams
     cudaEvent_t ev_io[8] = {};
-    bool pipeline = false;  // two-stream local pipeline (PCB_PIPELINE=1 enables; measured no gain on c3)
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_cols[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
     // entry gather
     int32_t bucket[3] = {1, 1, 1}, nb[3] = {1, 1, 1};
     pcb::DevBuf<int64_t> bucket_ptr;
@@ -220,17 +223,17 @@ void make_twiddles(pcb_op* op) {
     op->tw.upload(h);
 }
 
-PassArgs base_args(pcb_op* op, const Group& g) {
+PassArgs base_args(pcb_op* op, const int* P, int W, int64_t L, int nl) {
     PassArgs a{};
     a.D = op->D;
     for (int i = 0; i < 3; ++i) {
         a.dom_lo[i] = op->dom_lo[i];
         a.n[i] = op->n[i];
-        a.P[i] = g.P[i];
+        a.P[i] = P[i];
     }
-    a.W = g.W;
-    a.L = g.L;
-    a.nl_cols = g.nl;
+    a.W = W;
+    a.L = L;
+    a.nl_cols = nl;
     a.terms = op->d_terms.p;
     a.gdesc = op->d_gdesc.p;
     a.N = op->N;
@@ -241,8 +244,15 @@ PassArgs base_args(pcb_op* op, const Group& g) {
     a.spec_pool = op->spec_pool.p;
     a.tw = op->tw.p;
     double sc = 1.0;
-    for (int i = 0; i < op->D; ++i) sc /= (double)g.P[i];
+    for (int i = 0; i < op->D; ++i) sc /= (double)P[i];
     a.scale = sc;
+    return a;
+}
+PassArgs group_args(pcb_op* op, const Group& g) { return base_args(op, g.P, g.W, g.L, g.nl); }
+PassArgs class_args(pcb_op* op, const Class& c) {
+    int P[3] = {c.P0max, c.P1max, 1};
+    P[op->D - 1] = c.P_last;
+    PassArgs a = base_args(op, P, c.W, op->D == 2 ? c.W : (int64_t)c.P1max * c.W, 0);
     return a;
 }
 
@@ -279,15 +289,17 @@ void launch(pcb_op* op, cudaStream_t st, const char* what, Fn&& fn) {
 // ---------------------------------------------------------------------------
 // planning
 
-void build_csr(pcb_op* op, Group& g, Chunk& c, bool global) {
+void build_csr(pcb_op* op, Class& c, bool global, const std::vector<double>& term_scale) {
     const int D = op->D;
+    const int ax = D - 1;
     const int64_t n_lines = D == 2 ? op->n[0] : (int64_t)op->n[0] * op->n[1];
     auto line_of = [&](int64_t c0, int64_t c1) {  // absolute coordinates of the lead axes
         return D == 2 ? c0 - op->dom_lo[0] : (c0 - op->dom_lo[0]) * op->n[1] + (c1 - op->dom_lo[1]);
     };
-    const int ax = D - 1;
     // entry's output range along the last axis (domain-relative) and its line shift
     auto finish = [&](GatherEntry& e, const TermDesc& t, bool adjoint, int64_t w_row) {
+        const int64_t k = &t - op->terms.data();
+        e.scale = (k >= 0 && k < (int64_t)op->terms.size()) ? term_scale[k] : term_scale.back();
         if (!adjoint) {
             e.sh = (int)(t.s[ax] - op->dom_lo[ax]);
             e.lo = e.sh + t.o_lo[ax];
@@ -303,15 +315,16 @@ void build_csr(pcb_op* op, Group& g, Chunk& c, bool global) {
         e.hi = std::min(e.hi, op->n[ax]);
     };
     std::vector<std::vector<GatherEntry>> ap(n_lines), ad(n_lines);
-    for (int i = 0; i < c.count; ++i) {
-        const TermDesc& t = op->terms[g.terms[c.first + i]];
+    for (int k : c.terms) {
+        const TermDesc& t = op->terms[k];
+        const int64_t plane = D == 2 ? c.W : (int64_t)t.P1 * c.W;
         // adjoint: output on X_k (u ranges), T lines u0 [, u1]
         const int c1n = D == 3 ? t.m[1] : 1;
         for (int u0 = 0; u0 < t.m[0]; ++u0)
             for (int u1 = 0; u1 < c1n; ++u1) {
                 GatherEntry e{};
-                e.slot = i;
-                e.t_off = (int64_t)u0 * g.L + (D == 3 ? (int64_t)u1 * g.W : 0);
+                e.t_off = t.t_pool + (int64_t)u0 * plane + (int64_t)u1 * c.W;
+                e.t_vst = t.t_vst;
                 finish(e, t, true, D == 3 ? u0 * t.m[1] + u1 : u0);
                 ad[line_of(t.x_lo[0] + u0, D == 3 ? t.x_lo[1] + u1 : 0)].push_back(e);
             }
@@ -320,8 +333,8 @@ void build_csr(pcb_op* op, Group& g, Chunk& c, bool global) {
             for (int j0 = 0; j0 < t.o_cnt[0]; ++j0)
                 for (int j1 = 0; j1 < o1n; ++j1) {
                     GatherEntry e{};
-                    e.slot = i;
-                    e.t_off = (int64_t)j0 * g.L + (D == 3 ? (int64_t)j1 * g.W : 0);
+                    e.t_off = t.t_pool + (int64_t)j0 * plane + (int64_t)j1 * c.W;
+                    e.t_vst = t.t_vst;
                     finish(e, t, false, 0);
                     const int64_t y0 = t.s[0] + t.o_lo[0] + j0;
                     const int64_t y1 = D == 3 ? t.s[1] + t.o_lo[1] + j1 : 0;
@@ -330,13 +343,15 @@ void build_csr(pcb_op* op, Group& g, Chunk& c, bool global) {
         }
     }
     if (global) {
+        const TermDesc& g = op->gdesc;
+        const int64_t plane = D == 2 ? c.W : (int64_t)g.P1 * c.W;
         for (int64_t ln = 0; ln < n_lines; ++ln) {
             GatherEntry e{};
-            e.slot = 0;
             const int64_t j0 = D == 2 ? ln : ln / op->n[1];
             const int64_t j1 = D == 2 ? 0 : ln % op->n[1];
-            e.t_off = j0 * g.L + j1 * g.W;
-            finish(e, op->gdesc, false, 0);
+            e.t_off = g.t_pool + j0 * plane + j1 * c.W;
+            e.t_vst = g.t_vst;
+            finish(e, g, false, 0);
             ap[ln].push_back(e);
         }
     }
@@ -602,25 +617,29 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             gd.m[a] = gd.o_cnt[a];
         }
     }
-    // groups
+    // groups (full FFT shape) and classes (last-axis length)
     std::map<std::vector<int>, int> gid;
+    std::map<int, int> cid;
     for (int k : mine) {
         std::vector<int> key(3, 1);
         for (int a = 0; a < D; ++a) key[a] = (int)(mode == PCB_MODE_GLOBAL ? Pg[a] : local_P(k, a));
         auto it = gid.find(key);
-        int id;
         if (it == gid.end()) {
-            id = (int)op->groups.size();
-            gid.emplace(key, id);
+            it = gid.emplace(key, (int)op->groups.size()).first;
             op->groups.emplace_back();
-            Group& g = op->groups.back();
-            for (int a = 0; a < 3; ++a) g.P[a] = key[a];
-        } else {
-            id = it->second;
+            for (int a = 0; a < 3; ++a) op->groups.back().P[a] = key[a];
+            auto ct = cid.find(key[D - 1]);
+            if (ct == cid.end()) {
+                ct = cid.emplace(key[D - 1], (int)op->classes.size()).first;
+                op->classes.emplace_back();
+                op->classes.back().P_last = key[D - 1];
+            }
+            op->classes[ct->second].groups.push_back(it->second);
         }
-        op->groups[id].terms.push_back(k);
+        op->groups[it->second].terms.push_back(k);
+        op->classes[cid[key[D - 1]]].terms.push_back(k);
     }
-    // layout per group
+    // layout: spectra per group; scratch regions per term (pools reused class by class)
     int64_t spec_total = 0;
     for (Group& g : op->groups) {
         const int last = g.P[D - 1];
@@ -630,87 +649,103 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
         if (g.nl <= 0) fail(PCB_EINTERNAL, "unsupported FFT size");
         g.Lt = (g.L + g.nl - 1) / g.nl * g.nl;
         for (int k : g.terms) {
-            const TermDesc& t = op->terms[k];
-            g.m0max = std::max(g.m0max, t.m[0]);
-            g.o0max = std::max(g.o0max, t.o_cnt[0]);
-        }
-        for (int k : g.terms) {
             op->terms[k].spec_off = spec_total;
+            op->terms[k].P1 = D == 3 ? g.P[1] : 1;
             spec_total += (int64_t)g.P[0] * g.Lt;
         }
     }
+    op->gdesc.P1 = D == 3 && !op->groups.empty() ? op->groups[0].P[1] : 1;
     op->spec_pool.alloc((size_t)std::max<int64_t>(spec_total, 1));
     PCB_CK(cudaMemset(op->spec_pool.p, 0, op->spec_pool.bytes()));
 
-    // scratch budget and chunking
     size_t freeb = 0, totb = 0;
     PCB_CK(cudaMemGetInfo(&freeb, &totb));
-    int64_t budget = opt.scratch_bytes > 0 ? opt.scratch_bytes : std::min<int64_t>((int64_t)freeb / 3, 8LL << 30);
+    int64_t budget = opt.scratch_bytes > 0 ? opt.scratch_bytes : std::min<int64_t>((int64_t)freeb / 3, 16LL << 30);
     budget = std::max<int64_t>(budget, 64LL << 20);
-    const int mb = op->max_batch;
-    int64_t S_need = 0, T_need = 0;
-    for (Group& g : op->groups) {
-        const int64_t plane = g.L;
-        const int64_t n0 = op->n[0];
-        if (mode == PCB_MODE_LOCAL) {
-            g.S_apply = (int64_t)g.m0max * plane;
-            g.T_apply = (int64_t)g.o0max * plane;
-            g.S_adj = (int64_t)g.o0max * plane;
-            g.T_adj = (int64_t)g.m0max * plane;
-            const int64_t per_item = 16 * (std::max(g.S_apply, g.S_adj) + std::max(g.T_apply, g.T_adj));
-            int per_chunk = (int)std::max<int64_t>(1, budget / std::max<int64_t>(1, (op->pipeline ? 2 : 1) * per_item * mb));
-            per_chunk = std::min<int>(per_chunk, std::max(1, 65535 / mb));
-            // at least two chunks per group so the two-stream pipeline has something to overlap
-            if (op->pipeline) per_chunk = std::min<int>(per_chunk, std::max<int>(1, ((int)g.terms.size() + 1) / 2));
-            if (const char* e = getenv("PCB_CHUNK_TERMS")) per_chunk = std::max(1, atoi(e));
-            g.vb = mb;
-            for (int f = 0; f < (int)g.terms.size(); f += per_chunk) {
-                g.chunks.emplace_back();
-                g.chunks.back().first = f;
-                g.chunks.back().count = std::min<int>(per_chunk, (int)g.terms.size() - f);
-            }
-            S_need = std::max<int64_t>(S_need, (int64_t)per_chunk * mb * std::max(g.S_apply, g.S_adj));
-            T_need = std::max<int64_t>(T_need, (int64_t)per_chunk * mb * std::max(g.T_apply, g.T_adj));
-        } else {
-            const int64_t nt = (int64_t)g.terms.size();
-            g.S_apply = (int64_t)g.m0max * plane;
-            g.T_apply = n0 * plane;
-            g.S_adj = n0 * plane;
-            g.T_adj = (int64_t)g.m0max * plane;
-            const int64_t per_vec = 16 * (std::max(nt * g.S_apply, g.S_adj) + std::max(g.T_apply, nt * g.T_adj));
-            int vb = (int)std::max<int64_t>(1, std::min<int64_t>(mb, budget / std::max<int64_t>(1, per_vec)));
-            vb = std::min<int>(vb, std::max<int>(1, (int)(65535 / std::max<int64_t>(1, nt))));
-            g.vb = vb;
-            g.chunks.emplace_back();
-            g.chunks.back().first = 0;
-            g.chunks.back().count = (int)nt;
-            S_need = std::max<int64_t>(S_need, std::max(nt * vb * g.S_apply, (int64_t)vb * g.S_adj));
-            T_need = std::max<int64_t>(T_need, std::max((int64_t)vb * g.T_apply, nt * vb * g.T_adj));
+    // per-vector pool sizes: LOCAL: per class, sum over its terms of S and T regions; GLOBAL: term
+    // regions (S in apply, T in adjoint) in pool S, the shared full-grid region in pool T
+    int64_t s_per_vec = 0, t_per_vec = 0, spec_item = 1;
+    for (Class& c : op->classes) {
+        c.W = op->groups[c.groups[0]].W;
+        int64_t s_sum = 0, t_sum = 0;
+        for (int k : c.terms) {
+            const TermDesc& t = op->terms[k];
+            const int64_t plane = D == 2 ? c.W : (int64_t)t.P1 * c.W;
+            const int64_t reg = (int64_t)std::max(t.m[0], t.o_cnt[0]) * plane;
+            s_sum += mode == PCB_MODE_GLOBAL ? (int64_t)t.m[0] * plane : reg;
+            t_sum += mode == PCB_MODE_GLOBAL ? 0 : reg;
+            c.lines_apply = std::max<int>(c.lines_apply, D == 2 ? t.m[0] : t.m[0] * t.m[1]);
+            c.lines_adj = std::max<int>(c.lines_adj, D == 2 ? t.o_cnt[0] : t.o_cnt[0] * t.o_cnt[1]);
+            c.P1max = std::max(c.P1max, t.P1);
         }
-        // K1 scratch: at least one full P0 x L item
-        g.S_spec = (int64_t)g.P[0] * plane;
-        S_need = std::max<int64_t>(S_need, g.S_spec);
+        for (int gi : c.groups) c.P0max = std::max(c.P0max, op->groups[gi].P[0]);
+        if (mode == PCB_MODE_GLOBAL) {
+            const int64_t plane = D == 2 ? c.W : (int64_t)op->gdesc.P1 * c.W;
+            t_sum = (int64_t)op->n[0] * plane;
+            c.lines_adj = D == 2 ? op->n[0] : op->n[0] * op->n[1];
+        }
+        s_per_vec = std::max(s_per_vec, s_sum);
+        t_per_vec = std::max(t_per_vec, t_sum);
     }
-    op->S.alloc((size_t)std::max<int64_t>(S_need, 1));
-    op->T.alloc((size_t)std::max<int64_t>(T_need, 1));
+    for (const Group& g : op->groups) spec_item = std::max<int64_t>(spec_item, (int64_t)g.P[0] * g.L);
+    const int64_t per_vec_bytes = 16 * (s_per_vec + t_per_vec);
+    int vb = (int)std::max<int64_t>(1, std::min<int64_t>(op->max_batch, budget / std::max<int64_t>(1, per_vec_bytes)));
+    int64_t max_items = 1;
+    for (const Class& c : op->classes) max_items = std::max<int64_t>(max_items, (int64_t)c.terms.size());
+    vb = std::min<int>(vb, std::max<int>(1, (int)(65535 / max_items)));
+    if (const char* e = getenv("PCB_VB")) vb = std::max(1, atoi(e));
+    op->vb = vb;
+    // assign pool offsets (vector v of term k at pool + v * vst)
+    for (Class& c : op->classes) {
+        int64_t so = 0, to = 0;
+        for (int k : c.terms) {
+            TermDesc& t = op->terms[k];
+            const int64_t plane = D == 2 ? c.W : (int64_t)t.P1 * c.W;
+            const int64_t reg = mode == PCB_MODE_GLOBAL ? (int64_t)t.m[0] * plane
+                                                        : (int64_t)std::max(t.m[0], t.o_cnt[0]) * plane;
+            t.s_pool = so;
+            t.s_vst = reg;
+            so += reg * vb;
+            if (mode == PCB_MODE_GLOBAL) {  // the term region doubles as the adjoint's T region
+                t.t_pool = t.s_pool;
+                t.t_vst = t.s_vst;
+            } else {
+                t.t_pool = to;
+                t.t_vst = reg;
+                to += reg * vb;
+            }
+        }
+    }
+    if (mode == PCB_MODE_GLOBAL) {
+        TermDesc& g = op->gdesc;
+        const int64_t W = op->classes.empty() ? 8 : op->classes[0].W;
+        const int64_t plane = D == 2 ? W : (int64_t)g.P1 * W;
+        g.s_pool = g.t_pool = 0;
+        g.s_vst = g.t_vst = (int64_t)op->n[0] * plane;
+    }
+    op->S.alloc((size_t)std::max<int64_t>({s_per_vec * vb, spec_item, 1}));
+    op->T.alloc((size_t)std::max<int64_t>(t_per_vec * vb, 1));
     PCB_CK(cudaMemset(op->S.p, 0, op->S.bytes()));
     PCB_CK(cudaMemset(op->T.p, 0, op->T.bytes()));
-    if (mode == PCB_MODE_LOCAL && op->pipeline) {
-        op->T2.alloc((size_t)std::max<int64_t>(T_need, 1));
-        PCB_CK(cudaMemset(op->T2.p, 0, op->T2.bytes()));
-    }
 
-    // device descriptors and pools
+    // device descriptors, pools and gather lists
     op->d_terms.upload(op->terms.empty() ? std::vector<TermDesc>(1) : op->terms);
     op->d_gdesc.upload(std::vector<TermDesc>{op->gdesc});
     op->w_pool.upload(wpool);
     op->phi_pool.upload(ppool);
-    for (Group& g : op->groups)
-        for (Chunk& c : g.chunks) {
-            std::vector<int32_t> sl(g.terms.begin() + c.first, g.terms.begin() + c.first + c.count);
-            c.slots.upload(sl);
-            build_csr(op, g, c, mode == PCB_MODE_GLOBAL);
-        }
+    for (Group& g : op->groups) g.slots.upload(std::vector<int32_t>(g.terms.begin(), g.terms.end()));
+    // 1 / prod P per term (its group's FFT size); the last slot serves the global pseudo term
+    std::vector<double> term_scale(op->terms.size() + 1, 1.0);
+    for (const Group& g : op->groups) {
+        double sc = 1.0;
+        for (int a = 0; a < D; ++a) sc /= (double)g.P[a];
+        for (int k : g.terms) term_scale[k] = sc;
+        term_scale.back() = sc;
+    }
+    for (Class& c : op->classes) {
+        c.slots.upload(std::vector<int32_t>(c.terms.begin(), c.terms.end()));
+        build_csr(op, c, mode == PCB_MODE_GLOBAL, term_scale);
+    }
 
     // entry buckets over all terms with X and K
     {
@@ -777,24 +812,21 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     in.spectra_bytes = (int64_t)(16.0 * (double)spec_total);
     in.bytes_per_vector = sb + 16.0 * (double)op->N;
     in.flops_per_vector = mode == PCB_MODE_GLOBAL ? g_fl : l_fl;
-    int launches = 0;
-    for (const Group& g : op->groups) launches += (int)g.chunks.size() * (D == 3 ? 5 : 3);
-    in.launches_per_batch = launches;
+    in.launches_per_batch = (int)(2 * op->classes.size() + op->groups.size() * (D == 3 ? 3 : 1));
 }
 
 void build_spectra(pcb_op* op) {
     const int D = op->D;
     for (Group& g : op->groups) {
-        PassArgs a = base_args(op, g);
-        const int64_t per = std::max<int64_t>(1, (int64_t)(op->S.n / (size_t)g.S_spec));
-        DevBuf<int32_t> slots;
-        slots.upload(g.terms);
+        PassArgs a = group_args(op, g);
+        const int64_t item = (int64_t)g.P[0] * g.L;
+        const int64_t per = std::max<int64_t>(1, (int64_t)(op->S.n / (size_t)item));
         for (int64_t f = 0; f < (int64_t)g.terms.size(); f += per) {
             const int cnt = (int)std::min<int64_t>(per, (int64_t)g.terms.size() - f);
-            a.slots = slots.p + f;
+            a.slots = g.slots.p + f;
             a.n_slots = cnt;
             a.B = 1;
-            a.S_stride = g.S_spec;
+            a.S_stride = item;
             a.global = 0;
             launch_ck(launch_rows_fwd(a, RF_SPEC, op->stream), "rows_fwd(spec)");
             if (D == 3) launch_ck(launch_mid(a, MM_FWD_SPEC, op->stream), "mid(spec)");
@@ -804,114 +836,70 @@ void build_spectra(pcb_op* op) {
     }
 }
 
-// one apply / adjoint batch on device pointers.
-// GLOBAL: one chunk per vector block, on the caller's stream.
-// LOCAL: chunks of terms flow through a two-stream pipeline forked from the caller's stream:
-//   stream A: rows_fwd(i) -> [mid] -> cols(i) -> [mid_inv] (writes T[i % 2]) -> event cols[i % 2]
-//   stream B: wait cols[i % 2] -> rows_inv(i) (reads T[i % 2], accumulates into g) -> event done[i % 2]
-// stream A waits done[i % 2] before overwriting T[i % 2] again; rows_inv launches stay in chunk
-// order on stream B, so the accumulation order (and the result) is fixed.
+// One apply / adjoint batch on device pointers, ordered on the caller's stream.  Per block of
+// vb vectors and per class: rows_fwd (all class terms) -> per group [mid] cols [mid_inv] ->
+// rows_inv (all class terms, fixed ascending-k order per output line, accumulated into g).
 void run_batch(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG, cudaStream_t st) {
     const int D = op->D;
-    if (op->groups.empty()) {
+    if (op->classes.empty()) {
         launch(op, st, "zero", [&] { return launch_zero(dG, (int64_t)B * op->N, st); });
         return;
     }
     const bool global = op->mode == PCB_MODE_GLOBAL;
-    auto pass_args = [&](const Group& g, const Chunk& c, int b0, int bn, double2* T) {
-        PassArgs a = base_args(op, g);
-        a.slots = c.slots.p;
-        a.n_slots = c.count;
-        a.B = bn;
-        a.in = dF + (int64_t)b0 * op->N;
-        a.out = dG + (int64_t)b0 * op->N;
-        a.T = T;
-        a.S_stride = adjoint ? g.S_adj : g.S_apply;
-        a.T_stride = adjoint ? g.T_adj : g.T_apply;
-        return a;
-    };
-    auto front = [&](PassArgs a, cudaStream_t s) {  // K2 + K3 (+ 3-D middle passes)
-        a.global = global;
-        if (!adjoint) {
-            launch(op, s, "rows_fwd(apply)", [&] { return launch_rows_fwd(a, RF_APPLY, s); });
-            if (D == 3) launch(op, s, "mid(fwd apply)", [&] { return launch_mid(a, MM_FWD_APPLY, s); });
-            launch(op, s, global ? "cols(apply,global)" : "cols(apply,local)",
-                   [&] { return launch_cols(a, global ? CM_APPLY_GLOBAL : CM_APPLY_LOCAL, s); });
-            if (D == 3) launch(op, s, "mid(inv apply)", [&] { return launch_mid(a, MM_INV_APPLY, s); });
-        } else {
-            launch(op, s, "rows_fwd(adjoint)", [&] { return launch_rows_fwd(a, RF_ADJ, s); });
-            if (D == 3) launch(op, s, "mid(fwd adjoint)", [&] { return launch_mid(a, MM_FWD_ADJ, s); });
-            launch(op, s, global ? "cols(adjoint,global)" : "cols(adjoint,local)",
-                   [&] { return launch_cols(a, global ? CM_ADJ_GLOBAL : CM_ADJ_LOCAL, s); });
-            a.global = 0;
-            if (D == 3) launch(op, s, "mid(inv adjoint)", [&] { return launch_mid(a, MM_INV_ADJ, s); });
-        }
-    };
-    auto back = [&](PassArgs a, const Chunk& c, cudaStream_t s, bool accumulate) {  // K4
-        const Csr& csr = adjoint ? c.adj : c.apply;
-        a.global = global && !adjoint;
-        a.accumulate = accumulate ? 1 : 0;
-        a.line_ptr = csr.ptr.p;
-        a.line_id = csr.ids.p;
-        a.line_rng = csr.rng.p;
-        a.entries = csr.en.p;
-        if (csr.n_lines > 0)
-            launch(op, s, adjoint ? "rows_inv(adjoint)" : "rows_inv(apply)",
-                   [&] { return launch_rows_inv(a, adjoint ? RI_ADJ : RI_APPLY, csr.n_lines, s); });
-    };
-
-    if (global) {
-        const Group& g = op->groups[0];
-        const Chunk& c = g.chunks[0];
-        for (int b0 = 0; b0 < B; b0 += g.vb) {
-            const int bn = std::min(g.vb, B - b0);
-            if (adjoint)
-                PCB_CK(cudaMemsetAsync(dG + (int64_t)b0 * op->N, 0, (size_t)bn * op->N * sizeof(double), st));
-            PassArgs a = pass_args(g, c, b0, bn, op->T.p);
-            front(a, st);
-            back(a, c, st, adjoint);
-        }
-        return;
-    }
-
-    // LOCAL: fork the two pipeline streams off the caller's stream
-    PCB_CK(cudaEventRecord(op->ev_fork, st));
-    PCB_CK(cudaStreamWaitEvent(op->sA, op->ev_fork, 0));
-    PCB_CK(cudaStreamWaitEvent(op->sB, op->ev_fork, 0));
-    PCB_CK(cudaMemsetAsync(dG, 0, (size_t)B * op->N * sizeof(double), op->sB));
-    int64_t i = 0;
-    int vb = op->max_batch;
-    for (const Group& g : op->groups) vb = std::min(vb, g.vb);
-    for (int b0 = 0; b0 < B; b0 += vb) {
-        const int bn = std::min(vb, B - b0);
-        for (const Group& g : op->groups) {
-            for (const Chunk& c : g.chunks) {
-                const int par = (int)(i & 1);
-                double2* T = (par && op->pipeline) ? op->T2.p : op->T.p;
-                if (i >= 2 && op->pipeline) PCB_CK(cudaStreamWaitEvent(op->sA, op->ev_done[par], 0));
-                PassArgs a = pass_args(g, c, b0, bn, T);
-                front(a, op->sA);
-                if (op->pipeline) {
-                    PCB_CK(cudaEventRecord(op->ev_cols[par], op->sA));
-                    PCB_CK(cudaStreamWaitEvent(op->sB, op->ev_cols[par], 0));
-                    back(a, c, op->sB, true);
-                    PCB_CK(cudaEventRecord(op->ev_done[par], op->sB));
+    // LOCAL and every adjoint accumulate into g; GLOBAL apply writes every output line once
+    const bool accumulate = !global || adjoint;
+    if (accumulate) PCB_CK(cudaMemsetAsync(dG, 0, (size_t)B * op->N * sizeof(double), st));
+    // GLOBAL adjoint: the g transform lives in pool T, the per-term inverse regions in pool S
+    double2* poolS = global && adjoint ? op->T.p : op->S.p;
+    double2* poolT = global && adjoint ? op->S.p : op->T.p;
+    for (int b0 = 0; b0 < B; b0 += op->vb) {
+        const int bn = std::min(op->vb, B - b0);
+        for (const Class& c : op->classes) {
+            PassArgs a = class_args(op, c);
+            a.B = bn;
+            a.in = dF + (int64_t)b0 * op->N;
+            a.out = dG + (int64_t)b0 * op->N;
+            a.S = poolS;
+            a.T = poolT;
+            a.slots = c.slots.p;
+            a.n_slots = (int)c.terms.size();
+            a.global = global;
+            a.lines_max = adjoint ? c.lines_adj : c.lines_apply;
+            launch(op, st, adjoint ? "rows_fwd(adjoint)" : "rows_fwd(apply)",
+                   [&] { return launch_rows_fwd(a, adjoint ? RF_ADJ : RF_APPLY, st); });
+            for (int gi : c.groups) {
+                const Group& g = op->groups[gi];
+                PassArgs ga = group_args(op, g);
+                ga.B = bn;
+                ga.S = poolS;
+                ga.T = poolT;
+                ga.slots = g.slots.p;
+                ga.n_slots = (int)g.terms.size();
+                ga.global = global;
+                if (!adjoint) {
+                    if (D == 3) launch(op, st, "mid(fwd apply)", [&] { return launch_mid(ga, MM_FWD_APPLY, st); });
+                    launch(op, st, global ? "cols(apply,global)" : "cols(apply,local)",
+                           [&] { return launch_cols(ga, global ? CM_APPLY_GLOBAL : CM_APPLY_LOCAL, st); });
+                    if (D == 3) launch(op, st, "mid(inv apply)", [&] { return launch_mid(ga, MM_INV_APPLY, st); });
                 } else {
-                    if (i == 0) {
-                        PCB_CK(cudaEventRecord(op->ev_done[0], op->sB));
-                        PCB_CK(cudaStreamWaitEvent(op->sA, op->ev_done[0], 0));
-                    }
-                    back(a, c, op->sA, true);
+                    if (D == 3) launch(op, st, "mid(fwd adjoint)", [&] { return launch_mid(ga, MM_FWD_ADJ, st); });
+                    launch(op, st, global ? "cols(adjoint,global)" : "cols(adjoint,local)",
+                           [&] { return launch_cols(ga, global ? CM_ADJ_GLOBAL : CM_ADJ_LOCAL, st); });
+                    ga.global = 0;
+                    if (D == 3) launch(op, st, "mid(inv adjoint)", [&] { return launch_mid(ga, MM_INV_ADJ, st); });
                 }
-                ++i;
             }
+            const Csr& csr = adjoint ? c.adj : c.apply;
+            a.accumulate = accumulate ? 1 : 0;
+            a.line_ptr = csr.ptr.p;
+            a.line_id = csr.ids.p;
+            a.line_rng = csr.rng.p;
+            a.entries = csr.en.p;
+            if (csr.n_lines > 0)
+                launch(op, st, adjoint ? "rows_inv(adjoint)" : "rows_inv(apply)",
+                       [&] { return launch_rows_inv(a, adjoint ? RI_ADJ : RI_APPLY, csr.n_lines, st); });
         }
     }
-    // join: the caller's stream waits for both pipeline streams
-    PCB_CK(cudaEventRecord(op->ev_join, op->sA));
-    PCB_CK(cudaStreamWaitEvent(st, op->ev_join, 0));
-    PCB_CK(cudaEventRecord(op->ev_join, op->sB));
-    PCB_CK(cudaStreamWaitEvent(st, op->ev_join, 0));
 }
 
 EntryArgs entry_args(pcb_op* op) {
@@ -990,13 +978,9 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
         PCB_CK(cudaGetDeviceProperties(&prop, op->device));
         if (prop.major < 10) fail(PCB_ECUDA, "pcop-b200 kernels are built for sm_100a (Blackwell B200)");
         op->max_batch = opt.max_batch > 0 ? opt.max_batch : 16;
-        if (const char* e = getenv("PCB_PIPELINE")) op->pipeline = atoi(e) != 0;
+
         PCB_CK(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
-        PCB_CK(cudaStreamCreateWithFlags(&op->sA, cudaStreamNonBlocking));
-        PCB_CK(cudaStreamCreateWithFlags(&op->sB, cudaStreamNonBlocking));
-        for (cudaEvent_t* e : {&op->ev_fork, &op->ev_join, &op->ev_cols[0], &op->ev_cols[1], &op->ev_done[0],
-                               &op->ev_done[1]})
-            PCB_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+
         make_twiddles(op);
         plan(op, dim, dom_lo, dom_hi, r, w_lo, w_hi, w_vals, phi_lo, phi_hi, phi_vals, opt);
         build_spectra(op);
@@ -1027,13 +1011,11 @@ PCB_API pcb_status pcb_destroy(pcb_op* op) {
     for (auto e : op->ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : op->ev_io)
         if (e) cudaEventDestroy(e);
-    for (cudaStream_t s : {op->sA, op->sB, op->s_h2d, op->s_d2h})
+    for (cudaStream_t s : {op->s_h2d, op->s_d2h})
         if (s) {
             cudaStreamSynchronize(s);
             cudaStreamDestroy(s);
         }
-    for (cudaEvent_t e : {op->ev_fork, op->ev_join, op->ev_cols[0], op->ev_cols[1], op->ev_done[0], op->ev_done[1]})
-        if (e) cudaEventDestroy(e);
     delete op;
     return PCB_OK;
 }
