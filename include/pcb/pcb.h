@@ -122,6 +122,15 @@ PCB_API pcb_status pcb_blocks_dev(pcb_op* op, int32_t nblk, const int64_t* d_t_o
                                   const int64_t* d_s_origin, const int64_t* block_shape, double* d_out,
                                   void* stream);
 
+/* Replaces ProductConvolutionOperator::apply_block (pc_operator.cpp:98-130), batched over nblk
+ * (T, S) box pairs (each box inclusive, inside the domain): apply g_b = Atilde[T_b, S_b] f_b, or
+ * with adjoint != 0, g_b = (Atilde^*)[T_b, S_b] f_b.  f packs each f_b on S_b (lexicographic)
+ * back to back, g packs each g_b on T_b.  Small blocks use the exact entry gather fused with the
+ * block matvec; blocks with |T||S| > 2^24 use the FFT apply of f_b extended by zero, cropped. */
+PCB_API pcb_status pcb_apply_block(pcb_op* op, int32_t nblk, const int64_t* t_lo, const int64_t* t_hi,
+                                   const int64_t* s_lo, const int64_t* s_hi, const double* f, double* g,
+                                   int32_t adjoint);
+
 /* Randomized a-posteriori estimator (adaptivity.cpp:75-121): Ytilde_i =
  * Atilde^* zeta_i for q probes Z (q x N), eta_abs = sqrt(sum ||Ytilde-Y||^2/q),
  * eta_rel = ||Ytilde-Y||_F / ||Y||_F, eta_cells[c] over leaf box c.  ytilde

@@ -199,6 +199,36 @@ class PCOperator:
             s += wx * self.impulses[k].value_or_zero(z)
         return s
 
+    def apply_block(self, T: Box, S: Box, f: GF, adjoint: bool = False) -> GF:
+        """g on T from f on S via G = T - S kernel slices (pc_operator.cpp:98-130)."""
+        if intersect(self.domain, T) != (tuple(T[0]), tuple(T[1])) or intersect(self.domain, S) != (tuple(S[0]), tuple(S[1])):
+            raise ValueError("PCOp::apply_block: boxes must lie inside the domain")
+        out = GF(T[0], np.zeros(tuple(h - l + 1 for l, h in zip(*T))))
+        G = minkowski_diff(T, S)
+        for k in range(self.rank):
+            w, phi = self.weights[k], self.impulses[k]
+            if not adjoint:
+                if intersect(w.box, S) is None:
+                    continue
+                wf = restrict_to(f, S)  # overwrite into S (zeros outside f's box)
+                wf.values = wf.values * restrict_to(w, S).values  # multiply_into
+                sb = intersect(phi.box, G)
+                if sb is None:
+                    continue
+                accumulate(out, fft_convolve(restrict_to(phi, sb), wf))
+            else:
+                if intersect(w.box, T) is None:
+                    continue
+                sb = intersect(phi.box, minkowski_diff(S, T))
+                if sb is None:
+                    continue
+                conv = fft_convolve(flip(restrict_to(phi, sb)), restrict_to(f, S))
+                ov = intersect(w.box, conv.box)
+                ov = intersect(ov, out.box) if ov is not None else None
+                if ov is not None:
+                    out.values[_sl(ov, out.lo)] += w.values[_sl(ov, w.lo)] * conv.values[_sl(ov, conv.lo)]
+        return out
+
     def dense(self) -> np.ndarray:
         """Dense matrix via apply of basis vectors (verification.cpp:21-33); small N only."""
         N = int(np.prod(self.shape))

@@ -173,6 +173,19 @@ int ref_entries(void* h, std::int64_t cnt, const std::int64_t* y, const std::int
     });
 }
 
+// ProductConvolutionOperator::apply_block (pc_operator.cpp:98-130); f on S, out on T
+int ref_apply_block(void* h, const std::int64_t* t_lo, const std::int64_t* t_hi, const std::int64_t* s_lo,
+                    const std::int64_t* s_hi, const double* f, int adjoint, double* out) {
+    return guarded([&] {
+        auto* o = static_cast<RefOp*>(h);
+        const int d = o->dim;
+        const IndexBox T = make_box(d, t_lo, t_hi), S = make_box(d, s_lo, s_hi);
+        GridFunction fs = make_field(d, s_lo, s_hi, f);
+        GridFunction g = o->op.apply_block(T, S, fs, adjoint != 0);
+        std::memcpy(out, g.data(), static_cast<std::size_t>(g.size()) * sizeof(double));
+    });
+}
+
 int ref_fft_convolve(int dim, const std::int64_t* psi_lo, const std::int64_t* psi_hi,
                      const double* psi, const std::int64_t* f_lo, const std::int64_t* f_hi,
                      const double* f, std::int64_t* out_lo, std::int64_t* out_hi, double* out,

@@ -39,6 +39,7 @@ def lib():
             getattr(L, name).argtypes = [ctypes.c_void_p, _dp, _dp]
         L.ref_apply_batch_threads.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _dp, _dp, ctypes.c_int]
         L.ref_entries.argtypes = [ctypes.c_void_p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _dp]
+        L.ref_apply_block.argtypes = [ctypes.c_void_p] + [ctypes.POINTER(_i64)] * 4 + [_dp, ctypes.c_int, _dp]
         L.ref_estimate.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _dp, ctypes.c_int, ctypes.POINTER(_i64),
                                    ctypes.POINTER(_i64), _dp, _dp, _dp, _dp]
         _lib = L
@@ -115,6 +116,16 @@ class RefOperator:
         _check(lib().ref_entries(self.h, y.shape[0], y.ctypes.data_as(ctypes.POINTER(_i64)),
                                  x.ctypes.data_as(ctypes.POINTER(_i64)), _dptr(out)))
         return out
+
+    def apply_block(self, T, S, f: np.ndarray, adjoint: bool = False) -> np.ndarray:
+        """Reference apply_block (pc_operator.cpp:98-130): f on box S -> g on box T."""
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        shape = tuple(h - l + 1 for l, h in zip(T[0], T[1]))
+        out = np.zeros(int(np.prod(shape)))
+        L = lib()
+        _check(L.ref_apply_block(self.h, _arr(T[0], _i64), _arr(T[1], _i64), _arr(S[0], _i64), _arr(S[1], _i64),
+                                 _dptr(f), int(adjoint), _dptr(out)))
+        return out.reshape(shape)
 
     def estimate(self, Z: np.ndarray, Y: np.ndarray, leaves):
         Z = np.ascontiguousarray(Z, dtype=np.float64)

@@ -545,6 +545,61 @@ __global__ void k_blocks(EntryArgs a, int32_t nblk, const int64_t* __restrict__ 
     }
 }
 
+// Block apply, direct form (pc_operator.cpp:98-130 semantics): for block b,
+//   apply:   g_b[y] = sum_{x in S_b} Atilde[y, x] f_b[x],   y in T_b
+//   adjoint: g_b[x] = sum_{y in S_b} Atilde[y, x] f_b[y],   x in T_b
+// One CTA per (block, tile of 256 outputs); f_b staged in shared memory in chunks.
+__global__ void k_block_direct(EntryArgs a, int32_t nblk, const int64_t* __restrict__ t_lo,
+                               const int64_t* __restrict__ t_hi, const int64_t* __restrict__ s_lo,
+                               const int64_t* __restrict__ s_hi, const int64_t* __restrict__ f_off,
+                               const int64_t* __restrict__ g_off, const double* __restrict__ f,
+                               double* __restrict__ g, int adjoint, int32_t* bad) {
+    const int D = a.D;
+    const int blk = blockIdx.y;
+    if (blk >= nblk) return;
+    int64_t text[3] = {1, 1, 1}, sext[3] = {1, 1, 1}, tcnt = 1, scnt = 1;
+    for (int i = 0; i < D; ++i) {
+        text[i] = t_hi[blk * D + i] - t_lo[blk * D + i] + 1;
+        sext[i] = s_hi[blk * D + i] - s_lo[blk * D + i] + 1;
+        tcnt *= text[i];
+        scnt *= sext[i];
+    }
+    const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t pt[3] = {0, 0, 0};
+    {
+        int64_t r = o < tcnt ? o : 0;
+        for (int i = D - 1; i >= 0; --i) {
+            pt[i] = t_lo[blk * D + i] + r % text[i];
+            r /= text[i];
+        }
+    }
+    __shared__ double fs[512];
+    double sum = 0.0;
+    bool b = false;
+    for (int64_t c0 = 0; c0 < scnt; c0 += 512) {
+        const int cn = (int)((scnt - c0) < 512 ? (scnt - c0) : 512);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cn; i += blockDim.x) fs[i] = f[f_off[blk] + c0 + i];
+        __syncthreads();
+        if (o < tcnt) {
+            for (int j = 0; j < cn; ++j) {
+                const double fv = fs[j];
+                if (fv == 0.0) continue;
+                int64_t ps[3] = {0, 0, 0};
+                int64_t r = c0 + j;
+                for (int i = D - 1; i >= 0; --i) {
+                    ps[i] = s_lo[blk * D + i] + r % sext[i];
+                    r /= sext[i];
+                }
+                const double e = adjoint ? entry_value(a, ps, pt, b) : entry_value(a, pt, ps, b);
+                sum += e * fv;
+            }
+        }
+    }
+    if (o < tcnt) g[g_off[blk] + o] = sum;
+    if (b) atomicOr(bad, 1);
+}
+
 // ---------------------------------------------------------------------------
 // K5 reductions: d2[box, probe] = sum_{p in box cap Omega} (Yt - Y)^2, y2[probe] = sum Y^2
 __global__ void k_probe_sums(int D, int32_t n0, int32_t n1, int32_t n2, int32_t nbox, const int64_t* __restrict__ blo,
@@ -800,6 +855,16 @@ cudaError_t launch_probe_sums(int D, const int32_t* n, int32_t nbox, const int64
                               int32_t q, const double* Yt, const double* Y, double* d2, double* y2, cudaStream_t st) {
     dim3 grid((unsigned)(nbox + 1), (unsigned)q);
     k_probe_sums<<<grid, 256, 0, st>>>(D, n[0], n[1], D == 3 ? n[2] : 1, nbox, box_lo, box_hi, Yt, Y, d2, y2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_block_direct(const EntryArgs& a, int32_t nblk, int64_t max_t, const int64_t* t_lo,
+                                const int64_t* t_hi, const int64_t* s_lo, const int64_t* s_hi, const int64_t* f_off,
+                                const int64_t* g_off, const double* f, double* g, int adjoint, int32_t* bad,
+                                cudaStream_t st) {
+    if (nblk <= 0) return cudaSuccess;
+    dim3 grid((unsigned)((max_t + 255) / 256), (unsigned)nblk);
+    k_block_direct<<<grid, 256, 0, st>>>(a, nblk, t_lo, t_hi, s_lo, s_hi, f_off, g_off, f, g, adjoint, bad);
     return cudaGetLastError();
 }
 

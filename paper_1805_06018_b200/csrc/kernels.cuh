@@ -112,6 +112,12 @@ cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, co
 cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
                           const int32_t* bshape, double* out, int32_t* bad, cudaStream_t st);
 
+// block apply, direct form (small blocks)
+cudaError_t launch_block_direct(const EntryArgs& a, int32_t nblk, int64_t max_t, const int64_t* t_lo,
+                                const int64_t* t_hi, const int64_t* s_lo, const int64_t* s_hi, const int64_t* f_off,
+                                const int64_t* g_off, const double* f, double* g, int adjoint, int32_t* bad,
+                                cudaStream_t st);
+
 // estimator reductions (K5): per (box, probe) sums of (Yt - Y)^2 and Y^2
 cudaError_t launch_probe_sums(int D, const int32_t* n, int32_t nbox, const int64_t* box_lo, const int64_t* box_hi,
                               int32_t q, const double* Yt, const double* Y, double* d2, double* y2, cudaStream_t st);

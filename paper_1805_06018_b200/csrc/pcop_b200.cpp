@@ -1192,6 +1192,103 @@ PCB_API pcb_status pcb_blocks_dev(pcb_op* op, int32_t nblk, const int64_t* d_t_o
     });
 }
 
+PCB_API pcb_status pcb_apply_block(pcb_op* op, int32_t nblk, const int64_t* t_lo, const int64_t* t_hi,
+                                   const int64_t* s_lo, const int64_t* s_hi, const double* f, double* g,
+                                   int32_t adjoint) {
+    if (!op) {
+        set_err("null handle");
+        return PCB_EINVAL;
+    }
+    std::lock_guard<std::mutex> lk(op->mu);
+    return guarded([&] {
+        if (nblk < 0) fail(PCB_EINVAL, "pcb_apply_block: negative block count");
+        if (nblk == 0) return;
+        if (!t_lo || !t_hi || !s_lo || !s_hi || !f || !g) fail(PCB_EINVAL, "null pointer");
+        set_device(op);
+        const int D = op->D;
+        std::vector<int64_t> tl = to_internal_points(op, t_lo, nblk), th = to_internal_points(op, t_hi, nblk),
+                             sl = to_internal_points(op, s_lo, nblk), sh = to_internal_points(op, s_hi, nblk);
+        std::vector<int64_t> foff(nblk), goff(nblk);
+        int64_t ftot = 0, gtot = 0, tmax = 1;
+        std::vector<char> big(nblk, 0);
+        for (int32_t b = 0; b < nblk; ++b) {
+            int64_t tc = 1, sc = 1;
+            for (int a = 0; a < D; ++a) {
+                const int64_t lo_t = tl[b * D + a], hi_t = th[b * D + a], lo_s = sl[b * D + a], hi_s = sh[b * D + a];
+                const int64_t dlo = op->dom_lo[a], dhi = op->dom_lo[a] + op->n[a] - 1;
+                if (lo_t > hi_t || lo_s > hi_s) fail(PCB_EINVAL, "IndexBox: lo > hi");
+                if (lo_t < dlo || hi_t > dhi || lo_s < dlo || hi_s > dhi)
+                    fail(PCB_EINVAL, "PCOp::apply_block: boxes must lie inside the domain");
+                tc *= hi_t - lo_t + 1;
+                sc *= hi_s - lo_s + 1;
+            }
+            foff[b] = ftot;
+            goff[b] = gtot;
+            ftot += sc;
+            gtot += tc;
+            tmax = std::max(tmax, tc);
+            big[b] = (double)tc * (double)sc > (double)(1 << 24) ? 1 : 0;
+        }
+        // small blocks: exact entry gather fused with the block matvec (one launch for all)
+        op->st_in.ensure((size_t)ftot);
+        op->st_out.ensure((size_t)gtot);
+        op->st_flag.ensure(1);
+        DevBuf<int64_t> d_meta;
+        std::vector<int64_t> meta;
+        for (auto* v : {&tl, &th, &sl, &sh, &foff, &goff}) meta.insert(meta.end(), v->begin(), v->end());
+        d_meta.upload(meta);
+        PCB_CK(cudaMemcpyAsync(op->st_in.p, f, (size_t)ftot * 8, cudaMemcpyHostToDevice, op->stream));
+        PCB_CK(cudaMemsetAsync(op->st_flag.p, 0, 4, op->stream));
+        const int64_t nb = (int64_t)nblk * D;
+        launch(op, op->stream, "block_direct", [&] {
+            return launch_block_direct(entry_args(op), nblk, tmax, d_meta.p, d_meta.p + nb, d_meta.p + 2 * nb,
+                                       d_meta.p + 3 * nb, d_meta.p + 4 * nb, d_meta.p + 4 * nb + nblk, op->st_in.p,
+                                       op->st_out.p, adjoint ? 1 : 0, op->st_flag.p, op->stream);
+        });
+        PCB_CK(cudaMemcpyAsync(g, op->st_out.p, (size_t)gtot * 8, cudaMemcpyDeviceToHost, op->stream));
+        PCB_CK(cudaStreamSynchronize(op->stream));
+        // large blocks: the FFT apply of f extended by zero outside S, cropped to T (exact)
+        std::vector<double> full, out;
+        DevBuf<double> dfull, dout;
+        for (int32_t b = 0; b < nblk; ++b) {
+            if (!big[b]) continue;
+            if (full.empty()) {
+                full.assign((size_t)op->N, 0.0);
+                out.assign((size_t)op->N, 0.0);
+                dfull.alloc((size_t)op->N);
+                dout.alloc((size_t)op->N);
+            }
+            std::fill(full.begin(), full.end(), 0.0);
+            int64_t q = 0;
+            const int64_t* lo = &sl[b * D];
+            const int64_t* hi = &sh[b * D];
+            for (int64_t i0 = lo[0]; i0 <= hi[0]; ++i0)
+                for (int64_t i1 = lo[1]; i1 <= hi[1]; ++i1)
+                    for (int64_t i2 = D == 3 ? lo[2] : 0; i2 <= (D == 3 ? hi[2] : 0); ++i2) {
+                        const int64_t lin = D == 2 ? (i0 - op->dom_lo[0]) * op->n[1] + (i1 - op->dom_lo[1])
+                                                   : ((i0 - op->dom_lo[0]) * op->n[1] + (i1 - op->dom_lo[1])) * op->n[2] +
+                                                         (i2 - op->dom_lo[2]);
+                        full[lin] = f[foff[b] + q++];
+                    }
+            PCB_CK(cudaMemcpyAsync(dfull.p, full.data(), (size_t)op->N * 8, cudaMemcpyHostToDevice, op->stream));
+            run_batch(op, adjoint != 0, 1, dfull.p, dout.p, op->stream);
+            PCB_CK(cudaMemcpyAsync(out.data(), dout.p, (size_t)op->N * 8, cudaMemcpyDeviceToHost, op->stream));
+            PCB_CK(cudaStreamSynchronize(op->stream));
+            q = 0;
+            const int64_t* tlo = &tl[b * D];
+            const int64_t* thi = &th[b * D];
+            for (int64_t i0 = tlo[0]; i0 <= thi[0]; ++i0)
+                for (int64_t i1 = tlo[1]; i1 <= thi[1]; ++i1)
+                    for (int64_t i2 = D == 3 ? tlo[2] : 0; i2 <= (D == 3 ? thi[2] : 0); ++i2) {
+                        const int64_t lin = D == 2 ? (i0 - op->dom_lo[0]) * op->n[1] + (i1 - op->dom_lo[1])
+                                                   : ((i0 - op->dom_lo[0]) * op->n[1] + (i1 - op->dom_lo[1])) * op->n[2] +
+                                                         (i2 - op->dom_lo[2]);
+                        g[goff[b] + q++] = out[lin];
+                    }
+        }
+    });
+}
+
 static void estimate_common(pcb_op* op, int32_t q, const double* dZ, const double* dY, double* dYt, int32_t nleaf,
                             const int64_t* leaf_lo, const int64_t* leaf_hi, double* eta_cells, double* eta_abs,
                             double* eta_rel, cudaStream_t st) {

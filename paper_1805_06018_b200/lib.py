@@ -26,7 +26,7 @@ MODE_NAMES = {v: k for k, v in MODES.items()}
 EXPORTS = ["pcb_default_options", "pcb_last_error", "pcb_create", "pcb_destroy", "pcb_get_info", "pcb_apply_batch",
            "pcb_apply_adjoint_batch", "pcb_apply_batch_dev", "pcb_apply_adjoint_batch_dev", "pcb_entries",
            "pcb_blocks", "pcb_blocks_dev", "pcb_probe_estimate", "pcb_probe_estimate_dev", "pcb_launch_count",
-           "pcb_normal_fill", "pcb_uniform_int_fill", "pcb_profile_begin", "pcb_profile_end"]
+           "pcb_normal_fill", "pcb_uniform_int_fill", "pcb_profile_begin", "pcb_profile_end", "pcb_apply_block"]
 
 
 class Options(ctypes.Structure):
@@ -82,6 +82,7 @@ def load():
     L.pcb_entries.argtypes = [vp, i64, vp, vp, vp]
     L.pcb_blocks.argtypes = [vp, i32, vp, vp, P_i64, vp]
     L.pcb_blocks_dev.argtypes = [vp, i32, vp, vp, P_i64, vp, vp]
+    L.pcb_apply_block.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, i32]
     L.pcb_probe_estimate.argtypes = [vp, i32, vp, vp, i32, vp, vp, vp, vp, P_dbl, P_dbl]
     L.pcb_probe_estimate_dev.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, vp, P_dbl, P_dbl, vp]
     L.pcb_launch_count.restype = ctypes.c_longlong

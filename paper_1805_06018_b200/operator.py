@@ -171,6 +171,31 @@ class ProductConvolutionOperator:
     def blocks_dev(self, nblk: int, d_t: int, d_s: int, block_shape: Sequence[int], d_out: int, stream: int = 0):
         self._rc(_L.load().pcb_blocks_dev(self._h, int(nblk), d_t, d_s, _i64arr(block_shape), d_out, stream or None))
 
+    # --- block apply (pc_operator.cpp:98-130) ------------------------------
+    def apply_block(self, T, S, f, adjoint: bool = False) -> np.ndarray:
+        """g on box T from f on box S (boxes (lo, hi) inclusive, inside the domain); one block."""
+        return self.apply_blocks([T], [S], [f], adjoint)[0]
+
+    def apply_blocks(self, Ts, Ss, fs, adjoint: bool = False):
+        """Batched block apply: returns [g_b on T_b]; f_b given on S_b (arrays of the box shape)."""
+        nb = len(Ts)
+        tl = np.ascontiguousarray([t[0] for t in Ts], dtype=np.int64).reshape(-1)
+        th = np.ascontiguousarray([t[1] for t in Ts], dtype=np.int64).reshape(-1)
+        sl = np.ascontiguousarray([s[0] for s in Ss], dtype=np.int64).reshape(-1)
+        sh = np.ascontiguousarray([s[1] for s in Ss], dtype=np.int64).reshape(-1)
+        shapes_t = [tuple(h - l + 1 for l, h in zip(t[0], t[1])) for t in Ts]
+        flat = np.ascontiguousarray(np.concatenate([np.asarray(f, dtype=np.float64).reshape(-1) for f in fs])
+                                    if nb else np.zeros(0))
+        out = np.empty(int(sum(int(np.prod(s)) for s in shapes_t)))
+        self._rc(_L.load().pcb_apply_block(self._h, nb, _ptr(tl), _ptr(th), _ptr(sl), _ptr(sh), _ptr(flat),
+                                           _ptr(out), int(adjoint)))
+        res, o = [], 0
+        for s in shapes_t:
+            n = int(np.prod(s))
+            res.append(out[o:o + n].reshape(s))
+            o += n
+        return res
+
     # --- estimator ---------------------------------------------------------
     def probe_estimate(self, Z: np.ndarray, Y: np.ndarray, leaves: Iterable = (), want_ytilde: bool = False):
         Z = self._vecs(Z, "apply_adjoint")

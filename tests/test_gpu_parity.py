@@ -299,3 +299,56 @@ def test_cpp_host_example(gpu, tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "OK" in r.stdout
+
+
+def test_apply_block_vs_reference_golden(gpu):
+    """apply_block (pc_operator.cpp:98-130): batched blocks, both directions, vs the reference."""
+    d = np.load(os.path.join(GOLD, "apply_block.npz"))
+    inp = inputs.small_lattice(**SMALL["small2d"])
+    op = ProductConvolutionOperator.from_inputs(inp)
+    n = int(d["n"])
+    Ts = [tuple(map(tuple, d[f"b{i}_T"])) for i in range(n)]
+    Ss = [tuple(map(tuple, d[f"b{i}_S"])) for i in range(n)]
+    fs = [d[f"b{i}_f"] for i in range(n)]
+    for adj in (0, 1):
+        out = op.apply_blocks(Ts, Ss, fs, adjoint=bool(adj))
+        for i in range(n):
+            ref = d[f"b{i}_{adj}"]
+            assert np.max(np.abs(out[i] - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_apply_block_properties(gpu, cfg):
+    """T = S = Omega equals apply (test_pc_operator.cpp:185-194; the FFT path for big blocks), H-matrix
+    leaf blocks equal apply-then-restrict, far boxes give exact zeros, domain violations raise."""
+    inp = inputs.make_config(cfg)
+    op = ProductConvolutionOperator.from_inputs(inp)
+    n = inp.shape[0]
+    dom = (inp.dom_lo, inp.dom_hi)
+    f = normal_vectors(5, 1, inp.n_points)[0]
+    for adj in (False, True):
+        whole = op.apply_block(dom, dom, f.reshape(inp.shape), adjoint=adj)
+        full = (op.apply_adjoint if adj else op.apply)(f)
+        assert rel(whole.reshape(-1), full) <= 1e-12
+    rng = np.random.default_rng(3)
+    Ts, Ss, fs = [], [], []
+    for _ in range(32):
+        t = rng.integers(0, n - 8, 2)
+        s = np.clip(t + rng.integers(-12, 12, 2), 0, n - 8)
+        Ts.append((tuple(t), tuple(t + 7)))
+        Ss.append((tuple(s), tuple(s + 7)))
+        fs.append(rng.uniform(-1, 1, (8, 8)))
+    for adj in (False, True):
+        out = op.apply_blocks(Ts, Ss, fs, adjoint=adj)
+        for i in (0, 7, 31):
+            full = np.zeros(inp.shape)
+            s0, s1 = Ss[i]
+            full[s0[0]:s1[0] + 1, s0[1]:s1[1] + 1] = fs[i]
+            g = (op.apply_adjoint if adj else op.apply)(full.reshape(-1)).reshape(inp.shape)
+            t0, t1 = Ts[i]
+            ref = g[t0[0]:t1[0] + 1, t0[1]:t1[1] + 1]
+            assert np.max(np.abs(out[i] - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+    far = op.apply_block(((0, 0), (3, 3)), ((n - 4, n - 4), (n - 1, n - 1)), np.ones((4, 4)))
+    assert not far.any()
+    with pytest.raises(ValueError, match="boxes must lie inside the domain"):
+        op.apply_block(((0, 0), (n, 3)), ((0, 0), (3, 3)), np.ones((4, 4)))

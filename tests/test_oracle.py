@@ -213,3 +213,37 @@ def test_oracle_vs_reference_library_random():
         f = rng.standard_normal(inp.n_points)
         assert rel(op.apply(f), ref.apply(f)) <= 1e-13
         assert rel(op.apply_adjoint(f), ref.apply(f, adjoint=True)) <= 1e-13
+
+
+def test_oracle_apply_block_vs_reference_golden():  # pc_operator.cpp:98-130 via the reference build
+    d = np.load(os.path.join(GOLD, "apply_block.npz"))
+    inp = inputs.small_lattice(**SMALL["small2d"])
+    assert str(d["checksum"]) == inp.checksum()
+    op = O.PCOperator.from_inputs(inp)
+    for i in range(int(d["n"])):
+        T = tuple(map(tuple, d[f"b{i}_T"]))
+        S = tuple(map(tuple, d[f"b{i}_S"]))
+        f = O.GF(S[0], d[f"b{i}_f"])
+        for adj in (0, 1):
+            g = op.apply_block(T, S, f, bool(adj))
+            ref = d[f"b{i}_{adj}"]
+            assert np.max(np.abs(g.values - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+
+
+def test_oracle_apply_block_is_apply_then_restrict():  # test_pc_operator.cpp:153-183
+    inp = inputs.small_lattice(n=14, dim=2, m=2, sigma=1.3)
+    op = O.PCOperator.from_inputs(inp)
+    rng = np.random.default_rng(10)
+    for _ in range(6):
+        slo = np.minimum(rng.integers(0, 14, 2), rng.integers(0, 14, 2))
+        shi = np.maximum(slo, rng.integers(0, 14, 2))
+        tlo = np.minimum(rng.integers(0, 14, 2), rng.integers(0, 14, 2))
+        thi = np.maximum(tlo, rng.integers(0, 14, 2))
+        T, S = (tuple(tlo), tuple(thi)), (tuple(slo), tuple(shi))
+        f = O.GF(S[0], rng.uniform(-1, 1, tuple(shi - slo + 1)))
+        full = np.zeros((14, 14))
+        full[slo[0]:shi[0] + 1, slo[1]:shi[1] + 1] = f.values
+        for adj in (False, True):
+            g = (op.apply_adjoint if adj else op.apply)(full.reshape(-1)).reshape(14, 14)
+            blk = op.apply_block(T, S, f, adj)
+            assert np.max(np.abs(blk.values - g[tlo[0]:thi[0] + 1, tlo[1]:thi[1] + 1])) <= 1e-12
