@@ -1,24 +1,23 @@
-// fp64 complex line FFTs for sm_100a: register radix-16 Stockham stages with
-// shared-memory exchanges between stages.
+// fp64 complex line FFTs for sm_100a: register Stockham stages with shared-memory exchanges
+// between stages, for line lengths L = 2^a * {1, 3, 9} (8 <= L <= 4096).
 //
-// A CTA transforms NL lines of length L at once with TPL = L/16 threads per
-// line (thread (l, tl), l fastest).  Stage radices: one radix-R0 stage
-// (R0 = L / 16^S, 1 if L is a power of 16) plus S radix-16 stages.  The
-// forward transform runs R0 first and ends with a radix-16 stage whose
-// outputs X[tl + r*L/16] (natural order) stay in the thread's registers; the
-// inverse transform starts with a radix-16 stage that consumes exactly those
-// registers, so forward -> pointwise product -> inverse needs no shared-memory
-// round trip in the middle (this is what lets the frequency multiply-
-// accumulate of the product-convolution apply live in registers).
+// A CTA transforms NL lines of length L at once.  Every thread holds E elements of one line
+// (E = 16 for powers of two, E = 24 = 3 * 8 otherwise; TPL = L/E threads per line, thread
+// (l, tl) with l fastest).  A stage of radix RS (RS | E) runs E/RS butterflies per thread.
+// The forward transform's stage radices end with E; the inverse runs them in reverse, so it
+// starts with E.  The forward leaves X[tl + r*L/E] in registers and the inverse consumes exactly
+// those registers: forward -> pointwise product -> inverse needs no shared-memory round trip in
+// the middle (this is what lets the frequency multiply-accumulate of the product-convolution
+// apply live in registers).
 //
 // Stockham stage (span NS before the stage, radix RS), butterfly j in [0, L/RS):
 //   inputs   x[j + r*L/RS]                       r = 0..RS-1
 //   twiddle  x_r *= w^(r*(j mod NS)),  w = exp(DIR*2*pi*i/(NS*RS))
 //   DFT_RS
 //   outputs  y[(j/NS)*NS*RS + (j mod NS) + r*NS]
-// Twiddles come from a per-length table tw[m] = exp(-2*pi*i*m/L) in global
-// memory (computed on the host in long double, rounded once); inverse uses
-// the conjugate.  All arithmetic is IEEE fp64.
+// Stage twiddles come from a per-length table tw[m] = exp(-2*pi*i*m/L) in global memory
+// (computed on the host in long double, rounded once; the inverse uses the conjugate).  The
+// in-register DFTs use compile-time 48th roots of unity.  All arithmetic is IEEE fp64.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -38,35 +37,57 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 __device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
 
-// cos/sin(2*pi*m/16), m = 0..15
-__device__ constexpr double kC16[16] = {
-    1.0, 0.92387953251128673848, 0.70710678118654752440, 0.38268343236508977173,
-    0.0, -0.38268343236508977173, -0.70710678118654752440, -0.92387953251128673848,
-    -1.0, -0.92387953251128673848, -0.70710678118654752440, -0.38268343236508977173,
-    0.0, 0.38268343236508977173, 0.70710678118654752440, 0.92387953251128673848};
-__device__ constexpr double kS16[16] = {
-    0.0, 0.38268343236508977173, 0.70710678118654752440, 0.92387953251128673848,
-    1.0, 0.92387953251128673848, 0.70710678118654752440, 0.38268343236508977173,
-    0.0, -0.38268343236508977173, -0.70710678118654752440, -0.92387953251128673848,
-    -1.0, -0.92387953251128673848, -0.70710678118654752440, -0.38268343236508977173};
+// ---------------------------------------------------------------------------
+// supported lengths and the twiddle-table layout (shared with the host)
 
-// v * exp(DIR * 2*pi*i * m / 16), m compile-time after unrolling
+__host__ __device__ constexpr bool is_pow2c(int v) { return v > 0 && (v & (v - 1)) == 0; }
+__host__ __device__ constexpr bool fft_len_ok(int L) {
+    return L >= 8 && L <= 8192 && L % 8 == 0 &&
+           (is_pow2c(L) || (L % 3 == 0 && is_pow2c(L / 3)) || (L % 9 == 0 && is_pow2c(L / 9)));
+}
+// offset of length L's table in the concatenation of all supported lengths (ascending)
+__host__ __device__ constexpr long long tw_offset(int L) {
+    long long off = 0;
+    for (int x = 8; x < L; x += 8)
+        if (fft_len_ok(x)) off += x;
+    return off;
+}
+
+// ---------------------------------------------------------------------------
+// compile-time roots: cos/sin(2*pi*m/48), m = 0..47 (48 = lcm of all in-register radices)
+
+__device__ constexpr double kC48[48] = {
+    1.0, 0.99144486137381041114, 0.96592582628906828675, 0.92387953251128675613,
+    0.86602540378443864676, 0.79335334029123516458, 0.70710678118654752440, 0.60876142900872063942,
+    0.5, 0.38268343236508977173, 0.25881904510252076235, 0.13052619222005159155,
+    0.0, -0.13052619222005159155, -0.25881904510252076235, -0.38268343236508977173,
+    -0.5, -0.60876142900872063942, -0.70710678118654752440, -0.79335334029123516458,
+    -0.86602540378443864676, -0.92387953251128675613, -0.96592582628906828675, -0.99144486137381041114,
+    -1.0, -0.99144486137381041114, -0.96592582628906828675, -0.92387953251128675613,
+    -0.86602540378443864676, -0.79335334029123516458, -0.70710678118654752440, -0.60876142900872063942,
+    -0.5, -0.38268343236508977173, -0.25881904510252076235, -0.13052619222005159155,
+    0.0, 0.13052619222005159155, 0.25881904510252076235, 0.38268343236508977173,
+    0.5, 0.60876142900872063942, 0.70710678118654752440, 0.79335334029123516458,
+    0.86602540378443864676, 0.92387953251128675613, 0.96592582628906828675, 0.99144486137381041114};
+
+// v * exp(DIR * 2*pi*i * m / 48), m compile-time after unrolling
 template <int DIR>
-__device__ __forceinline__ double2 rot16(double2 v, int m) {
-    m &= 15;
+__device__ __forceinline__ double2 rot48(double2 v, int m) {
+    m = ((m % 48) + 48) % 48;
     if (m == 0) return v;
-    if (m == 8) return make_double2(-v.x, -v.y);
-    if (m == 4) return DIR < 0 ? make_double2(v.y, -v.x) : make_double2(-v.y, v.x);
-    if (m == 12) return DIR < 0 ? make_double2(-v.y, v.x) : make_double2(v.y, -v.x);
-    const double c = kC16[m];
-    const double s = DIR < 0 ? -kS16[m] : kS16[m];
+    if (m == 24) return make_double2(-v.x, -v.y);
+    if (m == 12) return DIR < 0 ? make_double2(v.y, -v.x) : make_double2(-v.y, v.x);
+    if (m == 36) return DIR < 0 ? make_double2(-v.y, v.x) : make_double2(v.y, -v.x);
+    const double c = kC48[m];
+    const double sn = kC48[(m + 36) % 48];  // sin(2 pi m/48) = cos(2 pi (m - 12)/48)
+    const double s = DIR < 0 ? -sn : sn;
     return make_double2(fma(v.x, c, -v.y * s), fma(v.x, s, v.y * c));
 }
 
-// In-register DFT of size R (2, 4, 8 or 16): radix-2 DIF network, bit-reversed
-// result permuted back to natural order.
+// In-register DFT of size R in {2, 4, 8, 16}: radix-2 DIF network, bit-reversed result
+// permuted back to natural order.
 template <int R, int DIR>
-__device__ __forceinline__ void dft(double2* a) {
+__device__ __forceinline__ void dft_pow2(double2* a) {
 #pragma unroll
     for (int half = R / 2; half >= 1; half >>= 1) {
 #pragma unroll
@@ -76,11 +97,10 @@ __device__ __forceinline__ void dft(double2* a) {
                 const double2 u = a[blk + j];
                 const double2 v = a[blk + j + half];
                 a[blk + j] = cadd(u, v);
-                a[blk + j + half] = rot16<DIR>(csub(u, v), j * (16 / (2 * half)));
+                a[blk + j + half] = rot48<DIR>(csub(u, v), j * (48 / (2 * half)));
             }
         }
     }
-    // bit reversal
     double2 t[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) t[i] = a[i];
@@ -94,19 +114,94 @@ __device__ __forceinline__ void dft(double2* a) {
     }
 }
 
+template <int DIR>
+__device__ __forceinline__ void dft3(double2& a, double2& b, double2& c) {
+    const double s = DIR < 0 ? -0.86602540378443864676 : 0.86602540378443864676;  // DIR * sin(2 pi / 3)
+    const double2 t1 = cadd(b, c);
+    const double2 t2 = csub(b, c);
+    const double2 m = make_double2(fma(-0.5, t1.x, a.x), fma(-0.5, t1.y, a.y));
+    a = cadd(a, t1);
+    b = make_double2(m.x - s * t2.y, m.y + s * t2.x);  // m + i s t2
+    c = make_double2(m.x + s * t2.y, m.y - s * t2.x);  // m - i s t2
+}
+
+// In-register DFT of any size R in {2,3,4,6,8,12,16,24}.  R = 3*Q: Cooley-Tukey with
+// n = Q*n1 + n2, k = k1 + 3*k2:  X[k1 + 3 k2] = sum_n2 W_Q^{n2 k2} W_R^{n2 k1} DFT3_{n1}(x[Q n1 + n2])[k1].
+template <int R, int DIR>
+__device__ __forceinline__ void dft(double2* a) {
+    if constexpr (R % 3 != 0) {
+        dft_pow2<R, DIR>(a);
+    } else {
+        constexpr int Q = R / 3;
+        double2 y[3][Q];
+#pragma unroll
+        for (int n2 = 0; n2 < Q; ++n2) {
+            double2 x0 = a[n2], x1 = a[Q + n2], x2 = a[2 * Q + n2];
+            dft3<DIR>(x0, x1, x2);
+            y[0][n2] = x0;
+            y[1][n2] = rot48<DIR>(x1, n2 * (48 / R));
+            y[2][n2] = rot48<DIR>(x2, 2 * n2 * (48 / R));
+        }
+#pragma unroll
+        for (int k1 = 0; k1 < 3; ++k1) {
+            if constexpr (Q > 1) dft_pow2<Q, DIR>(y[k1]);
+#pragma unroll
+            for (int k2 = 0; k2 < Q; ++k2) a[k1 + 3 * k2] = y[k1][k2];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// stage plans
+
 template <int L>
 struct FftCfg {
-    static_assert(L >= 8 && L <= 4096 && (L & (L - 1)) == 0, "line length must be 2^k, 8..4096");
-    static constexpr int R = L >= 16 ? 16 : L;
-    static constexpr int S = L >= 4096 ? 3 : L >= 256 ? 2 : L >= 16 ? 1 : 0;  // radix-16 stages
-    static constexpr int P16 = S == 3 ? 4096 : S == 2 ? 256 : S == 1 ? 16 : 1;
-    static constexpr int R0 = L / P16;  // 1 if none (for L == 8 the single stage is radix 8)
-    static constexpr int TPL = L / R;   // threads per line
+    static_assert(fft_len_ok(L) && L <= 4096, "unsupported FFT line length");
+    static constexpr bool P2 = is_pow2c(L);
+    static constexpr int R = P2 ? (L >= 16 ? 16 : L) : 24;  // elements per thread (= last radix)
+    static constexpr int TPL = L / R;                        // threads per line
+    // forward stage radices: the prefix factors L/R, then R
+    static constexpr int pref_radix(int rest) {
+        return rest % 16 == 0 && P2 ? 16 : rest % 12 == 0 && !P2 ? 12 : rest % 8 == 0 ? 8 : rest % 6 == 0 && !P2 ? 6
+               : rest % 4 == 0 ? 4 : rest % 3 == 0 ? 3 : rest % 2 == 0 ? 2 : 1;
+    }
+    static constexpr int nstages() {
+        int n = 1, rest = L / R;
+        while (rest > 1) {
+            rest /= pref_radix(rest);
+            ++n;
+        }
+        return n;
+    }
+    static constexpr int NSTG = nstages();
+    // radix of forward stage s (smallest factors first, R last)
+    static constexpr int radix(int s) {
+        int f[8] = {1, 1, 1, 1, 1, 1, 1, 1};
+        int n = 0, rest = L / R;
+        while (rest > 1) {
+            const int p = pref_radix(rest);
+            f[n++] = p;
+            rest /= p;
+        }
+        // ascending prefix order keeps the first stage the smallest radix
+        for (int i = 0; i < n; ++i)
+            for (int j = i + 1; j < n; ++j)
+                if (f[j] < f[i]) {
+                    const int t = f[i];
+                    f[i] = f[j];
+                    f[j] = t;
+                }
+        return s < n ? f[s] : R;
+    }
+    static constexpr int span(int s) {  // NS before forward stage s
+        int ns = 1;
+        for (int i = 0; i < s; ++i) ns *= radix(i);
+        return ns;
+    }
 };
 
-// shared-memory word index for element i of line l; NL lines interleaved
-// ([L][NL] layout, matching global column tiles) plus one pad word per 2^PS
-// words to break the power-of-two strides of the first Stockham stage.
+// shared-memory word index for element i of line l; NL lines interleaved ([L][NL] layout,
+// matching global column tiles) plus one pad word per 2^PS words.
 template <int NL, int PS>
 __device__ __forceinline__ int sidx(int i, int l) {
     const int w = i * NL + l;
@@ -117,14 +212,13 @@ struct SmemLine {
     static constexpr int WORDS = L * NL + ((L * NL) >> PS) + 1;
 };
 
-// One stage held in registers: NB = R/RS butterflies of radix RS per thread.
+// One stage held in registers: E/RS butterflies of radix RS per thread.
 template <int L, int RS, int NS, int DIR>
 __device__ __forceinline__ void stage_math(double2* v, int tl, const double2* __restrict__ tw) {
-    constexpr int R = FftCfg<L>::R;
+    constexpr int E = FftCfg<L>::R;
     constexpr int TPL = FftCfg<L>::TPL;
-    constexpr int NB = R / RS;
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
+    for (int b = 0; b < E / RS; ++b) {
         const int j = tl + b * TPL;
         if (NS > 1) {
             const int k = j % NS;
@@ -141,20 +235,20 @@ __device__ __forceinline__ void stage_math(double2* v, int tl, const double2* __
 
 template <int L, int RS, int NL, int PS>
 __device__ __forceinline__ void stage_load(double2* v, const double2* buf, int l, int tl) {
-    constexpr int R = FftCfg<L>::R;
+    constexpr int E = FftCfg<L>::R;
     constexpr int TPL = FftCfg<L>::TPL;
 #pragma unroll
-    for (int b = 0; b < R / RS; ++b)
+    for (int b = 0; b < E / RS; ++b)
 #pragma unroll
         for (int r = 0; r < RS; ++r) v[b * RS + r] = buf[sidx<NL, PS>(tl + b * TPL + r * (L / RS), l)];
 }
 
 template <int L, int RS, int NS, int NL, int PS>
 __device__ __forceinline__ void stage_store(const double2* v, double2* buf, int l, int tl) {
-    constexpr int R = FftCfg<L>::R;
+    constexpr int E = FftCfg<L>::R;
     constexpr int TPL = FftCfg<L>::TPL;
 #pragma unroll
-    for (int b = 0; b < R / RS; ++b) {
+    for (int b = 0; b < E / RS; ++b) {
         const int j = tl + b * TPL;
         const int base = (j / NS) * NS * RS + (j % NS);
 #pragma unroll
@@ -162,117 +256,89 @@ __device__ __forceinline__ void stage_store(const double2* v, double2* buf, int 
     }
 }
 
-// Positions held by a thread before the first stage of a transform whose first
-// stage has radix RS: element index of v[b*RS + r].
-template <int L, int RS>
-__device__ __forceinline__ int first_pos(int tl, int b, int r) {
-    return tl + b * FftCfg<L>::TPL + r * (L / RS);
-}
-
-// Radix-16 stage s (0-based among the radix-16 stages) of the forward transform.
+// forward stages s..NSTG-1; stage 0 consumes the caller's registers, the last leaves the
+// result in registers
 template <int L, int DIR, int NL, int PS, int s>
-struct Fwd16Stages {
+struct FwdStages {
     static __device__ __forceinline__ void run(double2* v, double2* buf, int l, int tl,
                                                const double2* __restrict__ tw) {
-        constexpr int R0 = FftCfg<L>::R0;
-        constexpr int S = FftCfg<L>::S;
-        constexpr int NS = (R0 > 1 ? R0 : 1) * (s == 0 ? 1 : s == 1 ? 16 : 256);
-        if (s > 0 || R0 > 1) {
-            __syncthreads();
-            stage_load<L, 16, NL, PS>(v, buf, l, tl);
-        }
-        stage_math<L, 16, NS, DIR>(v, tl, tw);
-        if (s + 1 < S) {
-            __syncthreads();
-            stage_store<L, 16, NS, NL, PS>(v, buf, l, tl);
-            Fwd16Stages<L, DIR, NL, PS, s + 1>::run(v, buf, l, tl, tw);
+        constexpr int NSTG = FftCfg<L>::NSTG;
+        if constexpr (s < NSTG) {
+            constexpr int RS = FftCfg<L>::radix(s);
+            constexpr int NS = FftCfg<L>::span(s);
+            if constexpr (s > 0) {
+                __syncthreads();
+                stage_load<L, RS, NL, PS>(v, buf, l, tl);
+            }
+            stage_math<L, RS, NS, DIR>(v, tl, tw);
+            if constexpr (s + 1 < NSTG) {
+                __syncthreads();
+                stage_store<L, RS, NS, NL, PS>(v, buf, l, tl);
+                FwdStages<L, DIR, NL, PS, s + 1>::run(v, buf, l, tl, tw);
+            }
         }
     }
 };
-template <int L, int DIR, int NL, int PS>
-struct Fwd16Stages<L, DIR, NL, PS, 3> {
-    static __device__ __forceinline__ void run(double2*, double2*, int, int, const double2*) {}
+
+// inverse-order stages (reverse of the forward radices), i = 0..NSTG-1
+template <int L, int DIR, int NL, int PS, int i>
+struct RevStages {
+    static __device__ __forceinline__ void run(double2* v, double2* buf, int l, int tl,
+                                               const double2* __restrict__ tw) {
+        constexpr int NSTG = FftCfg<L>::NSTG;
+        if constexpr (i < NSTG) {
+            constexpr int RS = FftCfg<L>::radix(NSTG - 1 - i);
+            constexpr int NS = L / FftCfg<L>::span(NSTG - i);  // product of the radices already applied
+            if constexpr (i > 0) {
+                __syncthreads();
+                stage_load<L, RS, NL, PS>(v, buf, l, tl);
+            }
+            stage_math<L, RS, NS, DIR>(v, tl, tw);
+            if constexpr (i + 1 < NSTG) {
+                __syncthreads();
+                stage_store<L, RS, NS, NL, PS>(v, buf, l, tl);
+                RevStages<L, DIR, NL, PS, i + 1>::run(v, buf, l, tl, tw);
+            }
+        }
+    }
 };
 
-// Forward-ordered transform: v holds inputs laid out for the first stage
-// (radix R0 if R0 > 1, else radix 16); on return v[r] = X[tl + r*L/16].
-// For L == 8 (single radix-8 stage, one thread per line) v[r] = X[r].
+// Forward-ordered transform: v holds inputs at FirstPos; on return v[r] = X[tl + r*L/E].
 template <int L, int DIR, int NL, int PS>
 __device__ __forceinline__ void fft_fwd_order(double2* v, double2* buf, int l, int tl,
                                               const double2* __restrict__ tw) {
-    constexpr int R0 = FftCfg<L>::R0;
-    if (L == 8) {
-        dft<8, DIR>(v);
-        return;
-    }
-    if (R0 > 1) {
-        stage_math<L, R0, 1, DIR>(v, tl, tw);
-        __syncthreads();
-        stage_store<L, R0, 1, NL, PS>(v, buf, l, tl);
-    }
-    Fwd16Stages<L, DIR, NL, PS, 0>::run(v, buf, l, tl, tw);
+    FwdStages<L, DIR, NL, PS, 0>::run(v, buf, l, tl, tw);
 }
 
-template <int L, int DIR, int NL, int PS, int s>
-struct Inv16Stages {
-    static __device__ __forceinline__ void run(double2* v, double2* buf, int l, int tl,
-                                               const double2* __restrict__ tw) {
-        constexpr int S = FftCfg<L>::S;
-        constexpr int NS = s == 0 ? 1 : s == 1 ? 16 : 256;
-        if (s > 0) {
-            __syncthreads();
-            stage_load<L, 16, NL, PS>(v, buf, l, tl);
-        }
-        stage_math<L, 16, NS, DIR>(v, tl, tw);
-        if (s + 1 < S || FftCfg<L>::R0 > 1) {
-            __syncthreads();
-            stage_store<L, 16, NS, NL, PS>(v, buf, l, tl);
-        }
-        if (s + 1 < S) Inv16Stages<L, DIR, NL, PS, s + 1>::run(v, buf, l, tl, tw);
-    }
-};
-template <int L, int DIR, int NL, int PS>
-struct Inv16Stages<L, DIR, NL, PS, 3> {
-    static __device__ __forceinline__ void run(double2*, double2*, int, int, const double2*) {}
-};
-
-// Reverse-ordered transform: v[r] holds x[tl + r*L/16] (the registers a
-// forward-ordered transform leaves behind).  On return v holds the outputs of
-// the last stage: position of v[b*RL + r] is last_pos(tl, b, r), RL = R0 if
-// R0 > 1 else 16.
+// Reverse-ordered transform: v[r] holds x[tl + r*L/E] (what fft_fwd_order leaves); on return
+// the outputs sit at LastPos.
 template <int L, int DIR, int NL, int PS>
 __device__ __forceinline__ void fft_rev_order(double2* v, double2* buf, int l, int tl,
                                               const double2* __restrict__ tw) {
-    constexpr int R0 = FftCfg<L>::R0;
-    constexpr int S = FftCfg<L>::S;
-    if (L == 8) {
-        dft<8, DIR>(v);
-        return;
-    }
-    Inv16Stages<L, DIR, NL, PS, 0>::run(v, buf, l, tl, tw);
-    if (R0 > 1) {
-        constexpr int NS = S == 1 ? 16 : S == 2 ? 256 : 4096;
-        __syncthreads();
-        stage_load<L, R0, NL, PS>(v, buf, l, tl);
-        stage_math<L, R0, NS, DIR>(v, tl, tw);
-    }
+    RevStages<L, DIR, NL, PS, 0>::run(v, buf, l, tl, tw);
 }
 
+// register positions: after fft_fwd_order / before fft_rev_order, v[r] is element tl + r*L/E
 template <int L>
-struct LastPos {
-    static constexpr int RL = FftCfg<L>::R0 > 1 ? FftCfg<L>::R0 : FftCfg<L>::R;
-    // output position of v[b*RL + r] after fft_rev_order
+__device__ __forceinline__ int mid_pos(int tl, int r) {
+    return tl + r * (L / FftCfg<L>::R);
+}
+
+// first-stage input layout of fft_fwd_order: radix RF = radix(0)
+template <int L>
+struct FirstPos {
+    static constexpr int RF = FftCfg<L>::radix(0);
     static __device__ __forceinline__ int pos(int tl, int b, int r) {
-        return tl + b * FftCfg<L>::TPL + r * (L / RL);
+        return tl + b * FftCfg<L>::TPL + r * (L / RF);
     }
 };
 
-// first-stage input layout of fft_fwd_order: radix RF = R0 if R0 > 1 else R
+// output positions after fft_rev_order: the last inverse stage has radix RL = radix(0)
 template <int L>
-struct FirstPos {
-    static constexpr int RF = FftCfg<L>::R0 > 1 ? FftCfg<L>::R0 : FftCfg<L>::R;
+struct LastPos {
+    static constexpr int RL = FftCfg<L>::radix(0);
     static __device__ __forceinline__ int pos(int tl, int b, int r) {
-        return tl + b * FftCfg<L>::TPL + r * (L / RF);
+        return tl + b * FftCfg<L>::TPL + r * (L / RL);
     }
 };
 

@@ -1,4 +1,5 @@
-// sm_100a fp64 kernels of the product-convolution apply path.
+// sm_100a fp64 kernels of the product-convolution apply path (templates; instantiated by
+// kernels_rows.cu, kernels_cols.cu, kernels_mid.cu; the gathers live in kernels_misc.cu).
 //
 //   K1  spectra build      rows_fwd<RF_SPEC> -> [mid<MM_FWD_SPEC>] -> cols<CM_SPEC>
 //   K2  weight+pad+FFT     rows_fwd<RF_APPLY> (w_k . f gathered on the footprint, zero-padded,
@@ -11,10 +12,15 @@
 //                          rows_inv<RI_ADJ>), plus probe_sums for eta
 //   K6  entry/block gather entries / blocks
 // Reference semantics: pc_operator.cpp:45-96, fft.cpp:64-162, adaptivity.cpp:75-121.
+#pragma once
 #include <cstdio>
 
 #include "fft.cuh"
 #include "kernels.cuh"
+
+#ifndef PCB_ROWS_MINB
+#define PCB_ROWS_MINB 1
+#endif
 
 namespace pcb {
 
@@ -27,7 +33,11 @@ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
 template <int NL>
 constexpr int PSH = ilog2c(NL) > 3 ? ilog2c(NL) : 3;
 
-__device__ __forceinline__ const double2* twtab(const double2* tw, int len) { return tw + (len - 8); }
+template <int LEN>
+__device__ __forceinline__ const double2* twtab(const double2* tw) {
+    static_assert(fft_len_ok(LEN), "no twiddle table for this length");
+    return tw + tw_offset(LEN);
+}
 
 template <int LEN, int NL>
 constexpr int smem_words() {
@@ -68,7 +78,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // w_k . f on the footprint window, ADJ gathers g on the output window (both
 // staged through shared memory with cp.async), SPEC places the trimmed kernel.
 template <int N, int NL, int MODE>
-__global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_fwd(PassArgs a) {
+__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, PCB_ROWS_MINB) k_rows_fwd(PassArgs a) {
     constexpr int R = FftCfg<N>::R;
     constexpr int RF = FirstPos<N>::RF;
     constexpr int NT = NL * FftCfg<N>::TPL;
@@ -173,25 +183,25 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_fwd(PassArgs a) {
                 v[b * RF + r] = make_double2(xv[0], xv[1]);
             }
     }
-    fft_fwd_order<N, -1, NL, PS>(v, buf, l, tl, twtab(a.tw, N));
+    fft_fwd_order<N, -1, NL, PS>(v, buf, l, tl, twtab<N>(a.tw));
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int pos = N >= 16 ? tl + r * (N / 16) : r;
+        const int pos = mid_pos<N>(tl, r);
         buf[sidx<NL, PS>(pos, l)] = v[r];
     }
     __syncthreads();
 
     // phase 3: even/odd split X[k] = A[k] + W^k B[k], k = 0..N
-    const double2* twP = twtab(a.tw, 2 * N);
+    const double2* twP = twtab<2 * N>(a.tw);
     double2* S_item = MODE == RF_SPEC ? a.S + (int64_t)item * a.S_stride : a.S + td.s_pool + vec * td.s_vst;
     for (int idx = threadIdx.x; idx < NL * (N + 1); idx += NT) {
         const int ll = idx / (N + 1);
         const int k = idx - ll * (N + 1);
         const int64_t row = m_row[ll];
         if (row < 0) continue;
-        const double2 zk = buf[sidx<NL, PS>(k & (N - 1), ll)];
-        const double2 zn = buf[sidx<NL, PS>((N - k) & (N - 1), ll)];
+        const double2 zk = buf[sidx<NL, PS>(k == N ? 0 : k, ll)];
+        const double2 zn = buf[sidx<NL, PS>(k == 0 ? 0 : N - k, ll)];
         const double2 A = make_double2(0.5 * (zk.x + zn.x), 0.5 * (zk.y - zn.y));
         const double2 Bm = make_double2(0.5 * (zk.y + zn.y), -0.5 * (zk.x - zn.x));  // (zk - conj zn)/(2i)
         S_item[row + k] = cadd(A, cmul(__ldg(&twP[k]), Bm));
@@ -238,21 +248,21 @@ __global__ void __launch_bounds__(NL * FftCfg<P1>::TPL) k_mid(PassArgs a) {
                 const int p = FirstPos<P1>::pos(tl, b, r);
                 v[b * RF + r] = (cvalid && p >= in_lo && p < in_lo + in_cnt) ? base[(int64_t)p * a.W] : czero();
             }
-        fft_fwd_order<P1, -1, NL, PSH<NL>>(v, buf, l, tl, twtab(a.tw, P1));
+        fft_fwd_order<P1, -1, NL, PSH<NL>>(v, buf, l, tl, twtab<P1>(a.tw));
         if (cvalid) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const int pos = P1 >= 16 ? tl + r * (P1 / 16) : r;
+                const int pos = mid_pos<P1>(tl, r);
                 base[(int64_t)pos * a.W] = v[r];
             }
         }
     } else {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int pos = P1 >= 16 ? tl + r * (P1 / 16) : r;
+            const int pos = mid_pos<P1>(tl, r);
             v[r] = cvalid ? base[(int64_t)pos * a.W] : czero();
         }
-        fft_rev_order<P1, +1, NL, PSH<NL>>(v, buf, l, tl, twtab(a.tw, P1));
+        fft_rev_order<P1, +1, NL, PSH<NL>>(v, buf, l, tl, twtab<P1>(a.tw));
         if (cvalid) {
 #pragma unroll
             for (int b = 0; b < R / RL; ++b)
@@ -282,7 +292,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
     const int64_t c = c0 + l;
     const bool cvalid = c < a.L;
     const int64_t tile_off = (c0 / NL) * (int64_t)P0 * NL + l;  // spectrum tile-major offset
-    const double2* tw0 = twtab(a.tw, P0);
+    const double2* tw0 = twtab<P0>(a.tw);
 
     auto load_in = [&](const double2* src, int in_lo, int in_cnt, double2* v) {
 #pragma unroll
@@ -304,7 +314,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
                 if (p >= keep_lo && p < keep_lo + keep_cnt) dst[(int64_t)(p - keep_lo) * a.L + c] = v[b * RL + r];
             }
     };
-    auto fpos = [&](int r) { return P0 >= 16 ? tl + r * (P0 / 16) : r; };
+    auto fpos = [&](int r) { return mid_pos<P0>(tl, r); };
 
     double2 v[R];
     if (MODE == CM_SPEC || MODE == CM_APPLY_LOCAL || MODE == CM_ADJ_LOCAL) {
@@ -387,7 +397,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
 // output positions p = t mod blockDim, so contributions to one position are
 // added by one thread in ascending entry order (deterministic, no atomics).
 template <int N, int NL, int MODE>
-__global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_inv(PassArgs a) {
+__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, PCB_ROWS_MINB) k_rows_inv(PassArgs a) {
     constexpr int R = FftCfg<N>::R;
     constexpr int RL = LastPos<N>::RL;
     constexpr int NT = NL * FftCfg<N>::TPL;
@@ -407,7 +417,7 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_inv(PassArgs a) {
     GatherEntry* meta = reinterpret_cast<GatherEntry*>(acc + a.n[ax] + (a.n[ax] & 1));
     const int64_t e_beg = a.line_ptr[aline];
     const int64_t e_end = a.line_ptr[aline + 1];
-    const double2* twP = twtab(a.tw, 2 * N);
+    const double2* twP = twtab<2 * N>(a.tw);
     const int l = threadIdx.x % NL;
     const int tl = threadIdx.x / NL;
     for (int i = ulo + threadIdx.x; i < uhi; i += NT) acc[i - ulo] = 0.0;
@@ -442,10 +452,10 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_inv(PassArgs a) {
         double2 v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int pos = N >= 16 ? tl + r * (N / 16) : r;
+            const int pos = mid_pos<N>(tl, r);
             v[r] = buf[sidx<NL, PSH<NL>>(pos, l)];
         }
-        fft_rev_order<N, +1, NL, PSH<NL>>(v, buf, l, tl, twtab(a.tw, N));
+        fft_rev_order<N, +1, NL, PSH<NL>>(v, buf, l, tl, twtab<N>(a.tw));
         __syncthreads();
 #pragma unroll
         for (int bb = 0; bb < R / RL; ++bb)
@@ -475,189 +485,7 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL) k_rows_inv(PassArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K6: Atilde[y,x] = sum_{k: x in U_k} w_k[x] phi_k^E[y - x], k ascending, the
-// reference's operation order (pc_operator.cpp:84-96) with IEEE mul/add (no FMA
-// contraction) so the result is the reference's bit for bit.
-__device__ __forceinline__ double entry_value(const EntryArgs& a, const int64_t* y, const int64_t* x, bool& bad) {
-    const int D = a.D;
-    int64_t bl = 0;
-    for (int i = 0; i < D; ++i) {
-        const int64_t yi = y[i] - a.dom_lo[i], xi = x[i] - a.dom_lo[i];
-        if (yi < 0 || yi >= a.n[i] || xi < 0 || xi >= a.n[i]) {
-            bad = true;
-            return 0.0;
-        }
-        bl = bl * a.nb[i] + xi / a.bucket[i];
-    }
-    double sum = 0.0;
-    for (int64_t q = a.bucket_ptr[bl]; q < a.bucket_ptr[bl + 1]; ++q) {
-        const TermDesc& t = a.terms[a.bucket_terms[q]];
-        int64_t wl = 0, zl = 0;
-        bool inx = true, inz = true;
-        for (int i = 0; i < D; ++i) {
-            const int64_t u = x[i] - t.x_lo[i];
-            if (u < 0 || u >= t.m[i]) inx = false;
-            wl = wl * t.m[i] + u;
-            const int64_t z = y[i] - x[i] - t.k_lo[i];
-            if (z < 0 || z >= t.k_ext[i]) inz = false;
-            zl = zl * t.k_ext[i] + z;
-        }
-        if (!inx) continue;
-        const double wx = a.w_pool[t.w_off + wl];
-        if (wx == 0.0) continue;
-        const double ph = inz ? a.phi_pool[t.phi_off + zl] : 0.0;
-        sum = __dadd_rn(sum, __dmul_rn(wx, ph));
-    }
-    return sum;
-}
-
-__global__ void k_entries(EntryArgs a, int64_t cnt, const int64_t* __restrict__ y, const int64_t* __restrict__ x,
-                          double* __restrict__ out, int32_t* bad) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
-        bool b = false;
-        const double v = entry_value(a, y + i * a.D, x + i * a.D, b);
-        out[i] = v;
-        if (b) atomicOr(bad, 1);
-    }
-}
-
-__global__ void k_blocks(EntryArgs a, int32_t nblk, const int64_t* __restrict__ t_origin,
-                         const int64_t* __restrict__ s_origin, const int32_t* __restrict__ bshape,
-                         double* __restrict__ out, int32_t* bad) {
-    const int D = a.D;
-    int64_t bs = 1;
-    for (int i = 0; i < D; ++i) bs *= bshape[i];
-    const int64_t total = (int64_t)nblk * bs * bs;
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t blk = g / (bs * bs);
-        const int64_t rem = g - blk * bs * bs;
-        int64_t i = rem / bs, j = rem - (rem / bs) * bs;
-        int64_t y[3], x[3];
-        for (int d = D - 1; d >= 0; --d) {
-            y[d] = t_origin[blk * D + d] + i % bshape[d];
-            i /= bshape[d];
-            x[d] = s_origin[blk * D + d] + j % bshape[d];
-            j /= bshape[d];
-        }
-        bool b = false;
-        out[g] = entry_value(a, y, x, b);
-        if (b) atomicOr(bad, 1);
-    }
-}
-
-// Block apply, direct form (pc_operator.cpp:98-130 semantics): for block b,
-//   apply:   g_b[y] = sum_{x in S_b} Atilde[y, x] f_b[x],   y in T_b
-//   adjoint: g_b[x] = sum_{y in S_b} Atilde[y, x] f_b[y],   x in T_b
-// One CTA per (block, tile of 256 outputs); f_b staged in shared memory in chunks.
-__global__ void k_block_direct(EntryArgs a, int32_t nblk, const int64_t* __restrict__ t_lo,
-                               const int64_t* __restrict__ t_hi, const int64_t* __restrict__ s_lo,
-                               const int64_t* __restrict__ s_hi, const int64_t* __restrict__ f_off,
-                               const int64_t* __restrict__ g_off, const double* __restrict__ f,
-                               double* __restrict__ g, int adjoint, int32_t* bad) {
-    const int D = a.D;
-    const int blk = blockIdx.y;
-    if (blk >= nblk) return;
-    int64_t text[3] = {1, 1, 1}, sext[3] = {1, 1, 1}, tcnt = 1, scnt = 1;
-    for (int i = 0; i < D; ++i) {
-        text[i] = t_hi[blk * D + i] - t_lo[blk * D + i] + 1;
-        sext[i] = s_hi[blk * D + i] - s_lo[blk * D + i] + 1;
-        tcnt *= text[i];
-        scnt *= sext[i];
-    }
-    const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t pt[3] = {0, 0, 0};
-    {
-        int64_t r = o < tcnt ? o : 0;
-        for (int i = D - 1; i >= 0; --i) {
-            pt[i] = t_lo[blk * D + i] + r % text[i];
-            r /= text[i];
-        }
-    }
-    __shared__ double fs[512];
-    double sum = 0.0;
-    bool b = false;
-    for (int64_t c0 = 0; c0 < scnt; c0 += 512) {
-        const int cn = (int)((scnt - c0) < 512 ? (scnt - c0) : 512);
-        __syncthreads();
-        for (int i = threadIdx.x; i < cn; i += blockDim.x) fs[i] = f[f_off[blk] + c0 + i];
-        __syncthreads();
-        if (o < tcnt) {
-            for (int j = 0; j < cn; ++j) {
-                const double fv = fs[j];
-                if (fv == 0.0) continue;
-                int64_t ps[3] = {0, 0, 0};
-                int64_t r = c0 + j;
-                for (int i = D - 1; i >= 0; --i) {
-                    ps[i] = s_lo[blk * D + i] + r % sext[i];
-                    r /= sext[i];
-                }
-                const double e = adjoint ? entry_value(a, ps, pt, b) : entry_value(a, pt, ps, b);
-                sum += e * fv;
-            }
-        }
-    }
-    if (o < tcnt) g[g_off[blk] + o] = sum;
-    if (b) atomicOr(bad, 1);
-}
-
-// ---------------------------------------------------------------------------
-// K5 reductions: d2[box, probe] = sum_{p in box cap Omega} (Yt - Y)^2, y2[probe] = sum Y^2
-__global__ void k_probe_sums(int D, int32_t n0, int32_t n1, int32_t n2, int32_t nbox, const int64_t* __restrict__ blo,
-                             const int64_t* __restrict__ bhi, const double* __restrict__ Yt,
-                             const double* __restrict__ Y, double* d2, double* y2) {
-    const int box = blockIdx.x;  // box == nbox -> whole domain (also sums Y^2)
-    const int probe = blockIdx.y;
-    const int32_t n[3] = {n0, n1, D == 3 ? n2 : 1};
-    int64_t lo[3] = {0, 0, 0}, hi[3] = {n0 - 1, n1 - 1, n[2] - 1};
-    if (box < nbox) {
-        for (int i = 0; i < D; ++i) {
-            lo[i] = blo[box * D + i] > 0 ? blo[box * D + i] : 0;
-            hi[i] = bhi[box * D + i] < n[i] - 1 ? bhi[box * D + i] : n[i] - 1;
-        }
-    }
-    int64_t ext[3];
-    int64_t cnt = 1;
-    for (int i = 0; i < 3; ++i) {
-        ext[i] = hi[i] >= lo[i] ? hi[i] - lo[i] + 1 : 0;
-        cnt *= ext[i];
-    }
-    const int64_t N = (int64_t)n[0] * n[1] * n[2];
-    const double* yt = Yt + probe * N;
-    const double* yy = Y + probe * N;
-    double s = 0.0, sy = 0.0;
-    for (int64_t q = threadIdx.x; q < cnt; q += blockDim.x) {
-        const int64_t i2 = q % ext[2];
-        const int64_t r = q / ext[2];
-        const int64_t i1 = r % ext[1];
-        const int64_t i0 = r / ext[1];
-        const int64_t off = ((lo[0] + i0) * n[1] + lo[1] + i1) * n[2] + lo[2] + i2;
-        const double dv = yt[off] - yy[off];
-        s += dv * dv;
-        sy += yy[off] * yy[off];
-    }
-    __shared__ double red[2][256];
-    red[0][threadIdx.x] = s;
-    red[1][threadIdx.x] = sy;
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) {
-            red[0][threadIdx.x] += red[0][threadIdx.x + w];
-            red[1][threadIdx.x] += red[1][threadIdx.x + w];
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        d2[(int64_t)box * gridDim.y + probe] = red[0][0];
-        if (box == nbox) y2[probe] = red[1][0];
-    }
-}
-
-__global__ void k_zero(double* p, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = 0.0;
-}
-
-// ---------------------------------------------------------------------------
-// dispatch over the compile-time sizes
+// launch helpers shared by the dispatch units
 
 template <typename K>
 cudaError_t launch_dyn(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const PassArgs& a) {
@@ -671,207 +499,21 @@ cudaError_t launch_dyn(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_
 
 template <int LEN>
 constexpr int rows_nl() {  // lines per CTA for the last-axis passes: ~128 threads
-    return LEN >= 2048 ? 1 : (2048 / LEN > 32 ? 32 : 2048 / LEN);
+    constexpr int t = 128 / FftCfg<LEN>::TPL;
+    return t < 1 ? 1 : (t > 32 ? 32 : t);
 }
 template <int P>
-constexpr int cols_nl() {
-    return P >= 1024 ? 2 : (2048 / P > 32 ? 32 : 2048 / P);
-}
-
-template <int N, int MODE>
-cudaError_t rows_fwd_n(const PassArgs& a, cudaStream_t st) {
-    constexpr int NL = rows_nl<N>();
-    const int64_t maxlines = MODE == RF_SPEC ? (a.D == 2 ? a.P[0] : (int64_t)a.P[0] * a.P[1]) : a.lines_max;
-    const int items = (MODE == RF_ADJ && a.global) ? a.B : a.n_slots * (MODE == RF_SPEC ? 1 : a.B);
-    dim3 grid((unsigned)((maxlines + NL - 1) / NL), (unsigned)items);
-    const size_t smem = sizeof(double2) * smem_words<N, NL>() + NL * (3 * sizeof(int64_t) + 2 * sizeof(int));
-    return launch_dyn(k_rows_fwd<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
-}
-
-template <int MODE>
-cudaError_t rows_fwd_mode(const PassArgs& a, cudaStream_t st) {
-    switch (a.P[a.D - 1] / 2) {
-        case 8: return rows_fwd_n<8, MODE>(a, st);
-        case 16: return rows_fwd_n<16, MODE>(a, st);
-        case 32: return rows_fwd_n<32, MODE>(a, st);
-        case 64: return rows_fwd_n<64, MODE>(a, st);
-        case 128: return rows_fwd_n<128, MODE>(a, st);
-        case 256: return rows_fwd_n<256, MODE>(a, st);
-        case 512: return rows_fwd_n<512, MODE>(a, st);
-        case 1024: return rows_fwd_n<1024, MODE>(a, st);
-        case 2048: return rows_fwd_n<2048, MODE>(a, st);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-template <int P1, int MODE>
-cudaError_t mid_p(const PassArgs& a, cudaStream_t st) {
-    constexpr int NL = cols_nl<P1>();
-    const bool gmode = a.global && (MODE == MM_INV_APPLY || MODE == MM_FWD_ADJ);
-    const int items = gmode ? a.B : a.n_slots * (MODE == MM_FWD_SPEC ? 1 : a.B);
-    dim3 grid((unsigned)((a.W + NL - 1) / NL), (unsigned)a.P[0], (unsigned)items);
-    const size_t smem = sizeof(double2) * smem_words<P1, NL>();
-    return launch_dyn(k_mid<P1, NL, MODE>, grid, dim3(NL * FftCfg<P1>::TPL), smem, st, a);
-}
-
-template <int MODE>
-cudaError_t mid_mode(const PassArgs& a, cudaStream_t st) {
-    switch (a.P[1]) {
-        case 16: return mid_p<16, MODE>(a, st);
-        case 32: return mid_p<32, MODE>(a, st);
-        case 64: return mid_p<64, MODE>(a, st);
-        case 128: return mid_p<128, MODE>(a, st);
-        case 256: return mid_p<256, MODE>(a, st);
-        case 512: return mid_p<512, MODE>(a, st);
-        case 1024: return mid_p<1024, MODE>(a, st);
-        case 2048: return mid_p<2048, MODE>(a, st);
-        case 4096: return mid_p<4096, MODE>(a, st);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-template <int P0, int MODE>
-cudaError_t cols_p(const PassArgs& a, cudaStream_t st) {
-    constexpr int NL = cols_nl<P0>();
-    if (a.nl_cols != NL) return cudaErrorInvalidValue;
-    const bool global = MODE == CM_APPLY_GLOBAL || MODE == CM_ADJ_GLOBAL;
-    const int items = global ? a.B : a.n_slots * (MODE == CM_SPEC ? 1 : a.B);
-    dim3 grid((unsigned)((a.L + NL - 1) / NL), (unsigned)items);
-    const size_t smem = sizeof(double2) * smem_words<P0, NL>();
-    return launch_dyn(k_cols<P0, NL, MODE>, grid, dim3(NL * FftCfg<P0>::TPL), smem, st, a);
-}
-
-template <int MODE>
-cudaError_t cols_mode(const PassArgs& a, cudaStream_t st) {
-    switch (a.P[0]) {
-        case 16: return cols_p<16, MODE>(a, st);
-        case 32: return cols_p<32, MODE>(a, st);
-        case 64: return cols_p<64, MODE>(a, st);
-        case 128: return cols_p<128, MODE>(a, st);
-        case 256: return cols_p<256, MODE>(a, st);
-        case 512: return cols_p<512, MODE>(a, st);
-        case 1024: return cols_p<1024, MODE>(a, st);
-        case 2048: return cols_p<2048, MODE>(a, st);
-        case 4096: return cols_p<4096, MODE>(a, st);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-template <int N, int MODE>
-cudaError_t rows_inv_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
-    constexpr int NL = rows_nl<N>();
-    dim3 grid((unsigned)n_lines, (unsigned)a.B);
-    constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
-                                                                          : (NL * (2 * N + 1) + 1) / 2;
-    const size_t smem = sizeof(double2) * (BUFW + NL * (N + 1)) + sizeof(double) * ((size_t)a.n[a.D - 1] + 1) +
-                        NL * sizeof(GatherEntry) + 16;
-    return launch_dyn(k_rows_inv<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
-}
-
-template <int MODE>
-cudaError_t rows_inv_mode(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
-    switch (a.P[a.D - 1] / 2) {
-        case 8: return rows_inv_n<8, MODE>(a, n_lines, st);
-        case 16: return rows_inv_n<16, MODE>(a, n_lines, st);
-        case 32: return rows_inv_n<32, MODE>(a, n_lines, st);
-        case 64: return rows_inv_n<64, MODE>(a, n_lines, st);
-        case 128: return rows_inv_n<128, MODE>(a, n_lines, st);
-        case 256: return rows_inv_n<256, MODE>(a, n_lines, st);
-        case 512: return rows_inv_n<512, MODE>(a, n_lines, st);
-        case 1024: return rows_inv_n<1024, MODE>(a, n_lines, st);
-        case 2048: return rows_inv_n<2048, MODE>(a, n_lines, st);
-        default: return cudaErrorInvalidValue;
-    }
+constexpr int cols_nl() {  // column-tile width of the axis-0 / axis-1 passes (>= 2: 32-B runs)
+    constexpr int t = 128 / FftCfg<P>::TPL;
+    return t < 2 ? 2 : (t > 32 ? 32 : t);
 }
 
 }  // namespace
 
-int cols_tile_width(int P0) {
-    switch (P0) {
-        case 16: return cols_nl<16>();
-        case 32: return cols_nl<32>();
-        case 64: return cols_nl<64>();
-        case 128: return cols_nl<128>();
-        case 256: return cols_nl<256>();
-        case 512: return cols_nl<512>();
-        case 1024: return cols_nl<1024>();
-        case 2048: return cols_nl<2048>();
-        case 4096: return cols_nl<4096>();
-        default: return -1;
-    }
-}
-
-cudaError_t launch_rows_fwd(const PassArgs& a, int mode, cudaStream_t st) {
-    switch (mode) {
-        case RF_APPLY: return rows_fwd_mode<RF_APPLY>(a, st);
-        case RF_ADJ: return rows_fwd_mode<RF_ADJ>(a, st);
-        case RF_SPEC: return rows_fwd_mode<RF_SPEC>(a, st);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-cudaError_t launch_mid(const PassArgs& a, int mode, cudaStream_t st) {
-    switch (mode) {
-        case MM_FWD_APPLY: return mid_mode<MM_FWD_APPLY>(a, st);
-        case MM_FWD_ADJ: return mid_mode<MM_FWD_ADJ>(a, st);
-        case MM_FWD_SPEC: return mid_mode<MM_FWD_SPEC>(a, st);
-        case MM_INV_APPLY: return mid_mode<MM_INV_APPLY>(a, st);
-        case MM_INV_ADJ: return mid_mode<MM_INV_ADJ>(a, st);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-cudaError_t launch_cols(const PassArgs& a, int mode, cudaStream_t st) {
-    switch (mode) {
-        case CM_SPEC: return cols_mode<CM_SPEC>(a, st);
-        case CM_APPLY_LOCAL: return cols_mode<CM_APPLY_LOCAL>(a, st);
-        case CM_APPLY_GLOBAL: return cols_mode<CM_APPLY_GLOBAL>(a, st);
-        case CM_ADJ_LOCAL: return cols_mode<CM_ADJ_LOCAL>(a, st);
-        case CM_ADJ_GLOBAL: return cols_mode<CM_ADJ_GLOBAL>(a, st);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-cudaError_t launch_rows_inv(const PassArgs& a, int mode, int64_t n_lines, cudaStream_t st) {
-    return mode == RI_APPLY ? rows_inv_mode<RI_APPLY>(a, n_lines, st) : rows_inv_mode<RI_ADJ>(a, n_lines, st);
-}
-
-cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, const int64_t* x, double* out,
-                           int32_t* bad, cudaStream_t st) {
-    if (cnt <= 0) return cudaSuccess;
-    const int64_t blocks = (cnt + 255) / 256;
-    k_entries<<<(unsigned)(blocks < 148 * 64 ? blocks : 148 * 64), 256, 0, st>>>(a, cnt, y, x, out, bad);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
-                          const int32_t* bshape, double* out, int32_t* bad, cudaStream_t st) {
-    if (nblk <= 0) return cudaSuccess;
-    k_blocks<<<148 * 16, 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape, out, bad);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_probe_sums(int D, const int32_t* n, int32_t nbox, const int64_t* box_lo, const int64_t* box_hi,
-                              int32_t q, const double* Yt, const double* Y, double* d2, double* y2, cudaStream_t st) {
-    dim3 grid((unsigned)(nbox + 1), (unsigned)q);
-    k_probe_sums<<<grid, 256, 0, st>>>(D, n[0], n[1], D == 3 ? n[2] : 1, nbox, box_lo, box_hi, Yt, Y, d2, y2);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_block_direct(const EntryArgs& a, int32_t nblk, int64_t max_t, const int64_t* t_lo,
-                                const int64_t* t_hi, const int64_t* s_lo, const int64_t* s_hi, const int64_t* f_off,
-                                const int64_t* g_off, const double* f, double* g, int adjoint, int32_t* bad,
-                                cudaStream_t st) {
-    if (nblk <= 0) return cudaSuccess;
-    dim3 grid((unsigned)((max_t + 255) / 256), (unsigned)nblk);
-    k_block_direct<<<grid, 256, 0, st>>>(a, nblk, t_lo, t_hi, s_lo, s_hi, f_off, g_off, f, g, adjoint, bad);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_zero(double* p, int64_t n, cudaStream_t st) {
-    if (n <= 0) return cudaSuccess;
-    k_zero<<<148 * 8, 256, 0, st>>>(p, n);
-    return cudaGetLastError();
-}
+// line lengths compiled for each pass: 2^a * {1, 3, 9}
+#define PCB_ROW_SIZES(X) X(8) X(16) X(24) X(32) X(48) X(64) X(72) X(96) X(128) X(144) X(192) X(256) X(288) \
+    X(384) X(512) X(576) X(768) X(1024) X(1152) X(1536) X(2048)
+#define PCB_COL_SIZES(X) X(16) X(32) X(48) X(64) X(96) X(128) X(144) X(192) X(256) X(288) X(384) X(512) \
+    X(576) X(768) X(1024) X(1152) X(1536) X(2048) X(2304) X(3072) X(4096)
 
 }  // namespace pcb

@@ -1,0 +1,65 @@
+// Dispatch of the last-axis passes (K2 rows_fwd, K4 rows_inv) over the compiled lengths.
+#include "kernels_impl.cuh"
+
+namespace pcb {
+namespace {
+
+template <int N, int MODE>
+cudaError_t rows_fwd_n(const PassArgs& a, cudaStream_t st) {
+    constexpr int NL = rows_nl<N>();
+    const int64_t maxlines = MODE == RF_SPEC ? (a.D == 2 ? a.P[0] : (int64_t)a.P[0] * a.P[1]) : a.lines_max;
+    const int items = (MODE == RF_ADJ && a.global) ? a.B : a.n_slots * (MODE == RF_SPEC ? 1 : a.B);
+    dim3 grid((unsigned)((maxlines + NL - 1) / NL), (unsigned)items);
+    const size_t smem = sizeof(double2) * smem_words<N, NL>() + NL * (3 * sizeof(int64_t) + 2 * sizeof(int));
+    return launch_dyn(k_rows_fwd<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
+}
+
+template <int MODE>
+cudaError_t rows_fwd_mode(const PassArgs& a, cudaStream_t st) {
+    switch (a.P[a.D - 1] / 2) {
+#define PCB_CASE(n) \
+    case n: return rows_fwd_n<n, MODE>(a, st);
+        PCB_ROW_SIZES(PCB_CASE)
+#undef PCB_CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int N, int MODE>
+cudaError_t rows_inv_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
+    constexpr int NL = rows_nl<N>();
+    constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
+                                                                          : (NL * (2 * N + 1) + 1) / 2;
+    dim3 grid((unsigned)n_lines, (unsigned)a.B);
+    const size_t smem = sizeof(double2) * (BUFW + NL * (N + 1)) + sizeof(double) * ((size_t)a.n[a.D - 1] + 1) +
+                        NL * sizeof(GatherEntry) + 16;
+    return launch_dyn(k_rows_inv<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
+}
+
+template <int MODE>
+cudaError_t rows_inv_mode(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
+    switch (a.P[a.D - 1] / 2) {
+#define PCB_CASE(n) \
+    case n: return rows_inv_n<n, MODE>(a, n_lines, st);
+        PCB_ROW_SIZES(PCB_CASE)
+#undef PCB_CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_rows_fwd(const PassArgs& a, int mode, cudaStream_t st) {
+    switch (mode) {
+        case RF_APPLY: return rows_fwd_mode<RF_APPLY>(a, st);
+        case RF_ADJ: return rows_fwd_mode<RF_ADJ>(a, st);
+        case RF_SPEC: return rows_fwd_mode<RF_SPEC>(a, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_rows_inv(const PassArgs& a, int mode, int64_t n_lines, cudaStream_t st) {
+    return mode == RI_APPLY ? rows_inv_mode<RI_APPLY>(a, n_lines, st) : rows_inv_mode<RI_ADJ>(a, n_lines, st);
+}
+
+}  // namespace pcb

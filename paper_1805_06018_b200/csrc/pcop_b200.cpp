@@ -29,6 +29,7 @@
 #include <string>
 #include <vector>
 
+#include "fft.cuh"
 #include "kernels.cuh"
 #include "pcb/pcb.h"
 
@@ -98,10 +99,23 @@ struct DevBuf {
     size_t bytes() const { return n * sizeof(T); }
 };
 
-int64_t pow2_at_least(int64_t v) {
-    int64_t p = 16;
-    while (p < v) p <<= 1;
-    return p;
+bool g_pow2_only = false;    // PCB_POW2=1: power-of-two FFT sizes only (A/B measurement)
+bool g_mixed_last = false;   // PCB_MIXED_LAST=1: 3-smooth sizes on the R2C axis too (default: pow2 there)
+
+// Smallest compiled FFT size >= max(v, 16): 2^a * {1, 3, 9}.  The last (R2C) axis also needs its
+// half length P/2 compiled for the row passes.
+int64_t fft_size_at_least(int64_t v, bool last_axis) {
+    for (int64_t p = 16; p <= (last_axis ? 4096 : 4096); p += 8) {
+        if (p < v) continue;
+        if (!fft_len_ok((int)p)) continue;
+        if (g_pow2_only && !is_pow2c((int)p)) continue;
+        if (last_axis && (!fft_len_ok((int)(p / 2)) || p / 2 > 2048 ||
+                          ((g_pow2_only || !g_mixed_last) && !is_pow2c((int)(p / 2)))))
+            continue;
+        if (!last_axis && cols_tile_width((int)p) < 0) continue;
+        return p;
+    }
+    return INT64_MAX / 4;  // unsupported: the caller rejects the plan
 }
 
 struct HBox {
@@ -214,7 +228,9 @@ pcb_status guarded(Fn&& fn) {
 
 void make_twiddles(pcb_op* op) {
     std::vector<double2> h;
-    for (int len = 8; len <= 8192; len <<= 1) {
+    for (int len = 8; len <= 8192; len += 8) {
+        if (!fft_len_ok(len)) continue;
+        if ((long long)h.size() != tw_offset(len)) fail(PCB_EINTERNAL, "twiddle table layout mismatch");
         for (int m = 0; m < len; ++m) {
             const long double ang = -2.0L * 3.141592653589793238462643383279502884L * (long double)m / (long double)len;
             h.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
@@ -533,10 +549,10 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     for (int a = 0; a < D; ++a) {
         int64_t mmax = 1;
         for (int k : mine) mmax = std::max<int64_t>(mmax, op->terms[k].m[a]);
-        Pg[a] = pow2_at_least(op->n[a] + mmax - 1);
+        Pg[a] = fft_size_at_least(op->n[a] + mmax - 1, a == D - 1);
     }
     auto local_P = [&](int k, int a) {
-        return pow2_at_least((int64_t)op->terms[k].m[a] + op->terms[k].k_ext[a] - 1);
+        return fft_size_at_least((int64_t)op->terms[k].m[a] + op->terms[k].k_ext[a] - 1, a == D - 1);
     };
     bool global_ok = true, local_ok = true;
     for (int a = 0; a < D; ++a) global_ok = global_ok && Pg[a] <= 4096;
@@ -978,6 +994,11 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
         PCB_CK(cudaGetDeviceProperties(&prop, op->device));
         if (prop.major < 10) fail(PCB_ECUDA, "pcop-b200 kernels are built for sm_100a (Blackwell B200)");
         op->max_batch = opt.max_batch > 0 ? opt.max_batch : 16;
+        if (const char* e = getenv("PCB_POW2")) g_pow2_only = atoi(e) != 0;
+        // 3-smooth sizes on the R2C axis pay off in 3-D (c4: +4%) but not in 2-D, where the
+        // 24-element row kernels lose more to register pressure than they save (c3, c2: measured)
+        g_mixed_last = dim == 3;
+        if (const char* e = getenv("PCB_MIXED_LAST")) g_mixed_last = atoi(e) != 0;
 
         PCB_CK(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
 
