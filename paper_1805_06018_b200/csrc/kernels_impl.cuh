@@ -347,20 +347,36 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
     }
 
     if (MODE == CM_APPLY_GLOBAL) {
+        // Phi_k tile (P0 x NL contiguous, tile-major) streamed into shared memory with async copies
+        // issued before the term's forward FFT, so the HBM stream overlaps the transform
+        double2* sspec = buf + smem_words<P0, NL>();
         const int vec = item;
         double2 acc[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = czero();
+        constexpr bool STAGE = P0 <= 512;  // long columns: direct loads measured faster (c3 GLOBAL)
         for (int slot = 0; slot < a.n_slots; ++slot) {
             const TermDesc& td = a.terms[a.slots[slot]];
+            const double2* tile = a.spec_pool + td.spec_off + (c0 / NL) * (int64_t)P0 * NL;
+            if (STAGE) {
+                __syncthreads();  // previous term's product finished reading sspec
+                for (int i = threadIdx.x; i < P0 * NL; i += NL * FftCfg<P0>::TPL) cp_async16(&sspec[i], tile + i);
+                asm volatile("cp.async.commit_group;\n" ::);
+            }
             const double2* S_item = a.S + td.s_pool + vec * td.s_vst;
             load_in(S_item, 0, td.m[0], v);
             fft_fwd_order<P0, -1, NL, PSH<NL>>(v, buf, l, tl, tw0);
-            const double2* spec = a.spec_pool + td.spec_off + tile_off;
+            if (STAGE) {
+                asm volatile("cp.async.wait_group 0;\n" ::);
+                __syncthreads();
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const double2 ph = cvalid ? __ldg(&spec[(int64_t)fpos(r) * NL]) : czero();
-                acc[r] = cadd(acc[r], cmul(v[r], ph));
+                for (int r = 0; r < R; ++r) acc[r] = cadd(acc[r], cmul(v[r], sspec[fpos(r) * NL + l]));
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const double2 ph = cvalid ? __ldg(&tile[(int64_t)fpos(r) * NL + l]) : czero();
+                    acc[r] = cadd(acc[r], cmul(v[r], ph));
+                }
             }
         }
         fft_rev_order<P0, +1, NL, PSH<NL>>(acc, buf, l, tl, tw0);
@@ -369,21 +385,31 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
         return;
     }
 
-    // CM_ADJ_GLOBAL: one forward transform of g, one pruned inverse per term
+    // CM_ADJ_GLOBAL: one forward transform of g, one pruned inverse per term; Phi_{k+1}'s tile
+    // streams into the other shared buffer while term k's inverse runs
     {
+        double2* sspec = buf + smem_words<P0, NL>();
         const int vec = item;
         const TermDesc& g = *a.gdesc;
         double2 x[R];
         load_in(a.S + g.s_pool + vec * g.s_vst, g.o_lo[0], g.o_cnt[0], x);
+        auto issue = [&](int slot) {
+            const TermDesc& td = a.terms[a.slots[slot]];
+            const double2* tile = a.spec_pool + td.spec_off + (c0 / NL) * (int64_t)P0 * NL;
+            double2* dst = sspec + (slot & 1) * P0 * NL;
+            for (int i = threadIdx.x; i < P0 * NL; i += NL * FftCfg<P0>::TPL) cp_async16(&dst[i], tile + i);
+            asm volatile("cp.async.commit_group;\n" ::);
+        };
+        if (a.n_slots > 0) issue(0);
         fft_fwd_order<P0, -1, NL, PSH<NL>>(x, buf, l, tl, tw0);
         for (int slot = 0; slot < a.n_slots; ++slot) {
             const TermDesc& td = a.terms[a.slots[slot]];
-            const double2* spec = a.spec_pool + td.spec_off + tile_off;
+            asm volatile("cp.async.wait_group 0;\n" ::);
+            __syncthreads();  // tile `slot` landed; the other buffer is free again
+            if (slot + 1 < a.n_slots) issue(slot + 1);
+            const double2* sp = sspec + (slot & 1) * P0 * NL;
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const double2 ph = cvalid ? __ldg(&spec[(int64_t)fpos(r) * NL]) : czero();
-                v[r] = cmulc(x[r], ph);
-            }
+            for (int r = 0; r < R; ++r) v[r] = cmulc(x[r], sp[fpos(r) * NL + l]);
             fft_rev_order<P0, +1, NL, PSH<NL>>(v, buf, l, tl, tw0);
             store_out(a.T + td.t_pool + vec * td.t_vst, 0, td.m[0], v);
         }
