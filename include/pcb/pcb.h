@@ -77,6 +77,11 @@ typedef struct pcb_info {
     double flops_per_vector;  /* nominal fp64 flops per applied vector */
     int32_t launches_per_batch; /* kernels launched by one apply batch call */
     int32_t reserved;
+    /* per applied vector, per kernel family {rows_fwd, mid, cols, rows_inv}: the bytes the kernel
+     * must read and write once (its inputs and outputs in this pipeline) and nominal fp64 flops
+     * (2.5 P log2 P per real line, 5 P log2 P per complex line, 8 per complex MAC) */
+    double kernel_bytes[4];
+    double kernel_flops[4];
 } pcb_info;
 
 PCB_API void pcb_default_options(pcb_options* opt);

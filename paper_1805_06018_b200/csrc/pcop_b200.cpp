@@ -829,6 +829,43 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     in.bytes_per_vector = sb + 16.0 * (double)op->N;
     in.flops_per_vector = mode == PCB_MODE_GLOBAL ? g_fl : l_fl;
     in.launches_per_batch = (int)(2 * op->classes.size() + op->groups.size() * (D == 3 ? 3 : 1));
+    // per-kernel compulsory bytes and nominal flops per vector (apply)
+    for (int i = 0; i < 4; ++i) in.kernel_bytes[i] = in.kernel_flops[i] = 0.0;
+    {
+        const bool gl = mode == PCB_MODE_GLOBAL;
+        for (const Group& g : op->groups) {
+            const double P0 = g.P[0], P1 = D == 3 ? g.P[1] : 1, Pl = g.P[D - 1];
+            const double Nc = Pl / 2 + 1;  // stored half-spectrum bins per row
+            const double lines_cols = (D == 3 ? P1 : 1) * Nc;
+            for (int k : g.terms) {
+                const TermDesc& t = op->terms[k];
+                const double mlead = D == 2 ? t.m[0] : (double)t.m[0] * t.m[1];
+                const double mall = mlead * t.m[D - 1];
+                const double olead = D == 2 ? t.o_cnt[0] : (double)t.o_cnt[0] * t.o_cnt[1];
+                in.kernel_bytes[0] += mall * 16.0 + mlead * Nc * 16.0;              // f, w in; S out
+                in.kernel_flops[0] += mlead * fft_flops_r(Pl);
+                if (D == 3) {
+                    in.kernel_bytes[1] += 2.0 * t.m[0] * P1 * Nc * 16.0;
+                    in.kernel_flops[1] += t.m[0] * Nc * fft_flops_c(P1) + (gl ? 0.0 : t.o_cnt[0] * Nc * fft_flops_c(P1));
+                }
+                in.kernel_bytes[2] += (t.m[0] * lines_cols + P0 * lines_cols) * 16.0 +  // S in, spectrum
+                                      (gl ? 0.0 : t.o_cnt[0] * lines_cols * 16.0);      // T out (local)
+                in.kernel_flops[2] += lines_cols * (fft_flops_c(P0) * (gl ? 1.0 : 2.0) + 8.0 * P0);
+                if (!gl) {
+                    in.kernel_bytes[3] += olead * (Nc * 16.0 + t.o_cnt[D - 1] * 8.0);  // T in, contributions
+                    in.kernel_flops[3] += olead * fft_flops_r(Pl);
+                }
+            }
+            if (gl) {  // the single inverse per vector
+                const double lead = D == 2 ? op->n[0] : (double)op->n[0] * op->n[1];
+                in.kernel_bytes[2] += op->n[0] * lines_cols * 16.0;
+                in.kernel_flops[2] += lines_cols * fft_flops_c(P0);
+                if (D == 3) in.kernel_flops[1] += op->n[0] * Nc * fft_flops_c(P1);
+                in.kernel_bytes[3] += lead * Nc * 16.0 + (double)op->N * 8.0;
+                in.kernel_flops[3] += lead * fft_flops_r(Pl);
+            }
+        }
+    }
 }
 
 void build_spectra(pcb_op* op) {

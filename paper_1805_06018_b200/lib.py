@@ -21,6 +21,7 @@ P_dbl = ctypes.POINTER(dbl)
 STATUS = {0: "PCB_OK", 1: "PCB_EINVAL", 2: "PCB_ENOMEM", 3: "PCB_ECUDA", 4: "PCB_ENCCL", 5: "PCB_EINTERNAL"}
 MODES = {"auto": 0, "global": 1, "local": 2}
 MODE_NAMES = {v: k for k, v in MODES.items()}
+KERNEL_FAMILIES = ("rows_fwd", "mid", "cols", "rows_inv")
 
 # every symbol include/pcb/pcb.h declares
 EXPORTS = ["pcb_default_options", "pcb_last_error", "pcb_create", "pcb_destroy", "pcb_get_info", "pcb_apply_batch",
@@ -38,7 +39,7 @@ class Info(ctypes.Structure):
     _fields_ = [("dim", i32), ("rank", i32), ("rank_active", i32), ("mode", i32), ("n_groups", i32),
                 ("fft_size", i32 * 3), ("n_points", i64), ("spectra_bytes", i64), ("device_bytes", i64),
                 ("bytes_per_vector", dbl), ("flops_per_vector", dbl), ("launches_per_batch", i32),
-                ("reserved", i32)]
+                ("reserved", i32), ("kernel_bytes", dbl * 4), ("kernel_flops", dbl * 4)]
 
     def as_dict(self) -> dict:
         return {"dim": self.dim, "rank": self.rank, "rank_active": self.rank_active,
@@ -46,7 +47,9 @@ class Info(ctypes.Structure):
                 "fft_size": [self.fft_size[i] for i in range(self.dim)], "n_points": self.n_points,
                 "spectra_bytes": self.spectra_bytes, "device_bytes": self.device_bytes,
                 "bytes_per_vector": self.bytes_per_vector, "flops_per_vector": self.flops_per_vector,
-                "launches_per_batch": self.launches_per_batch}
+                "launches_per_batch": self.launches_per_batch,
+                "kernel_bytes": dict(zip(KERNEL_FAMILIES, list(self.kernel_bytes))),
+                "kernel_flops": dict(zip(KERNEL_FAMILIES, list(self.kernel_flops)))}
 
 
 class PcbError(RuntimeError):
