@@ -256,12 +256,30 @@ __device__ __forceinline__ void stage_store(const double2* v, double2* buf, int 
     }
 }
 
+// First forward stage (span 1, no twiddles) for inputs known to vanish at positions >= m_valid:
+// a butterfly whose inputs r >= 1 all lie beyond m_valid is a broadcast of its r = 0 input.
+template <int L, int RS, int DIR>
+__device__ __forceinline__ void stage0_pruned(double2* v, int tl, int m_valid) {
+    constexpr int E = FftCfg<L>::R;
+    constexpr int TPL = FftCfg<L>::TPL;
+#pragma unroll
+    for (int b = 0; b < E / RS; ++b) {
+        const int j = tl + b * TPL;
+        if (j + L / RS >= m_valid) {
+#pragma unroll
+            for (int r = 1; r < RS; ++r) v[b * RS + r] = v[b * RS];
+        } else {
+            dft<RS, DIR>(&v[b * RS]);
+        }
+    }
+}
+
 // forward stages s..NSTG-1; stage 0 consumes the caller's registers, the last leaves the
 // result in registers
-template <int L, int DIR, int NL, int PS, int s>
+template <int L, int DIR, int NL, int PS, int s, bool PRUNE>
 struct FwdStages {
     static __device__ __forceinline__ void run(double2* v, double2* buf, int l, int tl,
-                                               const double2* __restrict__ tw) {
+                                               const double2* __restrict__ tw, int m_valid) {
         constexpr int NSTG = FftCfg<L>::NSTG;
         if constexpr (s < NSTG) {
             constexpr int RS = FftCfg<L>::radix(s);
@@ -270,11 +288,12 @@ struct FwdStages {
                 __syncthreads();
                 stage_load<L, RS, NL, PS>(v, buf, l, tl);
             }
-            stage_math<L, RS, NS, DIR>(v, tl, tw);
+            if constexpr (s == 0 && PRUNE) stage0_pruned<L, RS, DIR>(v, tl, m_valid);
+            else stage_math<L, RS, NS, DIR>(v, tl, tw);
             if constexpr (s + 1 < NSTG) {
                 __syncthreads();
                 stage_store<L, RS, NS, NL, PS>(v, buf, l, tl);
-                FwdStages<L, DIR, NL, PS, s + 1>::run(v, buf, l, tl, tw);
+                FwdStages<L, DIR, NL, PS, s + 1, PRUNE>::run(v, buf, l, tl, tw, m_valid);
             }
         }
     }
@@ -304,10 +323,11 @@ struct RevStages {
 };
 
 // Forward-ordered transform: v holds inputs at FirstPos; on return v[r] = X[tl + r*L/E].
-template <int L, int DIR, int NL, int PS>
+// Inputs at positions >= m_valid must be zero (pruned first stage).
+template <int L, int DIR, int NL, int PS, bool PRUNE = false>
 __device__ __forceinline__ void fft_fwd_order(double2* v, double2* buf, int l, int tl,
-                                              const double2* __restrict__ tw) {
-    FwdStages<L, DIR, NL, PS, 0>::run(v, buf, l, tl, tw);
+                                              const double2* __restrict__ tw, int m_valid = L) {
+    FwdStages<L, DIR, NL, PS, 0, PRUNE>::run(v, buf, l, tl, tw, m_valid);
 }
 
 // Reverse-ordered transform: v[r] holds x[tl + r*L/E] (what fft_fwd_order leaves); on return

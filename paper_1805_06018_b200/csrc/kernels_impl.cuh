@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
             }
             const double2* S_item = a.S + td.s_pool + vec * td.s_vst;
             load_in(S_item, 0, td.m[0], v);
-            fft_fwd_order<P0, -1, NL, PSH<NL>>(v, buf, l, tl, tw0);
+            fft_fwd_order<P0, -1, NL, PSH<NL>, true>(v, buf, l, tl, tw0, td.m[0]);
             if (STAGE) {
                 asm volatile("cp.async.wait_group 0;\n" ::);
                 __syncthreads();

@@ -104,13 +104,13 @@ bool g_mixed_last = false;   // PCB_MIXED_LAST=1: 3-smooth sizes on the R2C axis
 
 // Smallest compiled FFT size >= max(v, 16): 2^a * {1, 3, 9}.  The last (R2C) axis also needs its
 // half length P/2 compiled for the row passes.
-int64_t fft_size_at_least(int64_t v, bool last_axis) {
+int64_t fft_size_at_least(int64_t v, bool last_axis, bool mixed_last) {
     for (int64_t p = 16; p <= (last_axis ? 4096 : 4096); p += 8) {
         if (p < v) continue;
         if (!fft_len_ok((int)p)) continue;
         if (g_pow2_only && !is_pow2c((int)p)) continue;
         if (last_axis && (!fft_len_ok((int)(p / 2)) || p / 2 > 2048 ||
-                          ((g_pow2_only || !g_mixed_last) && !is_pow2c((int)(p / 2)))))
+                          ((g_pow2_only || !mixed_last) && !is_pow2c((int)(p / 2)))))
             continue;
         if (!last_axis && cols_tile_width((int)p) < 0) continue;
         return p;
@@ -549,10 +549,11 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     for (int a = 0; a < D; ++a) {
         int64_t mmax = 1;
         for (int k : mine) mmax = std::max<int64_t>(mmax, op->terms[k].m[a]);
-        Pg[a] = fft_size_at_least(op->n[a] + mmax - 1, a == D - 1);
+        // GLOBAL: 3-smooth sizes on every axis (its row passes are not the bottleneck)
+        Pg[a] = fft_size_at_least(op->n[a] + mmax - 1, a == D - 1, true);
     }
     auto local_P = [&](int k, int a) {
-        return fft_size_at_least((int64_t)op->terms[k].m[a] + op->terms[k].k_ext[a] - 1, a == D - 1);
+        return fft_size_at_least((int64_t)op->terms[k].m[a] + op->terms[k].k_ext[a] - 1, a == D - 1, g_mixed_last);
     };
     bool global_ok = true, local_ok = true;
     for (int a = 0; a < D; ++a) global_ok = global_ok && Pg[a] <= 4096;
