@@ -148,6 +148,20 @@ PCB_API pcb_status pcb_probe_estimate_dev(pcb_op* op, int32_t q, const double* d
                                           int32_t nleaf, const int64_t* leaf_lo, const int64_t* leaf_hi,
                                           double* eta_cells, double* eta_abs, double* eta_rel, void* stream);
 
+/* True operator of the benchmark configurations (reference roles:
+ * compute_impulse impulse.cpp:5-15 and make_probes' Y = A^* Z adaptivity.cpp:14-28):
+ *   A[y,x] = exp(-sum_a (y_a-x_a)^2 / (2 s_a(x)^2)) / Z(x) on sum_a ((y_a-x_a)/s_a(x))^2 <= 16,
+ * domain [0, n_a) per axis, per-source widths sigma (N x dim), Z(x) = the full-lattice sum of the
+ * truncated kernel (computed on the device at create).  Direct fp64 stencils. */
+typedef struct pcb_blur pcb_blur;
+PCB_API pcb_status pcb_blur_create(int32_t dim, const int64_t* n, const double* sigma, pcb_blur** out);
+PCB_API pcb_status pcb_blur_destroy(pcb_blur* blur);
+/* B vectors (B x N); adjoint != 0 applies A^*.  device_ptrs != 0: F, G on the device, ordered on
+ * `stream`; otherwise host pointers (synchronous). */
+PCB_API pcb_status pcb_blur_apply(pcb_blur* blur, int32_t B, const double* F, double* G, int32_t adjoint,
+                                  int32_t device_ptrs, void* stream);
+PCB_API const char* pcb_blur_last_error(void);
+
 /* Number of kernels this library has launched in the process (all handles). */
 PCB_API long long pcb_launch_count(void);
 

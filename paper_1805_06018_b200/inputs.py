@@ -191,6 +191,10 @@ class BlurSpec:
     def radius(self, x: Tuple[int, ...]) -> Tuple[int, ...]:
         return tuple(int(math.floor(4.0 * s)) for s in self.sigma(x))
 
+    def sigma_field(self) -> np.ndarray:
+        """Per-source widths on the whole lattice, shape (n^dim, dim), lexicographic (last axis fastest)."""
+        return np.array([self.sigma(x) for x in np.ndindex(*([self.n] * self.dim))], dtype=np.float64)
+
     def kernel(self, x: Tuple[int, ...]) -> Tuple[Tuple[int, ...], np.ndarray]:
         """Normalised truncated kernel on its support box [-R, R]; returns (lo, values)."""
         s = self.sigma(x)

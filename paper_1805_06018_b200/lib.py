@@ -27,7 +27,8 @@ KERNEL_FAMILIES = ("rows_fwd", "mid", "cols", "rows_inv")
 EXPORTS = ["pcb_default_options", "pcb_last_error", "pcb_create", "pcb_destroy", "pcb_get_info", "pcb_apply_batch",
            "pcb_apply_adjoint_batch", "pcb_apply_batch_dev", "pcb_apply_adjoint_batch_dev", "pcb_entries",
            "pcb_blocks", "pcb_blocks_dev", "pcb_probe_estimate", "pcb_probe_estimate_dev", "pcb_launch_count",
-           "pcb_normal_fill", "pcb_uniform_int_fill", "pcb_profile_begin", "pcb_profile_end", "pcb_apply_block"]
+           "pcb_normal_fill", "pcb_uniform_int_fill", "pcb_profile_begin", "pcb_profile_end", "pcb_apply_block",
+           "pcb_blur_create", "pcb_blur_destroy", "pcb_blur_apply", "pcb_blur_last_error"]
 
 
 class Options(ctypes.Structure):
@@ -93,8 +94,12 @@ def load():
     L.pcb_profile_end.argtypes = [vp, i32, vp, vp, vp, ctypes.POINTER(i32)]
     L.pcb_normal_fill.argtypes = [ctypes.c_uint64, i64, vp]
     L.pcb_uniform_int_fill.argtypes = [ctypes.c_uint64, i64, i64, i64, vp]
+    L.pcb_blur_create.argtypes = [i32, P_i64, vp, ctypes.POINTER(vp)]
+    L.pcb_blur_destroy.argtypes = [vp]
+    L.pcb_blur_apply.argtypes = [vp, i32, vp, vp, i32, i32, vp]
+    L.pcb_blur_last_error.restype = ctypes.c_char_p
     for n in EXPORTS:
-        if n not in ("pcb_default_options", "pcb_last_error", "pcb_launch_count"):
+        if n not in ("pcb_default_options", "pcb_last_error", "pcb_launch_count", "pcb_blur_last_error"):
             getattr(L, n).restype = ctypes.c_int
     _lib = L
     return L
@@ -103,6 +108,11 @@ def load():
 def check(rc: int) -> None:
     if rc != 0:
         raise PcbError(rc, load().pcb_last_error().decode())
+
+
+def check_blur(rc: int) -> None:
+    if rc != 0:
+        raise PcbError(rc, load().pcb_blur_last_error().decode())
 
 
 def default_options() -> Options:
