@@ -162,6 +162,30 @@ PCB_API pcb_status pcb_blur_apply(pcb_blur* blur, int32_t B, const double* F, do
                                   int32_t device_ptrs, void* stream);
 PCB_API const char* pcb_blur_last_error(void);
 
+/* GPU-resident a-posteriori estimator state (adaptivity.hpp:14-56):
+ *   pcb_estimator_create    make_probes' Z: q probes of mt19937_64(seed) via std::normal_distribution,
+ *                           probe i = draws [iN, (i+1)N) (adaptivity.cpp:14-28); device-resident
+ *   pcb_estimator_set_y     Y = A^* Z from the caller (host or device pointer), or
+ *   pcb_estimator_set_y_blur   computed on the device by a pcb_blur true operator;
+ *                           ||Y||_F as make_estimator_state (adaptivity.cpp:30-37)
+ *   pcb_estimator_update    update_samples (adaptivity.cpp:75-112) incl. its changed_ks checks:
+ *                           Ytilde = Atilde^* Z, eta_abs = sqrt(||Ytilde - Y||^2 / q), eta_rel
+ *   pcb_estimator_cells     eta_for_cells (adaptivity.cpp:114-121) over inclusive leaf boxes
+ *   pcb_estimator_probes    the device pointers of Z, Y, Ytilde (q x N each)
+ *   pcb_estimator_read      copies Z / Y / Ytilde to the host (any may be NULL) */
+typedef struct pcb_estimator pcb_estimator;
+PCB_API pcb_status pcb_estimator_create(int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t q,
+                                        uint64_t seed, int32_t device, pcb_estimator** out);
+PCB_API pcb_status pcb_estimator_destroy(pcb_estimator* est);
+PCB_API pcb_status pcb_estimator_probes(pcb_estimator* est, double** dZ, double** dY, double** dYtilde);
+PCB_API pcb_status pcb_estimator_set_y(pcb_estimator* est, const double* Y, int32_t device_ptr);
+PCB_API pcb_status pcb_estimator_set_y_blur(pcb_estimator* est, pcb_blur* blur);
+PCB_API pcb_status pcb_estimator_update(pcb_estimator* est, pcb_op* op, int32_t nchanged, const int32_t* changed_ks,
+                                        double* eta_abs, double* eta_rel);
+PCB_API pcb_status pcb_estimator_cells(pcb_estimator* est, int32_t nleaf, const int64_t* leaf_lo,
+                                       const int64_t* leaf_hi, double* eta_cells);
+PCB_API pcb_status pcb_estimator_read(pcb_estimator* est, double* Z, double* Y, double* Ytilde);
+
 /* Number of kernels this library has launched in the process (all handles). */
 PCB_API long long pcb_launch_count(void);
 

@@ -25,7 +25,9 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <memory>
 #include <random>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -1433,6 +1435,241 @@ PCB_API pcb_status pcb_probe_estimate_dev(pcb_op* op, int32_t q, const double* d
         set_device(op);
         estimate_common(op, q, dZ, dY, dYt, nleaf, leaf_lo, leaf_hi, eta_cells, eta_abs, eta_rel,
                         (cudaStream_t)stream);
+    });
+}
+
+// ---------------------------------------------------------------------------------------------
+// GPU-resident estimator state: make_probes / make_estimator_state /
+// update_samples / eta_for_cells, adaptivity.cpp:14-121.  Z, Y = A^* Z and Ytilde = Atilde^* Z live
+// on the device for the whole adaptive loop; only eta values cross to the host.
+//
+// update_samples keeps the reference's bookkeeping and argument checks (adaptivity.cpp:79-88) but
+// recomputes Ytilde with ONE fused adjoint pass over the q probes instead of re-convolving only
+// the changed terms' Theta_{k,i} (adaptivity.cpp:90-100): on a B200 the whole Atilde^* Z costs
+// q adjoint applies (c3, q = 5: ~1.5 ms), less than per-term cache maintenance.  The results are
+// identical whenever the cached Theta of the unchanged terms is still valid, which is the
+// reference's own contract for changed_ks.
+
+}  // extern "C"
+
+struct pcb_estimator {
+    std::mutex mu;
+    int device = 0;
+    int D = 0;
+    int64_t dom_lo[3] = {0, 0, 0};
+    int32_t n[3] = {1, 1, 1};
+    int64_t N = 0;
+    int32_t q = 0;
+    DevBuf<double> Z, Y, Yt;
+    DevBuf<int64_t> blo, bhi;
+    DevBuf<double> aux;
+    bool have_y = false;
+    bool have_yt = false;
+    double y_norm = 0.0;
+    int32_t cached = 0;  // size of the reference's theta cache
+    double eta_abs = 0.0, eta_rel = 0.0;
+    cudaStream_t stream = nullptr;
+};
+
+namespace {
+
+// sum over boxes (domain-relative, inclusive) of ||Yt - Y||^2 per probe, plus the whole domain
+void est_sums(pcb_estimator* e, int32_t nleaf, const int64_t* leaf_lo, const int64_t* leaf_hi, std::vector<double>& h) {
+    std::vector<int64_t> lo, hi;
+    for (int32_t c = 0; c < nleaf; ++c)
+        for (int a = 0; a < e->D; ++a) {
+            const int64_t l = leaf_lo[c * e->D + a] - e->dom_lo[a], u = leaf_hi[c * e->D + a] - e->dom_lo[a];
+            if (l < 0 || u >= e->n[a] || l > u) fail(PCB_EINVAL, "eta_for_cells: leaf box outside the domain");
+            lo.push_back(l);
+            hi.push_back(u);
+        }
+    e->blo.ensure(std::max<size_t>(1, lo.size()));
+    e->bhi.ensure(std::max<size_t>(1, hi.size()));
+    const size_t nd2 = (size_t)(nleaf + 1) * e->q;
+    e->aux.ensure(nd2 + e->q);
+    if (!lo.empty()) {
+        PCB_CK(cudaMemcpyAsync(e->blo.p, lo.data(), lo.size() * 8, cudaMemcpyHostToDevice, e->stream));
+        PCB_CK(cudaMemcpyAsync(e->bhi.p, hi.data(), hi.size() * 8, cudaMemcpyHostToDevice, e->stream));
+    }
+    launch_ck(launch_probe_sums(e->D, e->n, nleaf, e->blo.p, e->bhi.p, e->q, e->Yt.p, e->Y.p, e->aux.p, e->aux.p + nd2,
+                                e->stream),
+              "probe_sums");
+    g_launches.fetch_add(1);
+    h.resize(nd2 + e->q);
+    PCB_CK(cudaMemcpyAsync(h.data(), e->aux.p, h.size() * 8, cudaMemcpyDeviceToHost, e->stream));
+    PCB_CK(cudaStreamSynchronize(e->stream));
+}
+
+template <typename Fn>
+pcb_status est_guarded(pcb_estimator* e, Fn&& fn) {
+    if (!e) {
+        set_err("null estimator");
+        return PCB_EINVAL;
+    }
+    std::lock_guard<std::mutex> lk(e->mu);
+    return guarded([&] {
+        PCB_CK(cudaSetDevice(e->device));
+        fn();
+    });
+}
+
+void est_finish_y(pcb_estimator* e) {
+    std::vector<double> h;
+    est_sums(e, 0, nullptr, nullptr, h);  // y2 per probe lands after the (empty) box sums
+    double y2 = 0.0;
+    for (int i = 0; i < e->q; ++i) y2 += h[(size_t)e->q + i];
+    e->y_norm = std::sqrt(y2);
+    e->have_y = true;
+}
+
+}  // namespace
+
+extern "C" {
+
+PCB_API pcb_status pcb_estimator_create(int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t q,
+                                        uint64_t seed, int32_t device, pcb_estimator** out) {
+    if (!out) {
+        set_err("null output handle");
+        return PCB_EINVAL;
+    }
+    *out = nullptr;
+    return guarded([&] {
+        if (q < 1) fail(PCB_EINVAL, "make_probes: q >= 1 required");
+        if (dim < 1 || dim > 3 || !dom_lo || !dom_hi) fail(PCB_EINVAL, "bad domain");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+            (void)cudaGetLastError();
+            fail(PCB_ECUDA, "no CUDA device: the pcop-b200 estimator has no CPU fallback");
+        }
+        std::unique_ptr<pcb_estimator> e(new pcb_estimator);
+        if (device < 0) PCB_CK(cudaGetDevice(&device));
+        e->device = device;
+        PCB_CK(cudaSetDevice(device));
+        PCB_CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        e->D = dim;
+        e->N = 1;
+        for (int a = 0; a < dim; ++a) {
+            if (dom_hi[a] < dom_lo[a]) fail(PCB_EINVAL, "empty domain");
+            e->dom_lo[a] = dom_lo[a];
+            e->n[a] = (int32_t)(dom_hi[a] - dom_lo[a] + 1);
+            e->N *= e->n[a];
+        }
+        e->q = q;
+        const size_t cnt = (size_t)q * e->N;
+        // probe i = draws [i N, (i+1) N) of mt19937_64(seed) through std::normal_distribution (adaptivity.cpp:19-23)
+        std::vector<double> z(cnt);
+        std::mt19937_64 rng(seed);
+        std::normal_distribution<double> gauss(0.0, 1.0);
+        for (size_t i = 0; i < cnt; ++i) z[i] = gauss(rng);
+        e->Z.alloc(cnt);
+        e->Y.alloc(cnt);
+        e->Yt.alloc(cnt);
+        PCB_CK(cudaMemcpyAsync(e->Z.p, z.data(), cnt * 8, cudaMemcpyHostToDevice, e->stream));
+        PCB_CK(cudaStreamSynchronize(e->stream));
+        *out = e.release();
+    });
+}
+
+PCB_API pcb_status pcb_estimator_destroy(pcb_estimator* e) {
+    if (!e) return PCB_OK;
+    {
+        std::lock_guard<std::mutex> lk(e->mu);
+        cudaSetDevice(e->device);
+        if (e->stream) cudaStreamDestroy(e->stream);
+        e->stream = nullptr;
+    }
+    delete e;
+    return PCB_OK;
+}
+
+PCB_API pcb_status pcb_estimator_probes(pcb_estimator* e, double** dZ, double** dY, double** dYtilde) {
+    return est_guarded(e, [&] {
+        if (dZ) *dZ = e->Z.p;
+        if (dY) *dY = e->Y.p;
+        if (dYtilde) *dYtilde = e->Yt.p;
+    });
+}
+
+PCB_API pcb_status pcb_estimator_set_y(pcb_estimator* e, const double* Y, int32_t device_ptr) {
+    return est_guarded(e, [&] {
+        if (!Y) fail(PCB_EINVAL, "null Y");
+        PCB_CK(cudaMemcpyAsync(e->Y.p, Y, (size_t)e->q * e->N * 8,
+                               device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->stream));
+        PCB_CK(cudaMemsetAsync(e->Yt.p, 0, (size_t)e->q * e->N * 8, e->stream));
+        est_finish_y(e);
+    });
+}
+
+PCB_API pcb_status pcb_estimator_set_y_blur(pcb_estimator* e, pcb_blur* blur) {
+    return est_guarded(e, [&] {
+        if (!blur) fail(PCB_EINVAL, "null blur handle");
+        const pcb_status rc = pcb_blur_apply(blur, e->q, e->Z.p, e->Y.p, 1, 1, e->stream);
+        if (rc != PCB_OK) fail(rc, std::string("Y = A^* Z: ") + pcb_blur_last_error());
+        PCB_CK(cudaMemsetAsync(e->Yt.p, 0, (size_t)e->q * e->N * 8, e->stream));
+        est_finish_y(e);
+    });
+}
+
+PCB_API pcb_status pcb_estimator_update(pcb_estimator* e, pcb_op* op, int32_t nchanged, const int32_t* changed_ks,
+                                        double* eta_abs, double* eta_rel) {
+    if (!op) {
+        set_err("null handle");
+        return PCB_EINVAL;
+    }
+    std::lock_guard<std::mutex> lk(op->mu);
+    return est_guarded(e, [&] {
+        if (!e->have_y) fail(PCB_EINVAL, "update_samples: Y = A^* Z not set");
+        if (op->D != e->D || op->N != e->N || op->device != e->device)
+            fail(PCB_EINVAL, "update_samples: operator domain / device differs from the probes'");
+        for (int a = 0; a < e->D; ++a)
+            if (op->dom_lo[a] != e->dom_lo[a] || op->n[a] != e->n[a])
+                fail(PCB_EINVAL, "update_samples: operator domain differs from the probes'");
+        if (op->info.rank_active != op->info.rank)
+            fail(PCB_EINVAL, "update_samples: the estimator needs the unsharded operator");
+        if (nchanged < 0 || (nchanged > 0 && !changed_ks)) fail(PCB_EINVAL, "bad changed list");
+        const int32_t r = op->info.rank;
+        std::set<int32_t> changed(changed_ks, changed_ks + nchanged);
+        for (int32_t k : changed)
+            if (k < 0 || k >= r) fail(PCB_EINVAL, "update_samples: bad changed id");
+        if (e->cached > r) fail(PCB_EINVAL, "update_samples: stale cache (rank shrank)");
+        for (int32_t k = e->cached; k < r; ++k)
+            if (!changed.count(k)) fail(PCB_EINVAL, "update_samples: uncached sample point not marked changed");
+        e->cached = r;
+        run_batch(op, true, e->q, e->Z.p, e->Yt.p, e->stream);
+        e->have_yt = true;
+        std::vector<double> h;
+        est_sums(e, 0, nullptr, nullptr, h);
+        double d2 = 0.0;
+        for (int i = 0; i < e->q; ++i) d2 += h[i];
+        e->eta_abs = std::sqrt(d2 / e->q);
+        e->eta_rel = e->y_norm > 0.0 ? std::sqrt(d2) / e->y_norm : 0.0;
+        if (eta_abs) *eta_abs = e->eta_abs;
+        if (eta_rel) *eta_rel = e->eta_rel;
+    });
+}
+
+PCB_API pcb_status pcb_estimator_cells(pcb_estimator* e, int32_t nleaf, const int64_t* leaf_lo, const int64_t* leaf_hi,
+                                       double* eta_cells) {
+    return est_guarded(e, [&] {
+        if (!e->have_yt) fail(PCB_EINVAL, "eta_for_cells: update_samples has not run");
+        if (nleaf < 0 || (nleaf > 0 && (!leaf_lo || !leaf_hi || !eta_cells))) fail(PCB_EINVAL, "bad leaf arguments");
+        std::vector<double> h;
+        est_sums(e, nleaf, leaf_lo, leaf_hi, h);
+        for (int32_t c = 0; c < nleaf; ++c) {
+            double s = 0.0;
+            for (int i = 0; i < e->q; ++i) s += h[(size_t)c * e->q + i];
+            eta_cells[c] = std::sqrt(s / e->q);
+        }
+    });
+}
+
+PCB_API pcb_status pcb_estimator_read(pcb_estimator* e, double* Z, double* Y, double* Ytilde) {
+    return est_guarded(e, [&] {
+        const size_t b = (size_t)e->q * e->N * 8;
+        if (Z) PCB_CK(cudaMemcpyAsync(Z, e->Z.p, b, cudaMemcpyDeviceToHost, e->stream));
+        if (Y) PCB_CK(cudaMemcpyAsync(Y, e->Y.p, b, cudaMemcpyDeviceToHost, e->stream));
+        if (Ytilde) PCB_CK(cudaMemcpyAsync(Ytilde, e->Yt.p, b, cudaMemcpyDeviceToHost, e->stream));
+        PCB_CK(cudaStreamSynchronize(e->stream));
     });
 }
 

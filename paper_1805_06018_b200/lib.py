@@ -28,7 +28,9 @@ EXPORTS = ["pcb_default_options", "pcb_last_error", "pcb_create", "pcb_destroy",
            "pcb_apply_adjoint_batch", "pcb_apply_batch_dev", "pcb_apply_adjoint_batch_dev", "pcb_entries",
            "pcb_blocks", "pcb_blocks_dev", "pcb_probe_estimate", "pcb_probe_estimate_dev", "pcb_launch_count",
            "pcb_normal_fill", "pcb_uniform_int_fill", "pcb_profile_begin", "pcb_profile_end", "pcb_apply_block",
-           "pcb_blur_create", "pcb_blur_destroy", "pcb_blur_apply", "pcb_blur_last_error"]
+           "pcb_blur_create", "pcb_blur_destroy", "pcb_blur_apply", "pcb_blur_last_error",
+           "pcb_estimator_create", "pcb_estimator_destroy", "pcb_estimator_probes", "pcb_estimator_set_y",
+           "pcb_estimator_set_y_blur", "pcb_estimator_update", "pcb_estimator_cells", "pcb_estimator_read"]
 
 
 class Options(ctypes.Structure):
@@ -98,6 +100,14 @@ def load():
     L.pcb_blur_destroy.argtypes = [vp]
     L.pcb_blur_apply.argtypes = [vp, i32, vp, vp, i32, i32, vp]
     L.pcb_blur_last_error.restype = ctypes.c_char_p
+    L.pcb_estimator_create.argtypes = [i32, P_i64, P_i64, i32, ctypes.c_uint64, i32, ctypes.POINTER(vp)]
+    L.pcb_estimator_destroy.argtypes = [vp]
+    L.pcb_estimator_probes.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)]
+    L.pcb_estimator_set_y.argtypes = [vp, vp, i32]
+    L.pcb_estimator_set_y_blur.argtypes = [vp, vp]
+    L.pcb_estimator_update.argtypes = [vp, vp, i32, vp, P_dbl, P_dbl]
+    L.pcb_estimator_cells.argtypes = [vp, i32, vp, vp, vp]
+    L.pcb_estimator_read.argtypes = [vp, vp, vp, vp]
     for n in EXPORTS:
         if n not in ("pcb_default_options", "pcb_last_error", "pcb_launch_count", "pcb_blur_last_error"):
             getattr(L, n).restype = ctypes.c_int
