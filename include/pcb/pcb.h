@@ -186,6 +186,62 @@ PCB_API pcb_status pcb_estimator_cells(pcb_estimator* est, int32_t nleaf, const 
                                        const int64_t* leaf_hi, double* eta_cells);
 PCB_API pcb_status pcb_estimator_read(pcb_estimator* est, double* Z, double* Y, double* Ytilde);
 
+/* Domain of an operator (inclusive box, dim entries each). */
+PCB_API pcb_status pcb_get_domain(const pcb_op* op, int64_t* dom_lo, int64_t* dom_hi);
+
+/* H-matrix assembly over the GPU operator and the PCHM container (reference
+ * hmatrix.hpp:13-103, hmatrix.cpp):
+ *   pcb_cluster_tree        ClusterTree::build (hmatrix.cpp:40-76) alone (no blocks)
+ *   pcb_hmatrix_assemble    assemble_hmatrix (:338-377): tree, admissible partition, dense leaves
+ *                           from batched GPU entries, low-rank blocks by the randomized range
+ *                           finder over batched GPU apply_block (:152-234) or by adaptive cross
+ *                           approximation over batched GPU entries (:236-318)
+ *   pcb_hmatrix_compress    compress_block (:320-336) for listed (t, s) node pairs, appended as
+ *                           low-rank blocks
+ *   pcb_hmatrix_matvec      HMatrix::matvec (:379-400), host
+ *   pcb_hmatrix_save/_load  the little-endian "PCHM" v1 container, byte-compatible with the
+ *                           reference's save_hmatrix / load_hmatrix (:433-526)
+ *   pcb_hmatrix_tree / _block / _admissible / _get_info   inspection */
+typedef struct pcb_hmatrix pcb_hmatrix;
+typedef enum pcb_hm_method { PCB_HM_RANDOMIZED = 0, PCB_HM_CUR = 1 } pcb_hm_method;
+typedef struct pcb_hmatrix_info {
+    int32_t dim;
+    int32_t leaf_cap;
+    int64_t n_points;
+    int64_t n_nodes;
+    int64_t n_blocks;
+    int64_t n_low_rank;
+    int64_t n_dense;
+    int64_t max_rank;
+    int64_t stored_doubles;
+    int32_t any_rank_capped;
+    int32_t method;
+    double tol;
+    int32_t fixed_rank;
+    int32_t reserved;
+} pcb_hmatrix_info;
+PCB_API pcb_status pcb_cluster_tree(int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t leaf_cap,
+                                    pcb_hmatrix** out);
+PCB_API pcb_status pcb_hmatrix_assemble(pcb_op* op, double tol, int32_t leaf_cap, int32_t method, int32_t fixed_rank,
+                                        pcb_hmatrix** out);
+PCB_API pcb_status pcb_hmatrix_compress(pcb_op* op, pcb_hmatrix* h, int32_t nblk, const int32_t* t_nodes,
+                                        const int32_t* s_nodes, int32_t method, double tol, int32_t fixed_rank);
+PCB_API pcb_status pcb_hmatrix_destroy(pcb_hmatrix* h);
+PCB_API pcb_status pcb_hmatrix_get_info(pcb_hmatrix* h, pcb_hmatrix_info* info);
+/* perm (N), node_range (2 per node: begin, end), node_links (3 per node: split_axis, child_lo,
+ * child_hi), node_bbox (2*dim per node: lo..., hi...); any may be NULL */
+PCB_API pcb_status pcb_hmatrix_tree(pcb_hmatrix* h, int64_t* perm, int64_t* node_range, int32_t* node_links,
+                                    int64_t* node_bbox);
+/* block i: t_s_kind = {t_node, s_node, 0 low rank | 1 dense}, rows_cols_rank = {|T|, |S|, rank};
+ * B (|T| x rank), C (rank x |S|) or dense (|T| x |S|), row-major; any may be NULL */
+PCB_API pcb_status pcb_hmatrix_block(pcb_hmatrix* h, int64_t i, int32_t* t_s_kind, int64_t* rows_cols_rank, double* B,
+                                     double* C, double* dense);
+PCB_API pcb_status pcb_hmatrix_admissible(pcb_hmatrix* h, int32_t t, int32_t s, int32_t* adm, double* dist,
+                                          double* diam_t, double* diam_s);
+PCB_API pcb_status pcb_hmatrix_matvec(pcb_hmatrix* h, const double* f, double* g);
+PCB_API pcb_status pcb_hmatrix_save(pcb_hmatrix* h, const char* path);
+PCB_API pcb_status pcb_hmatrix_load(const char* path, pcb_hmatrix** out);
+
 /* Number of kernels this library has launched in the process (all handles). */
 PCB_API long long pcb_launch_count(void);
 

@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-diag-suppress", "177,128",
           "-Xcompiler", "-fPIC,-fvisibility=hidden", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
-SOURCES = ["kernels_rows.cu", "kernels_cols.cu", "kernels_mid.cu", "kernels_misc.cu", "blur.cu", "pcop_b200.cpp"]
+SOURCES = ["kernels_rows.cu", "kernels_cols.cu", "kernels_mid.cu", "kernels_misc.cu", "blur.cu", "hmatrix.cpp", "pcop_b200.cpp"]
 HEADERS = ["fft.cuh", "kernels.cuh", "kernels_impl.cuh"]
 
 

@@ -161,6 +161,9 @@ std::atomic<long long> g_launches{0};
 }  // namespace
 }  // namespace pcb
 
+// shared with the other host translation units (hmatrix.cpp): pcb_last_error() reports it
+void pcb_detail_set_error(const std::string& m) { pcb::g_err = m; }
+
 struct pcb_op {
     std::mutex mu;
     int device = 0;
@@ -1081,6 +1084,19 @@ PCB_API pcb_status pcb_destroy(pcb_op* op) {
     return PCB_OK;
 }
 
+PCB_API pcb_status pcb_get_domain(const pcb_op* op, int64_t* dom_lo, int64_t* dom_hi) {
+    if (!op || !dom_lo || !dom_hi) {
+        set_err("null argument");
+        return PCB_EINVAL;
+    }
+    const int off = op->D - op->dim_user;
+    for (int a = 0; a < op->dim_user; ++a) {
+        dom_lo[a] = op->dom_lo[a + off];
+        dom_hi[a] = op->dom_lo[a + off] + op->n[a + off] - 1;
+    }
+    return PCB_OK;
+}
+
 PCB_API pcb_status pcb_get_info(const pcb_op* op, pcb_info* info) {
     if (!op || !info) {
         set_err("pcb_get_info: null argument");
@@ -1455,7 +1471,8 @@ PCB_API pcb_status pcb_probe_estimate_dev(pcb_op* op, int32_t q, const double* d
 struct pcb_estimator {
     std::mutex mu;
     int device = 0;
-    int D = 0;
+    int D = 0;         // internal dims (1-D is lifted to 2-D with a unit leading axis, as pcb_op)
+    int dim_user = 0;
     int64_t dom_lo[3] = {0, 0, 0};
     int32_t n[3] = {1, 1, 1};
     int64_t N = 0;
@@ -1476,9 +1493,11 @@ namespace {
 // sum over boxes (domain-relative, inclusive) of ||Yt - Y||^2 per probe, plus the whole domain
 void est_sums(pcb_estimator* e, int32_t nleaf, const int64_t* leaf_lo, const int64_t* leaf_hi, std::vector<double>& h) {
     std::vector<int64_t> lo, hi;
+    const int off = e->D - e->dim_user;
     for (int32_t c = 0; c < nleaf; ++c)
         for (int a = 0; a < e->D; ++a) {
-            const int64_t l = leaf_lo[c * e->D + a] - e->dom_lo[a], u = leaf_hi[c * e->D + a] - e->dom_lo[a];
+            const int64_t l = a < off ? 0 : leaf_lo[c * e->dim_user + a - off] - e->dom_lo[a];
+            const int64_t u = a < off ? 0 : leaf_hi[c * e->dim_user + a - off] - e->dom_lo[a];
             if (l < 0 || u >= e->n[a] || l > u) fail(PCB_EINVAL, "eta_for_cells: leaf box outside the domain");
             lo.push_back(l);
             hi.push_back(u);
@@ -1546,13 +1565,15 @@ PCB_API pcb_status pcb_estimator_create(int32_t dim, const int64_t* dom_lo, cons
         e->device = device;
         PCB_CK(cudaSetDevice(device));
         PCB_CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
-        e->D = dim;
+        e->dim_user = dim;
+        e->D = dim == 1 ? 2 : dim;
+        const int off = e->D - dim;
         e->N = 1;
         for (int a = 0; a < dim; ++a) {
             if (dom_hi[a] < dom_lo[a]) fail(PCB_EINVAL, "empty domain");
-            e->dom_lo[a] = dom_lo[a];
-            e->n[a] = (int32_t)(dom_hi[a] - dom_lo[a] + 1);
-            e->N *= e->n[a];
+            e->dom_lo[a + off] = dom_lo[a];
+            e->n[a + off] = (int32_t)(dom_hi[a] - dom_lo[a] + 1);
+            e->N *= e->n[a + off];
         }
         e->q = q;
         const size_t cnt = (size_t)q * e->N;

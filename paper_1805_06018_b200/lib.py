@@ -30,7 +30,10 @@ EXPORTS = ["pcb_default_options", "pcb_last_error", "pcb_create", "pcb_destroy",
            "pcb_normal_fill", "pcb_uniform_int_fill", "pcb_profile_begin", "pcb_profile_end", "pcb_apply_block",
            "pcb_blur_create", "pcb_blur_destroy", "pcb_blur_apply", "pcb_blur_last_error",
            "pcb_estimator_create", "pcb_estimator_destroy", "pcb_estimator_probes", "pcb_estimator_set_y",
-           "pcb_estimator_set_y_blur", "pcb_estimator_update", "pcb_estimator_cells", "pcb_estimator_read"]
+           "pcb_estimator_set_y_blur", "pcb_estimator_update", "pcb_estimator_cells", "pcb_estimator_read",
+           "pcb_get_domain", "pcb_cluster_tree", "pcb_hmatrix_assemble", "pcb_hmatrix_compress",
+           "pcb_hmatrix_destroy", "pcb_hmatrix_get_info", "pcb_hmatrix_tree", "pcb_hmatrix_block",
+           "pcb_hmatrix_admissible", "pcb_hmatrix_matvec", "pcb_hmatrix_save", "pcb_hmatrix_load"]
 
 
 class Options(ctypes.Structure):
@@ -53,6 +56,15 @@ class Info(ctypes.Structure):
                 "launches_per_batch": self.launches_per_batch,
                 "kernel_bytes": dict(zip(KERNEL_FAMILIES, list(self.kernel_bytes))),
                 "kernel_flops": dict(zip(KERNEL_FAMILIES, list(self.kernel_flops)))}
+
+
+class HMatrixInfo(ctypes.Structure):
+    _fields_ = [("dim", i32), ("leaf_cap", i32), ("n_points", i64), ("n_nodes", i64), ("n_blocks", i64),
+                ("n_low_rank", i64), ("n_dense", i64), ("max_rank", i64), ("stored_doubles", i64),
+                ("any_rank_capped", i32), ("method", i32), ("tol", dbl), ("fixed_rank", i32), ("reserved", i32)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
 
 
 class PcbError(RuntimeError):
@@ -108,6 +120,18 @@ def load():
     L.pcb_estimator_update.argtypes = [vp, vp, i32, vp, P_dbl, P_dbl]
     L.pcb_estimator_cells.argtypes = [vp, i32, vp, vp, vp]
     L.pcb_estimator_read.argtypes = [vp, vp, vp, vp]
+    L.pcb_get_domain.argtypes = [vp, P_i64, P_i64]
+    L.pcb_cluster_tree.argtypes = [i32, P_i64, P_i64, i32, ctypes.POINTER(vp)]
+    L.pcb_hmatrix_assemble.argtypes = [vp, dbl, i32, i32, i32, ctypes.POINTER(vp)]
+    L.pcb_hmatrix_compress.argtypes = [vp, vp, i32, vp, vp, i32, dbl, i32]
+    L.pcb_hmatrix_destroy.argtypes = [vp]
+    L.pcb_hmatrix_get_info.argtypes = [vp, ctypes.POINTER(HMatrixInfo)]
+    L.pcb_hmatrix_tree.argtypes = [vp, vp, vp, vp, vp]
+    L.pcb_hmatrix_block.argtypes = [vp, i64, vp, vp, vp, vp, vp]
+    L.pcb_hmatrix_admissible.argtypes = [vp, i32, i32, vp, vp, vp, vp]
+    L.pcb_hmatrix_matvec.argtypes = [vp, vp, vp]
+    L.pcb_hmatrix_save.argtypes = [vp, ctypes.c_char_p]
+    L.pcb_hmatrix_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
     for n in EXPORTS:
         if n not in ("pcb_default_options", "pcb_last_error", "pcb_launch_count", "pcb_blur_last_error"):
             getattr(L, n).restype = ctypes.c_int

@@ -101,3 +101,17 @@ def test_y_from_true_operator_c3(gpu):
     Z, Y, _ = est.read()
     H = A.apply_adjoint(Z.reshape(2, 1024, 1024)).reshape(2, -1)
     assert np.array_equal(Y, H)
+
+
+def test_one_dimensional_domain(gpu):
+    inp = inputs.small_lattice(n=50, dim=1, m=5, sigma=2.0)
+    op = ProductConvolutionOperator.from_inputs(inp)
+    est = Estimator((inp.dom_lo, inp.dom_hi), q=3, seed=4)
+    Z, _, _ = est.read()
+    Y = Z * 0.5
+    est.set_y(Y)
+    ea, er = est.update(op, range(op.rank))
+    leaves = [((0,), (24,)), ((25,), (49,))]
+    yt, cells, ea2, er2 = op.probe_estimate(Z, Y, leaves, want_ytilde=True)
+    assert abs(ea - ea2) <= 1e-13 * ea2 and abs(er - er2) <= 1e-13 * er2
+    assert np.allclose(est.cells(leaves), cells, rtol=1e-13, atol=0)
