@@ -1142,15 +1142,37 @@ static pcb_status apply_host_common(pcb_op* op, bool adjoint, int32_t B, const d
         const size_t cnt = (size_t)B * (size_t)op->N;
         op->st_in.ensure(cnt);
         op->st_out.ensure(cnt);
-        // sub-batches overlap H2D(j+1) and D2H(j-1) with the kernels of sub-batch j
-        const int nsub = B >= 8 ? 4 : (B >= 2 ? 2 : 1);
+        // Sub-batches overlap H2D(j+1) and D2H(j-1) with the kernels of sub-batch j (PCIe is full duplex,
+        // ~55 GB/s per direction).  ~sub_mb MiB each; the first and the last are half size so the
+        // unoverlapped fill (first H2D) and drain (last D2H) stay short.
+        static const double sub_mb = [] {
+            const char* e = std::getenv("PCB_SUB_MB");
+            return e ? std::max(1.0, std::atof(e)) : 64.0;
+        }();
+        const double vec_mb = (double)op->N * 8.0 / (1 << 20);
+        const int per = (int)std::max(1.0, std::floor(sub_mb / vec_mb));
+        std::vector<int> sizes;
+        if (B <= per) {
+            sizes.push_back(B);
+        } else {
+            const int edge = std::max(1, per / 2);
+            int left = B - 2 * edge;
+            sizes.push_back(edge);
+            while (left > 0) {
+                const int c = std::min(per, left);
+                sizes.push_back(c);
+                left -= c;
+            }
+            sizes.push_back(edge);
+        }
         if (!op->s_h2d) {
             PCB_CK(cudaStreamCreateWithFlags(&op->s_h2d, cudaStreamNonBlocking));
             PCB_CK(cudaStreamCreateWithFlags(&op->s_d2h, cudaStreamNonBlocking));
             for (int j = 0; j < 8; ++j) PCB_CK(cudaEventCreateWithFlags(&op->ev_io[j], cudaEventDisableTiming));
         }
-        for (int j = 0; j < nsub; ++j) {
-            const int b0 = (int)((int64_t)B * j / nsub), b1 = (int)((int64_t)B * (j + 1) / nsub);
+        int b0 = 0;
+        for (size_t j = 0; j < sizes.size(); ++j) {
+            const int b1 = b0 + sizes[j];
             const size_t off = (size_t)b0 * op->N, n = (size_t)(b1 - b0) * op->N;
             PCB_CK(cudaMemcpyAsync(op->st_in.p + off, F + off, n * sizeof(double), cudaMemcpyHostToDevice, op->s_h2d));
             PCB_CK(cudaEventRecord(op->ev_io[2 * (j & 1)], op->s_h2d));
@@ -1159,6 +1181,7 @@ static pcb_status apply_host_common(pcb_op* op, bool adjoint, int32_t B, const d
             PCB_CK(cudaEventRecord(op->ev_io[2 * (j & 1) + 1], op->stream));
             PCB_CK(cudaStreamWaitEvent(op->s_d2h, op->ev_io[2 * (j & 1) + 1], 0));
             PCB_CK(cudaMemcpyAsync(G + off, op->st_out.p + off, n * sizeof(double), cudaMemcpyDeviceToHost, op->s_d2h));
+            b0 = b1;
         }
         PCB_CK(cudaStreamSynchronize(op->s_d2h));
         PCB_CK(cudaStreamSynchronize(op->stream));
