@@ -21,6 +21,13 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-diag-suppress", "177,128",
           "-Xcompiler", "-fPIC,-fvisibility=hidden", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
+EXTRA = os.environ.get("PCB_NVCC_EXTRA", "").split()  # experiments
+# elements per thread of the power-of-two FFT engines, per kernel family (fft.cuh PCB_E2)
+E_ROWS = os.environ.get("PCB_E_ROWS", "8")
+E_COLS = os.environ.get("PCB_E_COLS", "16")
+E_MID = os.environ.get("PCB_E_MID", "8")
+PER_SOURCE = {"kernels_rows.cu": [f"-DPCB_E2={E_ROWS}"], "kernels_cols.cu": [f"-DPCB_E2={E_COLS}"],
+              "kernels_mid.cu": [f"-DPCB_E2={E_MID}"]}
 SOURCES = ["kernels_rows.cu", "kernels_cols.cu", "kernels_mid.cu", "kernels_misc.cu", "blur.cu", "hmatrix.cpp", "pcop_b200.cpp"]
 HEADERS = ["fft.cuh", "kernels.cuh", "kernels_impl.cuh"]
 
@@ -36,7 +43,7 @@ def _compile(src: str, verbose: bool) -> str:
     if os.path.exists(obj) and os.path.getmtime(obj) >= _newest(deps):
         return obj
     lang = [] if src.endswith(".cu") else ["-x", "cu"]
-    cmd = [NVCC] + ARCH + COMMON + lang + ["-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [NVCC] + ARCH + COMMON + EXTRA + PER_SOURCE.get(src, []) + lang + ["-c", os.path.join(CSRC, src), "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

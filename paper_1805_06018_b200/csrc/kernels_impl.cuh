@@ -18,8 +18,24 @@
 #include "fft.cuh"
 #include "kernels.cuh"
 
+// Launch shape of the last-axis passes (measured on B200, round 1): small CTAs of ~64 threads
+// with 8 elements per thread and a 64-register cap (16 CTAs/SM) for the power-of-two lengths
+// beat 128-thread / 16-element CTAs by 1.35x at c3; the 3-smooth (E = 24) lengths keep their
+// registers.
+#ifndef PCB_ROWS_THREADS
+#define PCB_ROWS_THREADS 64
+#endif
 #ifndef PCB_ROWS_MINB
-#define PCB_ROWS_MINB 1
+#define PCB_ROWS_MINB 16
+#endif
+#ifndef PCB_ROWS_MINB_MIXED
+#define PCB_ROWS_MINB_MIXED 1
+#endif
+#ifndef PCB_COLS_THREADS
+#define PCB_COLS_THREADS 128
+#endif
+#ifndef PCB_COLS_MINB
+#define PCB_COLS_MINB 1
 #endif
 
 namespace pcb {
@@ -78,7 +94,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // w_k . f on the footprint window, ADJ gathers g on the output window (both
 // staged through shared memory with cp.async), SPEC places the trimmed kernel.
 template <int N, int NL, int MODE>
-__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, PCB_ROWS_MINB) k_rows_fwd(PassArgs a) {
+__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_MINB : PCB_ROWS_MINB_MIXED) k_rows_fwd(PassArgs a) {
     constexpr int R = FftCfg<N>::R;
     constexpr int RF = FirstPos<N>::RF;
     constexpr int NT = NL * FftCfg<N>::TPL;
@@ -278,7 +294,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P1>::TPL) k_mid(PassArgs a) {
 // ---------------------------------------------------------------------------
 // cols: axis-0 pass with the frequency-domain product (K3).
 template <int P0, int NL, int MODE>
-__global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
+__global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(PassArgs a) {
     constexpr int R = FftCfg<P0>::R;
     constexpr int RF = FirstPos<P0>::RF;
     constexpr int RL = LastPos<P0>::RL;
@@ -423,7 +439,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL) k_cols(PassArgs a) {
 // output positions p = t mod blockDim, so contributions to one position are
 // added by one thread in ascending entry order (deterministic, no atomics).
 template <int N, int NL, int MODE>
-__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, PCB_ROWS_MINB) k_rows_inv(PassArgs a) {
+__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_MINB : PCB_ROWS_MINB_MIXED) k_rows_inv(PassArgs a) {
     constexpr int R = FftCfg<N>::R;
     constexpr int RL = LastPos<N>::RL;
     constexpr int NT = NL * FftCfg<N>::TPL;
@@ -524,13 +540,13 @@ cudaError_t launch_dyn(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_
 }
 
 template <int LEN>
-constexpr int rows_nl() {  // lines per CTA for the last-axis passes: ~128 threads
-    constexpr int t = 128 / FftCfg<LEN>::TPL;
+constexpr int rows_nl() {  // lines per CTA for the last-axis passes: ~PCB_ROWS_THREADS threads
+    constexpr int t = PCB_ROWS_THREADS / FftCfg<LEN>::TPL;
     return t < 1 ? 1 : (t > 32 ? 32 : t);
 }
 template <int P>
 constexpr int cols_nl() {  // column-tile width of the axis-0 / axis-1 passes (>= 2: 32-B runs)
-    constexpr int t = 128 / FftCfg<P>::TPL;
+    constexpr int t = PCB_COLS_THREADS / FftCfg<P>::TPL;
     return t < 2 ? 2 : (t > 32 ? 32 : t);
 }
 

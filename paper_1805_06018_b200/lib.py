@@ -9,7 +9,7 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libpcop_b200.so")
+LIB_PATH = os.environ.get("PCB_LIB_PATH") or os.path.join(PKG, "lib", "libpcop_b200.so")  # PCB_LIB_PATH: A/B builds
 
 i32 = ctypes.c_int32
 i64 = ctypes.c_int64
