@@ -26,12 +26,15 @@
 #ifndef PCB_E2
 #define PCB_E2 16  // elements per thread of the power-of-two engines (set per translation unit)
 #endif
+#ifndef PCB_E3
+#define PCB_E3 24  // elements per thread of the 3-smooth engines (12 or 24)
+#endif
 #define PCB_NS_CAT2(a, b) a##b
 #define PCB_NS_CAT(a, b) PCB_NS_CAT2(a, b)
 
 namespace pcb {
 // the engine is instantiated per element count: distinct names per translation unit setting
-inline namespace PCB_NS_CAT(e, PCB_E2) {
+inline namespace PCB_NS_CAT(PCB_NS_CAT(e, PCB_E2), PCB_NS_CAT(_, PCB_E3)) {
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -166,13 +169,15 @@ template <int L>
 struct FftCfg {
     static_assert(fft_len_ok(L) && L <= 4096, "unsupported FFT line length");
     static constexpr bool P2 = is_pow2c(L);
-    static constexpr int R = P2 ? (L >= PCB_E2 ? PCB_E2 : L) : 24;  // elements per thread (= last radix)
+    static constexpr int R = P2 ? (L >= PCB_E2 ? PCB_E2 : L) : (L % PCB_E3 == 0 ? PCB_E3 : 24);  // elements per thread (= last radix)
     static constexpr int TPL = L / R;                        // threads per line
     // forward stage radices: the prefix factors L/R, then R
     static constexpr int pref_radix(int rest) {
-        // a stage radix never exceeds the elements a thread holds (R)
-        return rest % 16 == 0 && P2 && R >= 16 ? 16 : rest % 12 == 0 && !P2 ? 12 : rest % 8 == 0 && R >= 8 ? 8
-               : rest % 6 == 0 && !P2 ? 6 : rest % 4 == 0 && R >= 4 ? 4 : rest % 3 == 0 ? 3 : rest % 2 == 0 ? 2 : 1;
+        // the largest supported radix dividing both the remaining length and R (a stage never
+        // exceeds, and always tiles, the elements a thread holds)
+        return rest % 16 == 0 && R % 16 == 0 ? 16 : rest % 12 == 0 && R % 12 == 0 ? 12 : rest % 8 == 0 && R % 8 == 0 ? 8
+               : rest % 6 == 0 && R % 6 == 0 ? 6 : rest % 4 == 0 && R % 4 == 0 ? 4 : rest % 3 == 0 && R % 3 == 0 ? 3
+               : rest % 2 == 0 ? 2 : 1;
     }
     static constexpr int nstages() {
         int n = 1, rest = L / R;

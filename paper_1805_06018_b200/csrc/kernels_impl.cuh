@@ -32,7 +32,7 @@
 #define PCB_ROWS_MINB_MIXED 1
 #endif
 #ifndef PCB_COLS_THREADS
-#define PCB_COLS_THREADS 128
+#define PCB_COLS_THREADS 64
 #endif
 #ifndef PCB_COLS_MINB
 #define PCB_COLS_MINB 1
