@@ -46,6 +46,19 @@ struct GatherEntry {
     double scale;     // 1 / prod P of the entry's term (its group's FFT size)
 };
 
+// LOCAL apply gather, frequency-domain bundles: the T lines of one output line whose shifted
+// supports fit in one P-periodic window are summed as spectra, each multiplied by its scale and
+// the phase exp(-2 pi i k delta / P) of its shift delta relative to the bundle origin, and
+// transformed once.  The bundle header is a GatherEntry {lo, hi: union output range; sh: origin;
+// pad_: member count; t_off: first member}; members carry the per-line data.
+struct BundleMember {
+    int64_t t_off;    // double2 offset of the T line for vector 0
+    int64_t t_vst;    // ... plus t_vst per vector
+    double scale;     // 1 / prod P
+    int32_t delta;    // shift relative to the bundle origin, 0 <= delta < P
+    int32_t pad_;
+};
+
 // Everything one pipeline pass needs.  D in {2, 3}: axes 0..D-1, last axis is
 // the R2C/C2R axis (contiguous in memory, reference layout "last axis
 // fastest", grid_function.hpp:11-13).
@@ -79,16 +92,18 @@ struct PassArgs {
     const int64_t* line_id;       // output line of each active line
     const int32_t* line_rng;      // [2*i], [2*i+1]: union of the entries' last-axis ranges
     const GatherEntry* entries;
+    const BundleMember* members;  // RI_APPLY_B: bundle members (entries are bundle headers)
     double scale;          // 1 / prod P
 };
 
 enum RowsFwdMode { RF_APPLY = 0, RF_ADJ = 1, RF_SPEC = 2 };
 enum ColsMode { CM_SPEC = 0, CM_APPLY_LOCAL = 1, CM_APPLY_GLOBAL = 2, CM_ADJ_LOCAL = 3, CM_ADJ_GLOBAL = 4 };
 enum MidMode { MM_FWD_APPLY = 0, MM_FWD_ADJ = 1, MM_FWD_SPEC = 2, MM_INV_APPLY = 3, MM_INV_ADJ = 4 };
-enum RowsInvMode { RI_APPLY = 0, RI_ADJ = 1 };
+enum RowsInvMode { RI_APPLY = 0, RI_ADJ = 1, RI_APPLY_B = 2 };
 
 // launchers (kernels.cu); return cudaGetLastError()
 cudaError_t launch_rows_fwd(const PassArgs& a, int mode, cudaStream_t st);
+int rows_lanes(int P_last);  // lines (rows_fwd) / gather lanes (rows_inv) per CTA for a last-axis length
 cudaError_t launch_mid(const PassArgs& a, int mode, cudaStream_t st);
 cudaError_t launch_cols(const PassArgs& a, int mode, cudaStream_t st);
 cudaError_t launch_rows_inv(const PassArgs& a, int mode, int64_t n_lines, cudaStream_t st);

@@ -28,6 +28,12 @@
 #ifndef PCB_ROWS_MINB
 #define PCB_ROWS_MINB 16
 #endif
+#ifndef PCB_ROWS_MINB_B
+#define PCB_ROWS_MINB_B 8
+#endif
+#ifndef PCB_BUNDLE_MB
+#define PCB_BUNDLE_MB 2  // bundle members staged per lane at a time
+#endif
 #ifndef PCB_ROWS_MINB_MIXED
 #define PCB_ROWS_MINB_MIXED 1
 #endif
@@ -519,6 +525,117 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
                 const double* w = a.w_pool + meta[ll].w_off;
                 for (; p < hi; p += NT) acc[p - ulo] += w[p] * (x[p] * sc);
             }
+        }
+    }
+    __syncthreads();
+    double* g = a.out + (int64_t)vec * a.N + line * a.n[ax];
+    for (int i = ulo + threadIdx.x; i < uhi; i += NT) g[i] = a.accumulate ? g[i] + acc[i - ulo] : acc[i - ulo];
+}
+
+// ---------------------------------------------------------------------------
+// rows_inv, LOCAL apply, frequency-domain bundles (BundleMember).  Lane l of the CTA owns one
+// bundle of the batch.  Members are staged MB at a time per lane with cp.async (MB * NL lines in
+// flight per CTA), summed into the lane's half spectrum in registers -- scale * T[k] *
+// exp(-2 pi i k delta / P) -- then one C2R per bundle and one add of its range into the output
+// line.  Members are summed in CSR order, bundles in CSR order: deterministic.
+template <int N, int NL>
+__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_MINB_B : PCB_ROWS_MINB_MIXED)
+    k_rows_inv_b(PassArgs a) {
+    constexpr int R = FftCfg<N>::R;
+    constexpr int RL = LastPos<N>::RL;
+    constexpr int NT = NL * FftCfg<N>::TPL;
+    constexpr int TPL = FftCfg<N>::TPL;
+    constexpr int XS = 2 * N + 1;
+    constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
+                                                                          : (NL * (2 * N + 1) + 1) / 2;
+    constexpr int P = 2 * N;
+    constexpr int MB = PCB_BUNDLE_MB;
+    constexpr int SL = N + 1;  // staged line length
+    extern __shared__ double2 buf[];
+    const int64_t aline = blockIdx.x;
+    const int vec = blockIdx.y;
+    const int ax = a.D - 1;
+    const int64_t line = a.line_id[aline];
+    const int ulo = a.line_rng[2 * aline], uhi = a.line_rng[2 * aline + 1];
+    // layout: buf [BUFW] (FFT; reused as xs) | stage [NL][MB][N+1] | acc [n_last] | meta [NL]
+    double* xs = reinterpret_cast<double*>(buf);
+    double2* stg = buf + BUFW;
+    double* acc = reinterpret_cast<double*>(stg + NL * MB * SL);
+    GatherEntry* meta = reinterpret_cast<GatherEntry*>(acc + a.n[ax] + (a.n[ax] & 1));
+    const int64_t b_beg = a.line_ptr[aline];
+    const int64_t b_end = a.line_ptr[aline + 1];
+    const double2* twP = twtab<P>(a.tw);
+    const int l = threadIdx.x % NL;
+    const int tl = threadIdx.x / NL;
+    for (int i = ulo + threadIdx.x; i < uhi; i += NT) acc[i - ulo] = 0.0;
+
+    for (int64_t b0 = b_beg; b0 < b_end; b0 += NL) {
+        const int nb = (int)((b_end - b0) < NL ? (b_end - b0) : NL);
+        __syncthreads();  // previous batch finished with meta / xs
+        if (threadIdx.x < nb) meta[threadIdx.x] = a.entries[b0 + threadIdx.x];
+        __syncthreads();
+        int mmax = 0;
+        for (int ll = 0; ll < nb; ++ll) mmax = max(mmax, meta[ll].pad_);
+        const int cnt = l < nb ? meta[l].pad_ : 0;
+        const BundleMember* mb = a.members + (l < nb ? meta[l].t_off : 0);
+        double2 zk[R], zn[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) zk[r] = zn[r] = czero();
+        for (int m0 = 0; m0 < mmax; m0 += MB) {
+#pragma unroll
+            for (int j = 0; j < MB; ++j)
+                if (m0 + j < cnt) {
+                    const double2* src = a.T + mb[m0 + j].t_off + vec * mb[m0 + j].t_vst;
+                    double2* dst = stg + (l * MB + j) * SL;
+                    for (int i = tl; i < SL; i += TPL) cp_async16(&dst[i], src + i);
+                }
+            cp_async_wait_all();
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < MB; ++j)
+                if (m0 + j < cnt) {
+                    const double2* x = stg + (l * MB + j) * SL;
+                    const double sc = mb[m0 + j].scale;
+                    const int dl = mb[m0 + j].delta;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int k = tl + r * TPL;
+                        double2 xk = x[k], xn = x[N - k];
+                        if (dl != 0) {
+                            xk = cmul(xk, __ldg(&twP[(k * dl) % P]));
+                            xn = cmul(xn, __ldg(&twP[((N - k) * dl) % P]));
+                        }
+                        zk[r] = make_double2(fma(sc, xk.x, zk[r].x), fma(sc, xk.y, zk[r].y));
+                        zn[r] = make_double2(fma(sc, xn.x, zn[r].x), fma(sc, xn.y, zn[r].y));
+                    }
+                }
+            __syncthreads();  // stage slots free
+        }
+        double2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int k = tl + r * TPL;
+            const double2 E = make_double2(zk[r].x + zn[r].x, zk[r].y - zn[r].y);   // Z[k] + conj Z[N-k]
+            const double2 Dd = make_double2(zk[r].x - zn[r].x, zk[r].y + zn[r].y);  // Z[k] - conj Z[N-k]
+            const double2 O = cmulc(Dd, __ldg(&twP[k]));                            // * exp(+2 pi i k / P)
+            v[r] = make_double2(E.x - O.y, E.y + O.x);                              // E + i O
+        }
+        fft_rev_order<N, +1, NL, PSH<NL>>(v, buf, l, tl, twtab<N>(a.tw));
+        __syncthreads();
+#pragma unroll
+        for (int bb = 0; bb < R / RL; ++bb)
+#pragma unroll
+            for (int r = 0; r < RL; ++r) {
+                const int p = LastPos<N>::pos(tl, bb, r);
+                xs[l * XS + 2 * p] = v[bb * RL + r].x;
+                xs[l * XS + 2 * p + 1] = v[bb * RL + r].y;
+            }
+        __syncthreads();
+        for (int ll = 0; ll < nb; ++ll) {
+            const int lo = meta[ll].lo, hi = meta[ll].hi;
+            const double* x = xs + ll * XS - meta[ll].sh;
+            int p = lo + (int)((threadIdx.x + NT - (unsigned)(lo % NT)) % NT);
+            for (; p < hi; p += NT) acc[p - ulo] += x[p];
         }
     }
     __syncthreads();

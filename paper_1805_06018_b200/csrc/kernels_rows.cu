@@ -36,8 +36,28 @@ cudaError_t rows_inv_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
     return launch_dyn(k_rows_inv<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
 }
 
+template <int N>
+cudaError_t rows_inv_b_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
+    constexpr int NL = rows_nl<N>();
+    constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
+                                                                          : (NL * (2 * N + 1) + 1) / 2;
+    dim3 grid((unsigned)n_lines, (unsigned)a.B);
+    const size_t smem = sizeof(double2) * (BUFW + (size_t)NL * PCB_BUNDLE_MB * (N + 1)) +
+                        sizeof(double) * ((size_t)a.n[a.D - 1] + 1) + NL * sizeof(GatherEntry) + 16;
+    return launch_dyn(k_rows_inv_b<N, NL>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
+}
+
 template <int MODE>
 cudaError_t rows_inv_mode(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
+    if constexpr (MODE == RI_APPLY_B) {
+        switch (a.P[a.D - 1] / 2) {
+#define PCB_CASE(n) \
+    case n: return rows_inv_b_n<n>(a, n_lines, st);
+            PCB_ROW_SIZES(PCB_CASE)
+#undef PCB_CASE
+            default: return cudaErrorInvalidValue;
+        }
+    } else {
     switch (a.P[a.D - 1] / 2) {
 #define PCB_CASE(n) \
     case n: return rows_inv_n<n, MODE>(a, n_lines, st);
@@ -45,9 +65,20 @@ cudaError_t rows_inv_mode(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
 #undef PCB_CASE
         default: return cudaErrorInvalidValue;
     }
+    }
 }
 
 }  // namespace
+
+int rows_lanes(int P_last) {
+    switch (P_last / 2) {
+#define PCB_CASE(n) \
+    case n: return rows_nl<n>();
+        PCB_ROW_SIZES(PCB_CASE)
+#undef PCB_CASE
+        default: return 1;
+    }
+}
 
 cudaError_t launch_rows_fwd(const PassArgs& a, int mode, cudaStream_t st) {
     switch (mode) {
@@ -59,7 +90,12 @@ cudaError_t launch_rows_fwd(const PassArgs& a, int mode, cudaStream_t st) {
 }
 
 cudaError_t launch_rows_inv(const PassArgs& a, int mode, int64_t n_lines, cudaStream_t st) {
-    return mode == RI_APPLY ? rows_inv_mode<RI_APPLY>(a, n_lines, st) : rows_inv_mode<RI_ADJ>(a, n_lines, st);
+    switch (mode) {
+        case RI_APPLY: return rows_inv_mode<RI_APPLY>(a, n_lines, st);
+        case RI_ADJ: return rows_inv_mode<RI_ADJ>(a, n_lines, st);
+        case RI_APPLY_B: return rows_inv_mode<RI_APPLY_B>(a, n_lines, st);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace pcb

@@ -103,6 +103,7 @@ struct DevBuf {
 
 bool g_pow2_only = false;    // PCB_POW2=1: power-of-two FFT sizes only (A/B measurement)
 bool g_mixed_last = false;   // PCB_MIXED_LAST=1: 3-smooth sizes on the R2C axis too (default: pow2 there)
+bool g_bundle = true;        // PCB_BUNDLE=0: one C2R per gather entry in the LOCAL apply (A/B)
 
 // Smallest compiled FFT size >= max(v, 16): 2^a * {1, 3, 9}.  The last (R2C) axis also needs its
 // half length P/2 compiled for the row passes.
@@ -129,7 +130,9 @@ struct Csr {  // rows_inv gather list over the active output lines of one class
     int64_t n_lines = 0;
     DevBuf<int64_t> ptr, ids;
     DevBuf<int32_t> rng;
-    DevBuf<GatherEntry> en;
+    DevBuf<GatherEntry> en;      // entries, or bundle headers when bundled
+    DevBuf<BundleMember> mem;    // bundle members
+    bool bundled = false;
 };
 
 // Terms with the same full FFT shape: the axis-0 (cols) and axis-1 (mid) passes and the spectra.
@@ -336,6 +339,7 @@ void build_csr(pcb_op* op, Class& c, bool global, const std::vector<double>& ter
         e.hi = std::min(e.hi, op->n[ax]);
     };
     std::vector<std::vector<GatherEntry>> ap(n_lines), ad(n_lines);
+    std::vector<std::vector<int>> apk(n_lines);  // term of each apply entry (bundling)
     for (int k : c.terms) {
         const TermDesc& t = op->terms[k];
         const int64_t plane = D == 2 ? c.W : (int64_t)t.P1 * c.W;
@@ -360,6 +364,7 @@ void build_csr(pcb_op* op, Class& c, bool global, const std::vector<double>& ter
                     const int64_t y0 = t.s[0] + t.o_lo[0] + j0;
                     const int64_t y1 = D == 3 ? t.s[1] + t.o_lo[1] + j1 : 0;
                     ap[line_of(y0, y1)].push_back(e);
+                    apk[line_of(y0, y1)].push_back(k);
                 }
         }
     }
@@ -406,7 +411,81 @@ void build_csr(pcb_op* op, Class& c, bool global, const std::vector<double>& ter
         out.rng.upload(rg);
         out.en.upload(he);
     };
-    flatten(ap, c.apply);
+    // LOCAL apply: frequency-domain bundles (BundleMember) -- entries sorted by shift, greedily
+    // grouped while every member's shifted support [delta + o_lo, delta + o_lo + o_cnt) stays
+    // inside one period P of the class
+    auto flatten_b = [&](Csr& out) {
+        std::vector<int64_t> hp, ids;
+        std::vector<int32_t> rg;
+        std::vector<GatherEntry> he;
+        std::vector<BundleMember> hm;
+        for (int64_t ln = 0; ln < n_lines; ++ln) {
+            const std::vector<GatherEntry>& L = ap[ln];
+            if (L.empty()) continue;
+            std::vector<int> idx(L.size());
+            for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
+            std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return L[x].sh < L[y].sh; });
+            int ulo = INT32_MAX, uhi = INT32_MIN;
+            for (const GatherEntry& e : L) {
+                ulo = std::min(ulo, e.lo);
+                uhi = std::max(uhi, e.hi);
+            }
+            hp.push_back((int64_t)he.size());
+            ids.push_back(ln);
+            rg.push_back(ulo);
+            rg.push_back(std::max(ulo, uhi));
+            // members per bundle: at most ceil(entries / lanes), so a line's bundles still fill the
+            // CTA's lanes (3-D lines gather many same-shift entries)
+            const int lanes = std::max(1, rows_lanes(c.P_last));
+            const size_t maxm = std::max<size_t>(1, (L.size() + lanes - 1) / lanes);
+            size_t i = 0;
+            while (i < idx.size()) {
+                const int sh0 = L[idx[i]].sh;
+                GatherEntry h{};
+                h.sh = sh0;
+                h.lo = INT32_MAX;
+                h.hi = INT32_MIN;
+                h.t_off = (int64_t)hm.size();
+                h.w_off = -1;
+                size_t j = i;
+                while (j < idx.size()) {
+                    const GatherEntry& e = L[idx[j]];
+                    const TermDesc& t = op->terms[apk[ln][idx[j]]];
+                    // the whole support of the line's C2R (not only its in-domain part) must stay
+                    // inside the period, or the out-of-domain tail would wrap onto the window
+                    const int end = e.sh - sh0 + t.m[ax] + t.k_ext[ax] - 1;
+                    if (j > i && (end > c.P_last || j - i >= maxm)) break;
+                    if (e.lo < e.hi) {
+                        h.lo = std::min(h.lo, e.lo);
+                        h.hi = std::max(h.hi, e.hi);
+                    }
+                    hm.push_back(BundleMember{e.t_off, e.t_vst, e.scale, e.sh - sh0, 0});
+                    ++h.pad_;
+                    ++j;
+                }
+                if (h.lo > h.hi) h.lo = h.hi = std::max(0, std::min(sh0, op->n[ax]));
+                he.push_back(h);
+                i = j;
+            }
+        }
+        hp.push_back((int64_t)he.size());
+        out.n_lines = (int64_t)ids.size();
+        out.ptr.upload(hp);
+        if (ids.empty()) {
+            ids.push_back(0);
+            rg.push_back(0);
+            rg.push_back(0);
+        }
+        if (he.empty()) he.push_back(GatherEntry{});
+        if (hm.empty()) hm.push_back(BundleMember{});
+        out.ids.upload(ids);
+        out.rng.upload(rg);
+        out.en.upload(he);
+        out.mem.upload(hm);
+        out.bundled = true;
+    };
+    if (!global && g_bundle) flatten_b(c.apply);
+    else flatten(ap, c.apply);
     flatten(ad, c.adj);
 }
 
@@ -954,9 +1033,11 @@ void run_batch(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG
             a.line_id = csr.ids.p;
             a.line_rng = csr.rng.p;
             a.entries = csr.en.p;
+            a.members = csr.mem.p;
+            const int ri = adjoint ? RI_ADJ : (csr.bundled ? RI_APPLY_B : RI_APPLY);
             if (csr.n_lines > 0)
                 launch(op, st, adjoint ? "rows_inv(adjoint)" : "rows_inv(apply)",
-                       [&] { return launch_rows_inv(a, adjoint ? RI_ADJ : RI_APPLY, csr.n_lines, st); });
+                       [&] { return launch_rows_inv(a, ri, csr.n_lines, st); });
         }
     }
 }
@@ -1042,6 +1123,10 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
         // 24-element row kernels lose more to register pressure than they save (c3, c2: measured)
         g_mixed_last = dim == 3;
         if (const char* e = getenv("PCB_MIXED_LAST")) g_mixed_last = atoi(e) != 0;
+        // frequency-domain bundles pay in 2-D (c3 rows_inv 3.85 -> 3.36 ms); 3-D lines gather many
+        // short same-shift entries and the per-entry path is faster there (c4: measured)
+        g_bundle = dim == 2;
+        if (const char* e = getenv("PCB_BUNDLE")) g_bundle = atoi(e) != 0;
 
         PCB_CK(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
 
