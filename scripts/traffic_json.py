@@ -15,6 +15,7 @@ def run(csv_path, steps, out_path):
         base = name.split("<")[0].replace("unnamed>::k_", "").replace("k_", "").strip()
         mode = name.split(",")[-1].split(">")[0].strip() if "<" in name else ""
         f = base.split("(")[0]
+        f = "rows_inv" if f == "rows_inv_b" else f  # bundled gather is the rows_inv family
         if f.startswith("rows_fwd") and mode == "2" or f.startswith("cols") and mode == "0":
             continue  # spectra build (K1) launches
         fam[f] = fam.get(f, 0.0) + v["dram_bytes_per_step"]
