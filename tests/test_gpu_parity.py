@@ -352,3 +352,17 @@ def test_apply_block_properties(gpu, cfg):
     assert not far.any()
     with pytest.raises(ValueError, match="boxes must lie inside the domain"):
         op.apply_block(((0, 0), (n, 3)), ((0, 0), (3, 3)), np.ones((4, 4)))
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_bundled_gather_matches_per_entry_gather(gpu, name, monkeypatch):
+    """The frequency-domain bundles of the LOCAL apply gather (phase-shifted spectra summed, one
+    C2R per bundle) agree with the one-C2R-per-entry gather at full config size."""
+    inp = inputs.make_config(name)
+    F = normal_vectors(8, 2, inp.n_points)
+    monkeypatch.setenv("PCB_BUNDLE", "0")
+    a = ProductConvolutionOperator.from_inputs(inp, mode="local").apply_batch(F)
+    monkeypatch.setenv("PCB_BUNDLE", "1")
+    b = ProductConvolutionOperator.from_inputs(inp, mode="local").apply_batch(F)
+    for i in range(2):
+        assert rel(b[i], a[i]) <= 1e-14
