@@ -5,9 +5,10 @@ One "step" = one apply of the product-convolution operator to the configuration'
 vectors (c3: 64 vectors on 1024^2, r = 256).  Contract (README / task):
   * W >= 3 untimed warm-up steps, then K timed steps, each bracketed by CUDA events on the
     launching stream; L2 is flushed (a 256 MiB write) between timed steps, outside the events;
-  * multi-GPU: one process per GPU (torchrun); the batch is sharded across ranks by vector
-    (``--shard rhs``, no collective) or the terms are sharded (``--shard k``, one NCCL
-    all-reduce of the partial outputs inside the timed region); time = max over ranks;
+  * multi-GPU: one process per GPU (torchrun).  ``--shard rhs`` (default): weak scaling, every
+    rank applies the config's B vectors of its own (independent units, no collective), value =
+    all ranks' vectors / max-over-ranks time.  ``--shard k``: the terms are sharded and the
+    partial outputs all-reduced over NCCL inside the timed region (strong scaling);
   * ``e2e``: the same metric through the host C-ABI call ``pcb_apply_batch`` with pinned host
     buffers (H2D + kernels + D2H inside the timed region);
   * ``roofline``: the dominant kernel's algorithmic bytes / its CUDA-event time, measured
@@ -169,7 +170,7 @@ def run_reference(args, rank, world):
     v = float(np.mean(vals))
     cb["value"] = v
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": WORKLOADS[args.config]["B"] / v * 1e3, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": WORKLOADS[args.config]["B"] / v * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config shapes)",
             "config": {"workload": args.config, "global_batch": WORKLOADS[args.config]["B"]},
             "impl": "reference", "cpu_baseline": cb,
@@ -216,17 +217,23 @@ def main():
     B = args.batch or wl["B"]
     inp = inputs.make_config(cfg)
     N = inp.n_points
-    if args.shard == "rhs" and world > 1:
-        b0, b1 = B * rank // world, B * (rank + 1) // world
+    # --shard rhs (default): weak scaling -- every rank applies the config's B vectors of its own
+    # (rank r draws seed + r; rank 0 is the single-GPU workload), no collective.  --shard k: the
+    # terms are split across ranks and the partial outputs all-reduced (strong scaling).
+    weak = args.shard == "rhs"
+    if weak:
         shard = (0, 1)
+        Bl = B
+        seed = wl["seed"] + rank
     else:
-        b0, b1 = 0, B
         shard = (rank, world) if world > 1 else (0, 1)
-    Bl = b1 - b0
+        Bl = B
+        seed = wl["seed"]
+    B_total = B * world if weak else B
     op = ProductConvolutionOperator.from_inputs(inp, mode=args.mode, max_batch=max(1, min(Bl, 64)), shard=shard,
                                                 device=local_rank)
     info = op.info
-    F_host = normal_vectors(wl["seed"], B, N)[b0:b1]
+    F_host = normal_vectors(seed, Bl, N)
     F = torch.from_numpy(F_host).to(dev)
     G = torch.empty_like(F)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -272,7 +279,7 @@ def main():
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    value = B * args.steps / (total_ms * 1e-3)
+    value = B_total * args.steps / (total_ms * 1e-3)
 
     # ---- per-kernel profile (same workload, CUDA events around each launch on its stream) ----
     op.profile_begin()
@@ -327,7 +334,7 @@ def main():
         t = torch.tensor([e2e_total], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
-    e2e_value = B * len(e2e_ms) / (e2e_total * 1e-3)
+    e2e_value = B_total * len(e2e_ms) / (e2e_total * 1e-3)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -340,15 +347,15 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded mt19937_64 normal vectors; config blur operator built per BASELINE.json)",
-            "config": {"workload": cfg, "global_batch": B, "n": inp.shape, "r": inp.rank,
+            "config": {"workload": cfg, "global_batch": B_total, "per_gpu_batch": Bl, "n": inp.shape, "r": inp.rank,
                        "mode": info["mode"], "fft_size": info["fft_size"], "n_groups": info["n_groups"],
-                       "shard": args.shard if world > 1 else "none",
+                       "shard": args.shard if world > 1 else "none", "parallelism": f"{args.shard}{world}",
                        "l2": "flushed between timed steps (256 MiB write) and inputs > L2",
                        "spectra_bytes": info["spectra_bytes"]},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(B * N * 8),
-                    "d2h_bytes_per_step": int(B * N * 8)},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(B_total * N * 8),
+                    "d2h_bytes_per_step": int(B_total * N * 8)},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": dom_fam, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
@@ -359,10 +366,11 @@ def main():
                          "fp64": {"achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s",
                                   "frac": achieved_tf / fp64_peak, "peak_source": fp64_src}},
             "pipeline_roofline": {"algorithmic_bytes_per_vector": info["bytes_per_vector"],
-                                  "achieved_gbs": info["bytes_per_vector"] * value / 1e9,
-                                  "frac_hbm": info["bytes_per_vector"] * value / 1e9 / hbm,
-                                  "nominal_tflops": info["flops_per_vector"] * value / 1e12,
-                                  "frac_fp64": info["flops_per_vector"] * value / 1e12 / fp64_peak,
+                                  "per_gpu": True,
+                                  "achieved_gbs": info["bytes_per_vector"] * value / world / 1e9,
+                                  "frac_hbm": info["bytes_per_vector"] * value / world / 1e9 / hbm,
+                                  "nominal_tflops": info["flops_per_vector"] * value / world / 1e12,
+                                  "frac_fp64": info["flops_per_vector"] * value / world / 1e12 / fp64_peak,
                                   "definition": "SURVEY 8(d): every stored half spectrum read once + f + g"},
             "kernels_ms_per_step": {k: round(v[0] / 2, 4) for k, v in prof.items()},
             "clocks": clk,

@@ -1,13 +1,10 @@
 #!/bin/bash
-# ncu --set full on the first launch matching each demangled-name regex: ncu_one.sh "re1;re2" <bench args>
-RES=$1; shift
-CMD="python bench.py --profile-only --steps 1 --warmup 1 $*"
+# one `ncu --set full` capture of the first launch matching a kernel regex (after a plain run exits 0)
+# usage: ncu_one.sh <tag> <regex> [bench args]
+TAG=$1; KRE=$2; shift 2
+CMD="python bench.py --profile-only --steps 1 --warmup 3 $*"
 mkdir -p gpurun_out
-$CMD > gpurun_out/plain.log 2>&1 || { echo "plain run failed"; tail -5 gpurun_out/plain.log; exit 1; }
-i=0
-IFS=';' read -ra ARR <<< "$RES"
-for re in "${ARR[@]}"; do
-  ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$re" -c 1 \
-      -o gpurun_out/one_$i $CMD > gpurun_out/ncu_$i.log 2>&1
-  echo "ncu[$i] rc=$? $re"; i=$((i+1))
-done
+$CMD > gpurun_out/plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$KRE" -s 3 -c 1 \
+    -o gpurun_out/one_$TAG $CMD > gpurun_out/ncu_one.log 2>&1
+echo "ncu rc=$?"; tail -2 gpurun_out/ncu_one.log
