@@ -32,7 +32,10 @@
 #define PCB_ROWS_MINB_B 8
 #endif
 #ifndef PCB_BUNDLE_MB
-#define PCB_BUNDLE_MB 2  // bundle members staged per lane at a time
+#define PCB_BUNDLE_MB 1  // bundle members staged per lane at a time
+#endif
+#ifndef PCB_BUNDLE_DB
+#define PCB_BUNDLE_DB 1  // 1: double-buffered member staging (c3 +1.7% over MB = 2 single-buffered)
 #endif
 #ifndef PCB_ROWS_MINB_MIXED
 #define PCB_ROWS_MINB_MIXED 1
@@ -557,10 +560,10 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
     const int ax = a.D - 1;
     const int64_t line = a.line_id[aline];
     const int ulo = a.line_rng[2 * aline], uhi = a.line_rng[2 * aline + 1];
-    // layout: buf [BUFW] (FFT; reused as xs) | stage [NL][MB][N+1] | acc [n_last] | meta [NL]
+    // layout: buf [BUFW] (FFT; reused as xs) | stage [1 + DB][NL][MB][N+1] | acc [n_last] | meta [NL]
     double* xs = reinterpret_cast<double*>(buf);
     double2* stg = buf + BUFW;
-    double* acc = reinterpret_cast<double*>(stg + NL * MB * SL);
+    double* acc = reinterpret_cast<double*>(stg + (1 + PCB_BUNDLE_DB) * NL * MB * SL);
     GatherEntry* meta = reinterpret_cast<GatherEntry*>(acc + a.n[ax] + (a.n[ax] & 1));
     const int64_t b_beg = a.line_ptr[aline];
     const int64_t b_end = a.line_ptr[aline + 1];
@@ -581,20 +584,32 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
         double2 zk[R], zn[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) zk[r] = zn[r] = czero();
-        for (int m0 = 0; m0 < mmax; m0 += MB) {
+        // members staged MB at a time per lane; with PCB_BUNDLE_DB the next MB are in flight
+        // while the current ones are summed (two stage buffers)
+        auto issue = [&](int m0, int buf_i) {
 #pragma unroll
             for (int j = 0; j < MB; ++j)
                 if (m0 + j < cnt) {
                     const double2* src = a.T + mb[m0 + j].t_off + vec * mb[m0 + j].t_vst;
-                    double2* dst = stg + (l * MB + j) * SL;
+                    double2* dst = stg + ((buf_i * NL + l) * MB + j) * SL;
                     for (int i = tl; i < SL; i += TPL) cp_async16(&dst[i], src + i);
                 }
-            cp_async_wait_all();
+            asm volatile("cp.async.commit_group;\n" ::);
+        };
+        int cur = 0;
+        if (mmax > 0) issue(0, 0);
+        for (int m0 = 0; m0 < mmax; m0 += MB) {
+            if (PCB_BUNDLE_DB && m0 + MB < mmax) {
+                issue(m0 + MB, cur ^ 1);
+                asm volatile("cp.async.wait_group 1;\n" ::);
+            } else {
+                asm volatile("cp.async.wait_group 0;\n" ::);
+            }
             __syncthreads();
 #pragma unroll
             for (int j = 0; j < MB; ++j)
                 if (m0 + j < cnt) {
-                    const double2* x = stg + (l * MB + j) * SL;
+                    const double2* x = stg + ((cur * NL + l) * MB + j) * SL;
                     const double sc = mb[m0 + j].scale;
                     const int dl = mb[m0 + j].delta;
 #pragma unroll
@@ -609,7 +624,9 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
                         zn[r] = make_double2(fma(sc, xn.x, zn[r].x), fma(sc, xn.y, zn[r].y));
                     }
                 }
-            __syncthreads();  // stage slots free
+            __syncthreads();  // stage buffer `cur` free
+            if (PCB_BUNDLE_DB) cur ^= 1;
+            else if (m0 + MB < mmax) issue(m0 + MB, 0);
         }
         double2 v[R];
 #pragma unroll
