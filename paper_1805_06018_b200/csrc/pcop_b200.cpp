@@ -101,19 +101,25 @@ struct DevBuf {
     size_t bytes() const { return n * sizeof(T); }
 };
 
-bool g_pow2_only = false;    // PCB_POW2=1: power-of-two FFT sizes only (A/B measurement)
-bool g_mixed_last = false;   // PCB_MIXED_LAST=1: 3-smooth sizes on the R2C axis too (default: pow2 there)
-bool g_bundle = true;        // PCB_BUNDLE=0: one C2R per gather entry in the LOCAL apply (A/B)
+// Plan switches, fixed per handle at create (defaults, overridable for A/B measurement by env):
+//   PCB_POW2=1        power-of-two FFT sizes only
+//   PCB_MIXED_LAST=1  3-smooth sizes on the R2C axis too (default: only in 3-D)
+//   PCB_BUNDLE=0      one C2R per gather entry in the LOCAL apply (default: bundles in 2-D)
+struct PlanSwitches {
+    bool pow2_only = false;
+    bool mixed_last = false;
+    bool bundle = true;
+};
 
 // Smallest compiled FFT size >= max(v, 16): 2^a * {1, 3, 9}.  The last (R2C) axis also needs its
 // half length P/2 compiled for the row passes.
-int64_t fft_size_at_least(int64_t v, bool last_axis, bool mixed_last) {
+int64_t fft_size_at_least(int64_t v, bool last_axis, bool mixed_last, bool pow2_only) {
     for (int64_t p = 16; p <= (last_axis ? 4096 : 4096); p += 8) {
         if (p < v) continue;
         if (!fft_len_ok((int)p)) continue;
-        if (g_pow2_only && !is_pow2c((int)p)) continue;
+        if (pow2_only && !is_pow2c((int)p)) continue;
         if (last_axis && (!fft_len_ok((int)(p / 2)) || p / 2 > 2048 ||
-                          ((g_pow2_only || !mixed_last) && !is_pow2c((int)(p / 2)))))
+                          ((pow2_only || !mixed_last) && !is_pow2c((int)(p / 2)))))
             continue;
         if (!last_axis && cols_tile_width((int)p) < 0) continue;
         return p;
@@ -177,6 +183,7 @@ struct pcb_op {
     int r = 0;
     int mode = PCB_MODE_AUTO;
     int max_batch = 16;
+    pcb::PlanSwitches sw;
     std::vector<pcb::TermDesc> terms;
     std::vector<char> has_x, has_k, owned;
     pcb::TermDesc gdesc{};
@@ -484,7 +491,7 @@ void build_csr(pcb_op* op, Class& c, bool global, const std::vector<double>& ter
         out.mem.upload(hm);
         out.bundled = true;
     };
-    if (!global && g_bundle) flatten_b(c.apply);
+    if (!global && op->sw.bundle) flatten_b(c.apply);
     else flatten(ap, c.apply);
     flatten(ad, c.adj);
 }
@@ -634,10 +641,11 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
         int64_t mmax = 1;
         for (int k : mine) mmax = std::max<int64_t>(mmax, op->terms[k].m[a]);
         // GLOBAL: 3-smooth sizes on every axis (its row passes are not the bottleneck)
-        Pg[a] = fft_size_at_least(op->n[a] + mmax - 1, a == D - 1, true);
+        Pg[a] = fft_size_at_least(op->n[a] + mmax - 1, a == D - 1, true, op->sw.pow2_only);
     }
     auto local_P = [&](int k, int a) {
-        return fft_size_at_least((int64_t)op->terms[k].m[a] + op->terms[k].k_ext[a] - 1, a == D - 1, g_mixed_last);
+        return fft_size_at_least((int64_t)op->terms[k].m[a] + op->terms[k].k_ext[a] - 1, a == D - 1,
+                                 op->sw.mixed_last, op->sw.pow2_only);
     };
     bool global_ok = true, local_ok = true;
     for (int a = 0; a < D; ++a) global_ok = global_ok && Pg[a] <= 4096;
@@ -1118,15 +1126,15 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
         PCB_CK(cudaGetDeviceProperties(&prop, op->device));
         if (prop.major < 10) fail(PCB_ECUDA, "pcop-b200 kernels are built for sm_100a (Blackwell B200)");
         op->max_batch = opt.max_batch > 0 ? opt.max_batch : 16;
-        if (const char* e = getenv("PCB_POW2")) g_pow2_only = atoi(e) != 0;
+        if (const char* e = getenv("PCB_POW2")) op->sw.pow2_only = atoi(e) != 0;
         // 3-smooth sizes on the R2C axis pay off in 3-D (c4: +4%) but not in 2-D, where the
         // 24-element row kernels lose more to register pressure than they save (c3, c2: measured)
-        g_mixed_last = dim == 3;
-        if (const char* e = getenv("PCB_MIXED_LAST")) g_mixed_last = atoi(e) != 0;
+        op->sw.mixed_last = dim == 3;
+        if (const char* e = getenv("PCB_MIXED_LAST")) op->sw.mixed_last = atoi(e) != 0;
         // frequency-domain bundles pay in 2-D (c3 rows_inv 3.85 -> 3.36 ms); 3-D lines gather many
         // short same-shift entries and the per-entry path is faster there (c4: measured)
-        g_bundle = dim == 2;
-        if (const char* e = getenv("PCB_BUNDLE")) g_bundle = atoi(e) != 0;
+        op->sw.bundle = dim == 2;
+        if (const char* e = getenv("PCB_BUNDLE")) op->sw.bundle = atoi(e) != 0;
 
         PCB_CK(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
 
