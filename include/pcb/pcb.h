@@ -76,7 +76,7 @@ typedef struct pcb_info {
     double bytes_per_vector;  /* algorithmic HBM bytes per applied vector (spectra read once + f,g) */
     double flops_per_vector;  /* nominal fp64 flops per applied vector */
     int32_t launches_per_batch; /* kernels launched by one apply batch call */
-    int32_t reserved;
+    int32_t n_row_families; /* LOCAL apply: shared row-transform families (separable weights), 0: none */
     /* per applied vector, per kernel family {rows_fwd, mid, cols, rows_inv}: the bytes the kernel
      * must read and write once (its inputs and outputs in this pipeline) and nominal fp64 flops
      * (2.5 P log2 P per real line, 5 P log2 P per complex line, 8 per complex MAC) */

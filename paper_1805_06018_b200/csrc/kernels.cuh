@@ -30,7 +30,14 @@ struct TermDesc {
     // scratch pools (double2): this term's forward (S) / inverse (T) region for vector 0 and the
     // per-vector stride; rows of a region are planes of P1 * W (3-D) or W (2-D) values
     int64_t s_pool, s_vst, t_pool, t_vst;
-    int32_t P1;        // axis-1 FFT size of the term (3-D plane stride); 1 in 2-D
+    // row family (LOCAL apply, separable weights w_k = A_k(lead axes) * c(last axis)): the term's
+    // forward row transforms are the family's shared rows (double2 offset f_off for vector 0,
+    // + f_vst per vector, f_ps lines per family plane in 3-D) times A_k (a_pool + a_off); -1: none
+    int64_t f_off, f_vst, a_off;
+    int32_t f_ps;
+    int32_t P1;        // axis-1 FFT size of the term (3-D plane stride); 1 in 2-D.  A family
+                       // descriptor (rows_fwd item) holds its lead-axis-1 line count here
+    int32_t wrow0;     // 1: one weight row (w_off) serves every line (family descriptors)
     int32_t pad_;
 };
 
@@ -85,6 +92,7 @@ struct PassArgs {
     double2* T;            // inverse scratch pool (TermDesc::t_pool / t_vst)
     const double* w_pool;
     const double* phi_pool;
+    const double* a_pool;  // lead-axis weight factors of family terms (TermDesc::a_off)
     double2* spec_pool;
     const double2* tw;     // twiddle tables: length L at tw + (L - 8)
     const TermDesc* gdesc; // global-mode pseudo term (s = dom_lo, o = [0,n))

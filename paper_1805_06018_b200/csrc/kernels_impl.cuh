@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
                 const int64_t x1 = D == 3 ? td.x_lo[1] + c1 - a.dom_lo[1] : 0;
                 src = (int64_t)vec * a.N + (D == 3 ? (x0 * a.n[1] + x1) * a.n[2] : x0 * a.n[1]) +
                       (td.x_lo[ax] - a.dom_lo[ax]);
-                woff = td.w_off + (D == 3 ? c0 * td.m[1] + c1 : c0) * (int64_t)td.m[ax];
+                woff = td.w_off + (td.wrow0 ? 0 : (D == 3 ? c0 * td.m[1] + c1 : c0) * (int64_t)td.m[ax]);
                 row = D == 3 ? (c0 * td.P1 + c1) * a.W : c0 * a.W;
                 lo = 0;
                 hi = td.m[ax];
@@ -266,13 +266,31 @@ __global__ void __launch_bounds__(NL * FftCfg<P1>::TPL) k_mid(PassArgs a) {
                     plane * (int64_t)a.P[1] * a.W + c;
     double2 v[R];
     if (fwd) {
+        // family term: the input lines are the family's shared rows scaled by A_k(plane, line)
+        const bool fam = MODE == MM_FWD_APPLY && td.a_off >= 0;
+        const double2* src = fam ? a.S + td.f_off + vec * td.f_vst + plane * (int64_t)td.f_ps * a.W + c : base;
+        double sc[R];
+        if (fam) {
+            const double* av = a.a_pool + td.a_off + plane * (int64_t)td.m[1];
+#pragma unroll
+            for (int b = 0; b < R / RF; ++b)
+#pragma unroll
+                for (int r = 0; r < RF; ++r) {
+                    const int p = FirstPos<P1>::pos(tl, b, r);
+                    sc[b * RF + r] = (p >= in_lo && p < in_lo + in_cnt) ? __ldg(&av[p]) : 0.0;
+                }
+        }
 #pragma unroll
         for (int b = 0; b < R / RF; ++b)
 #pragma unroll
             for (int r = 0; r < RF; ++r) {
                 const int p = FirstPos<P1>::pos(tl, b, r);
-                v[b * RF + r] = (cvalid && p >= in_lo && p < in_lo + in_cnt) ? base[(int64_t)p * a.W] : czero();
+                v[b * RF + r] = (cvalid && p >= in_lo && p < in_lo + in_cnt) ? src[(int64_t)p * a.W] : czero();
             }
+        if (fam) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[r] = cscale(v[r], sc[r]);
+        }
         fft_fwd_order<P1, -1, NL, PSH<NL>>(v, buf, l, tl, twtab<P1>(a.tw));
         if (cvalid) {
 #pragma unroll
@@ -348,7 +366,27 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
         const int vec = item % nvec;
         const double2* S_item = MODE == CM_SPEC ? a.S + (int64_t)item * a.S_stride : a.S + td.s_pool + vec * td.s_vst;
         if (MODE == CM_SPEC) load_in(S_item, 0, P0, v);
-        else if (MODE == CM_APPLY_LOCAL) load_in(S_item, 0, td.m[0], v);
+        else if (MODE == CM_APPLY_LOCAL) {
+            // family term (2-D): the family's shared rows scaled by A_k(row).  All row and factor
+            // loads are issued before the first multiply (no per-element load -> use chains).
+            const bool fam = a.D == 2 && td.a_off >= 0;
+            double sc[R];
+            if (fam) {
+                const double* av = a.a_pool + td.a_off;
+#pragma unroll
+                for (int b = 0; b < R / RF; ++b)
+#pragma unroll
+                    for (int r = 0; r < RF; ++r) {
+                        const int p = FirstPos<P0>::pos(tl, b, r);
+                        sc[b * RF + r] = p < td.m[0] ? __ldg(&av[p]) : 0.0;
+                    }
+            }
+            load_in(fam ? a.S + td.f_off + vec * td.f_vst : S_item, 0, td.m[0], v);
+            if (fam) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[r] = cscale(v[r], sc[r]);
+            }
+        }
         else load_in(S_item, td.o_lo[0], td.o_cnt[0], v);
         fft_fwd_order<P0, -1, NL, PSH<NL>>(v, buf, l, tl, tw0);
         double2* spec = a.spec_pool + td.spec_off + tile_off;

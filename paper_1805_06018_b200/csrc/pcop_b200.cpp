@@ -18,6 +18,9 @@
 //           term's cropped output is gathered into Omega in ascending k.
 #include <cuda_runtime.h>
 
+#include <cfloat>
+#include <tuple>
+
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -109,6 +112,7 @@ struct PlanSwitches {
     bool pow2_only = false;
     bool mixed_last = false;
     bool bundle = true;
+    bool families = true;  // PCB_FAMILIES=0: per-term row transforms even for separable weights
 };
 
 // Smallest compiled FFT size >= max(v, 16): 2^a * {1, 3, 9}.  The last (R2C) axis also needs its
@@ -163,6 +167,10 @@ struct Class {
     int lines_apply = 1, lines_adj = 1;  // max rows_fwd lines per item
     int P0max = 1, P1max = 1;
     Csr apply, adj;
+    // row families (LOCAL apply): rows_fwd runs over these descriptors instead of the terms
+    std::vector<int> fams;  // indices into pcb_op::fams
+    DevBuf<int32_t> fam_slots;
+    int fam_lines = 1;      // max rows_fwd lines per family
 };
 
 std::atomic<long long> g_launches{0};
@@ -187,8 +195,9 @@ struct pcb_op {
     std::vector<pcb::TermDesc> terms;
     std::vector<char> has_x, has_k, owned;
     pcb::TermDesc gdesc{};
-    pcb::DevBuf<pcb::TermDesc> d_terms, d_gdesc;
-    pcb::DevBuf<double> w_pool, phi_pool;
+    pcb::DevBuf<pcb::TermDesc> d_terms, d_gdesc, d_fams;
+    std::vector<pcb::TermDesc> fams;  // row-family descriptors (rows_fwd items of family classes)
+    pcb::DevBuf<double> w_pool, phi_pool, a_pool;
     pcb::DevBuf<double2> spec_pool, tw;
     std::vector<pcb::Group> groups;
     std::vector<pcb::Class> classes;
@@ -272,6 +281,7 @@ PassArgs base_args(pcb_op* op, const int* P, int W, int64_t L, int nl) {
     a.T = op->T.p;
     a.w_pool = op->w_pool.p;
     a.phi_pool = op->phi_pool.p;
+    a.a_pool = op->a_pool.p;
     a.spec_pool = op->spec_pool.p;
     a.tw = op->tw.p;
     double sc = 1.0;
@@ -725,6 +735,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             gd.o_cnt[a] = a < D ? op->n[a] : 1;
             gd.m[a] = gd.o_cnt[a];
         }
+        gd.f_off = gd.f_vst = gd.a_off = -1;
     }
     // groups (full FFT shape) and classes (last-axis length)
     std::map<std::vector<int>, int> gid;
@@ -748,6 +759,109 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
         op->groups[it->second].terms.push_back(k);
         op->classes[cid[key[D - 1]]].terms.push_back(k);
     }
+    // Row families (LOCAL apply).  A term whose weight factors exactly as w_k[u] = A_k(u_lead) *
+    // c(u_last) (tensor-product tents, pc_operator.cpp:221-248) has last-axis row transforms
+    // R2C(w_k f)[lead] = A_k(lead) * R2C(c f)[lead].  Terms of one class with the same last-axis
+    // window and the same factor c (bitwise) share the row transforms of c f over the union of
+    // their lead boxes; the pass after the rows (cols in 2-D, mid in 3-D) applies A_k as it loads.
+    // A class uses families only when every term factors and the shared rows are >= 1.2x fewer.
+    for (TermDesc& t : op->terms) {
+        t.f_off = t.f_vst = t.a_off = -1;
+        t.f_ps = 0;
+        t.wrow0 = 0;
+    }
+    std::vector<double> apool;
+    std::vector<int> term_fam(r, -1);
+    if (mode == PCB_MODE_LOCAL && op->sw.families) {
+        const int ax = D - 1;
+        auto lead_of = [&](const TermDesc& t) { return D == 2 ? (int64_t)t.m[0] : (int64_t)t.m[0] * t.m[1]; };
+        for (Class& c : op->classes) {
+            std::vector<std::vector<double>> A(c.terms.size()), cf(c.terms.size());
+            bool ok = true;
+            for (size_t i = 0; i < c.terms.size() && ok; ++i) {
+                const TermDesc& t = op->terms[c.terms[i]];
+                const int64_t ml = t.m[ax], lead = lead_of(t);
+                const double* w = wpool.data() + t.w_off;
+                int64_t piv = -1;
+                double pv = 0.0;
+                for (int64_t j = 0; j < lead * ml; ++j)
+                    if (std::fabs(w[j]) > pv) {
+                        pv = std::fabs(w[j]);
+                        piv = j;
+                    }
+                if (piv < 0) {
+                    ok = false;
+                    break;
+                }
+                const int64_t pl = piv / ml, pq = piv % ml;
+                cf[i].assign(w + pl * ml, w + pl * ml + ml);
+                A[i].resize(lead);
+                for (int64_t L = 0; L < lead; ++L) A[i][L] = w[L * ml + pq] / w[piv];
+                for (int64_t L = 0; L < lead && ok; ++L)
+                    for (int64_t q = 0; q < ml; ++q) {
+                        const double ref = w[L * ml + q];
+                        if (std::fabs(A[i][L] * cf[i][q] - ref) > 4.0 * DBL_EPSILON * std::fabs(ref)) {
+                            ok = false;
+                            break;
+                        }
+                    }
+            }
+            if (!ok || c.terms.empty()) continue;
+            std::map<std::tuple<int64_t, int32_t, std::vector<double>>, int> fid;
+            std::vector<std::vector<int>> members;  // positions in c.terms
+            for (size_t i = 0; i < c.terms.size(); ++i) {
+                const TermDesc& t = op->terms[c.terms[i]];
+                auto key = std::make_tuple(t.x_lo[ax], t.m[ax], cf[i]);
+                auto it = fid.find(key);
+                if (it == fid.end()) {
+                    it = fid.emplace(key, (int)members.size()).first;
+                    members.emplace_back();
+                }
+                members[it->second].push_back((int)i);
+            }
+            std::vector<TermDesc> fd(members.size());
+            int64_t lines_terms = 0, lines_fams = 0;
+            for (size_t f = 0; f < members.size(); ++f) {
+                TermDesc& d = fd[f];
+                d = TermDesc{};
+                const TermDesc& t0 = op->terms[c.terms[members[f][0]]];
+                for (int a = 0; a < D - 1; ++a) {
+                    int64_t lo = INT64_MAX, hi = INT64_MIN;
+                    for (int i : members[f]) {
+                        const TermDesc& t = op->terms[c.terms[i]];
+                        lo = std::min<int64_t>(lo, t.x_lo[a]);
+                        hi = std::max<int64_t>(hi, t.x_lo[a] + t.m[a]);
+                    }
+                    d.x_lo[a] = lo;
+                    d.m[a] = (int32_t)(hi - lo);
+                }
+                for (int a = D - 1; a < 3; ++a) {
+                    d.x_lo[a] = t0.x_lo[a];
+                    d.m[a] = t0.m[a];
+                }
+                d.P1 = D == 3 ? d.m[1] : 1;
+                d.wrow0 = 1;
+                d.f_off = d.f_vst = d.a_off = -1;
+                lines_fams += lead_of(d);
+                for (int i : members[f]) lines_terms += lead_of(op->terms[c.terms[i]]);
+            }
+            if (members.size() == c.terms.size() || (double)lines_terms < 1.2 * (double)lines_fams) continue;
+            for (size_t f = 0; f < members.size(); ++f) {
+                fd[f].w_off = (int64_t)wpool.size();
+                wpool.insert(wpool.end(), cf[members[f][0]].begin(), cf[members[f][0]].end());
+                for (int i : members[f]) {
+                    TermDesc& t = op->terms[c.terms[i]];
+                    t.a_off = (int64_t)apool.size();
+                    apool.insert(apool.end(), A[i].begin(), A[i].end());
+                    term_fam[c.terms[i]] = (int)op->fams.size();
+                }
+                c.fams.push_back((int)op->fams.size());
+                c.fam_lines = std::max<int>(c.fam_lines, (int)lead_of(fd[f]));
+                op->fams.push_back(fd[f]);
+            }
+        }
+    }
+
     // layout: spectra per group; scratch regions per term (pools reused class by class)
     int64_t spec_total = 0;
     for (Group& g : op->groups) {
@@ -787,6 +901,10 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             c.lines_adj = std::max<int>(c.lines_adj, D == 2 ? t.o_cnt[0] : t.o_cnt[0] * t.o_cnt[1]);
             c.P1max = std::max(c.P1max, t.P1);
         }
+        for (int fi : c.fams) {
+            const TermDesc& f = op->fams[fi];
+            s_sum += (D == 2 ? (int64_t)f.m[0] : (int64_t)f.m[0] * f.m[1]) * c.W;
+        }
         for (int gi : c.groups) c.P0max = std::max(c.P0max, op->groups[gi].P[0]);
         if (mode == PCB_MODE_GLOBAL) {
             const int64_t plane = D == 2 ? c.W : (int64_t)op->gdesc.P1 * c.W;
@@ -824,6 +942,22 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
                 to += reg * vb;
             }
         }
+        for (int fi : c.fams) {  // family rows after the term regions
+            TermDesc& f = op->fams[fi];
+            f.s_pool = so;
+            f.s_vst = (D == 2 ? (int64_t)f.m[0] : (int64_t)f.m[0] * f.m[1]) * c.W;
+            so += f.s_vst * vb;
+        }
+        for (int k : c.terms) {
+            if (term_fam[k] < 0) continue;
+            TermDesc& t = op->terms[k];
+            const TermDesc& f = op->fams[term_fam[k]];
+            const int64_t line0 = D == 2 ? t.x_lo[0] - f.x_lo[0]
+                                         : (t.x_lo[0] - f.x_lo[0]) * f.m[1] + (t.x_lo[1] - f.x_lo[1]);
+            t.f_off = f.s_pool + line0 * c.W;
+            t.f_vst = f.s_vst;
+            t.f_ps = D == 3 ? f.m[1] : 0;
+        }
     }
     if (mode == PCB_MODE_GLOBAL) {
         TermDesc& g = op->gdesc;
@@ -842,6 +976,8 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     op->d_gdesc.upload(std::vector<TermDesc>{op->gdesc});
     op->w_pool.upload(wpool);
     op->phi_pool.upload(ppool);
+    op->d_fams.upload(op->fams.empty() ? std::vector<TermDesc>(1) : op->fams);
+    op->a_pool.upload(apool.empty() ? std::vector<double>(1, 0.0) : apool);
     for (Group& g : op->groups) g.slots.upload(std::vector<int32_t>(g.terms.begin(), g.terms.end()));
     // 1 / prod P per term (its group's FFT size); the last slot serves the global pseudo term
     std::vector<double> term_scale(op->terms.size() + 1, 1.0);
@@ -853,6 +989,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     }
     for (Class& c : op->classes) {
         c.slots.upload(std::vector<int32_t>(c.terms.begin(), c.terms.end()));
+        if (!c.fams.empty()) c.fam_slots.upload(std::vector<int32_t>(c.fams.begin(), c.fams.end()));
         build_csr(op, c, mode == PCB_MODE_GLOBAL, term_scale);
     }
 
@@ -922,8 +1059,16 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     in.bytes_per_vector = sb + 16.0 * (double)op->N;
     in.flops_per_vector = mode == PCB_MODE_GLOBAL ? g_fl : l_fl;
     in.launches_per_batch = (int)(2 * op->classes.size() + op->groups.size() * (D == 3 ? 3 : 1));
+    in.n_row_families = (int32_t)op->fams.size();
     // per-kernel compulsory bytes and nominal flops per vector (apply)
     for (int i = 0; i < 4; ++i) in.kernel_bytes[i] = in.kernel_flops[i] = 0.0;
+    for (const Class& c : op->classes)
+        for (int fi : c.fams) {  // shared rows: f and c in, the family's transforms out
+            const TermDesc& f = op->fams[fi];
+            const double lead = D == 2 ? f.m[0] : (double)f.m[0] * f.m[1];
+            in.kernel_bytes[0] += lead * f.m[D - 1] * 8.0 + lead * (c.P_last / 2 + 1) * 16.0;
+            in.kernel_flops[0] += lead * fft_flops_r((double)c.P_last);
+        }
     {
         const bool gl = mode == PCB_MODE_GLOBAL;
         for (const Group& g : op->groups) {
@@ -935,8 +1080,10 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
                 const double mlead = D == 2 ? t.m[0] : (double)t.m[0] * t.m[1];
                 const double mall = mlead * t.m[D - 1];
                 const double olead = D == 2 ? t.o_cnt[0] : (double)t.o_cnt[0] * t.o_cnt[1];
-                in.kernel_bytes[0] += mall * 16.0 + mlead * Nc * 16.0;              // f, w in; S out
-                in.kernel_flops[0] += mlead * fft_flops_r(Pl);
+                if (t.a_off < 0) {  // (family classes: counted per family below)
+                    in.kernel_bytes[0] += mall * 16.0 + mlead * Nc * 16.0;          // f, w in; S out
+                    in.kernel_flops[0] += mlead * fft_flops_r(Pl);
+                }
                 if (D == 3) {
                     in.kernel_bytes[1] += 2.0 * t.m[0] * P1 * Nc * 16.0;
                     in.kernel_flops[1] += t.m[0] * Nc * fft_flops_c(P1) + (gl ? 0.0 : t.o_cnt[0] * Nc * fft_flops_c(P1));
@@ -1011,8 +1158,17 @@ void run_batch(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG
             a.n_slots = (int)c.terms.size();
             a.global = global;
             a.lines_max = adjoint ? c.lines_adj : c.lines_apply;
-            launch(op, st, adjoint ? "rows_fwd(adjoint)" : "rows_fwd(apply)",
-                   [&] { return launch_rows_fwd(a, adjoint ? RF_ADJ : RF_APPLY, st); });
+            if (!adjoint && !c.fams.empty()) {  // shared row transforms of the class's families
+                PassArgs af = a;
+                af.terms = op->d_fams.p;
+                af.slots = c.fam_slots.p;
+                af.n_slots = (int)c.fams.size();
+                af.lines_max = c.fam_lines;
+                launch(op, st, "rows_fwd(apply)", [&] { return launch_rows_fwd(af, RF_APPLY, st); });
+            } else {
+                launch(op, st, adjoint ? "rows_fwd(adjoint)" : "rows_fwd(apply)",
+                       [&] { return launch_rows_fwd(a, adjoint ? RF_ADJ : RF_APPLY, st); });
+            }
             for (int gi : c.groups) {
                 const Group& g = op->groups[gi];
                 PassArgs ga = group_args(op, g);
@@ -1135,6 +1291,7 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
         // short same-shift entries and the per-entry path is faster there (c4: measured)
         op->sw.bundle = dim == 2;
         if (const char* e = getenv("PCB_BUNDLE")) op->sw.bundle = atoi(e) != 0;
+        if (const char* e = getenv("PCB_FAMILIES")) op->sw.families = atoi(e) != 0;
 
         PCB_CK(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
 

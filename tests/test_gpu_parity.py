@@ -366,3 +366,42 @@ def test_bundled_gather_matches_per_entry_gather(gpu, name, monkeypatch):
     b = ProductConvolutionOperator.from_inputs(inp, mode="local").apply_batch(F)
     for i in range(2):
         assert rel(b[i], a[i]) <= 1e-14
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "small2d", "small3d", "small1d"])
+def test_row_families_match_per_term_rows(gpu, name, monkeypatch):
+    """Separable (tent) weights: terms sharing a last-axis weight factor share their row
+    transforms, scaled per term by the lead-axis factor.  Same operator as the per-term rows
+    (PCB_FAMILIES=0) and as the oracle; the adjoint path is untouched."""
+    inp = inputs.make_config(name) if name.startswith("c") else inputs.small_lattice(**SMALL[name])
+    F = normal_vectors(9, 2, inp.n_points)
+    monkeypatch.setenv("PCB_FAMILIES", "0")
+    off = ProductConvolutionOperator.from_inputs(inp, mode="local")
+    monkeypatch.setenv("PCB_FAMILIES", "1")
+    on = ProductConvolutionOperator.from_inputs(inp, mode="local")
+    assert off.info["n_row_families"] == 0
+    if inp.dim > 1:
+        assert 0 < on.info["n_row_families"] < inp.rank
+    a, b = off.apply_batch(F), on.apply_batch(F)
+    for i in range(2):
+        assert rel(b[i], a[i]) <= 1e-14
+    if name.startswith("small"):
+        ref = O.PCOperator.from_inputs(inp)
+        for i in range(2):
+            assert rel(b[i], ref.apply(F[i])) <= APPLY_TOL
+    assert np.array_equal(on.apply_adjoint_batch(F), off.apply_adjoint_batch(F))
+
+
+def test_non_separable_weights_use_per_term_rows(gpu):
+    """Weights that do not factor (a random perturbation of the tents) keep per-term rows."""
+    inp = inputs.small_lattice(n=24, dim=2, m=3, sigma=1.7)
+    rng = np.random.default_rng(5)
+    for w in inp.weights:
+        w.values[...] = w.values * (1.0 + 0.1 * rng.random(w.values.shape))
+    op = ProductConvolutionOperator.from_inputs(inp, mode="local")
+    assert op.info["n_row_families"] == 0
+    F = normal_vectors(4, 2, inp.n_points)
+    ref = O.PCOperator.from_inputs(inp)
+    G = op.apply_batch(F)
+    for i in range(2):
+        assert rel(G[i], ref.apply(F[i])) <= APPLY_TOL
