@@ -82,6 +82,8 @@ typedef struct pcb_info {
      * (2.5 P log2 P per real line, 5 P log2 P per complex line, 8 per complex MAC) */
     double kernel_bytes[4];
     double kernel_flops[4];
+    int32_t n_column_chains; /* 2-D LOCAL apply: column chains (terms sharing one axis-0 inverse) */
+    int32_t n_chained_terms; /* terms in chains of two or more */
 } pcb_info;
 
 PCB_API void pcb_default_options(pcb_options* opt);

@@ -93,6 +93,11 @@ struct PassArgs {
     const double* w_pool;
     const double* phi_pool;
     const double* a_pool;  // lead-axis weight factors of family terms (TermDesc::a_off)
+    // column chains (CM_APPLY_CHAIN): slots index chains; chain c has output descriptor chains[c]
+    // and member terms chain_terms[chain_ptr[c] .. chain_ptr[c + 1])
+    const TermDesc* chains;
+    const int32_t* chain_ptr;
+    const int32_t* chain_terms;
     double2* spec_pool;
     const double2* tw;     // twiddle tables: length L at tw + (L - 8)
     const TermDesc* gdesc; // global-mode pseudo term (s = dom_lo, o = [0,n))
@@ -105,7 +110,8 @@ struct PassArgs {
 };
 
 enum RowsFwdMode { RF_APPLY = 0, RF_ADJ = 1, RF_SPEC = 2 };
-enum ColsMode { CM_SPEC = 0, CM_APPLY_LOCAL = 1, CM_APPLY_GLOBAL = 2, CM_ADJ_LOCAL = 3, CM_ADJ_GLOBAL = 4 };
+enum ColsMode { CM_SPEC = 0, CM_APPLY_LOCAL = 1, CM_APPLY_GLOBAL = 2, CM_ADJ_LOCAL = 3, CM_ADJ_GLOBAL = 4,
+                CM_APPLY_CHAIN = 5 };
 enum MidMode { MM_FWD_APPLY = 0, MM_FWD_ADJ = 1, MM_FWD_SPEC = 2, MM_INV_APPLY = 3, MM_INV_ADJ = 4 };
 enum RowsInvMode { RI_APPLY = 0, RI_ADJ = 1, RI_APPLY_B = 2 };
 

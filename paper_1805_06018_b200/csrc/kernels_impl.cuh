@@ -40,6 +40,9 @@
 #ifndef PCB_ROWS_MINB_MIXED
 #define PCB_ROWS_MINB_MIXED 1
 #endif
+#ifndef PCB_CHAIN_STAGE
+#define PCB_CHAIN_STAGE 1  // column chains: stage each member's spectrum tile in shared memory
+#endif
 #ifndef PCB_COLS_THREADS
 #define PCB_COLS_THREADS 64
 #endif
@@ -358,6 +361,27 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
             }
     };
     auto fpos = [&](int r) { return mid_pos<P0>(tl, r); };
+    // apply input of term td, vector vec: its S rows, or (2-D family term) the family's shared rows
+    // scaled by A_k(row).  All row and factor loads are issued before the first multiply.
+    auto load_apply = [&](const TermDesc& td, int vec, double2* v) {
+        const bool fam = a.D == 2 && td.a_off >= 0;
+        double sc[R];
+        if (fam) {
+            const double* av = a.a_pool + td.a_off;
+#pragma unroll
+            for (int b = 0; b < R / RF; ++b)
+#pragma unroll
+                for (int r = 0; r < RF; ++r) {
+                    const int p = FirstPos<P0>::pos(tl, b, r);
+                    sc[b * RF + r] = p < td.m[0] ? __ldg(&av[p]) : 0.0;
+                }
+        }
+        load_in(fam ? a.S + td.f_off + vec * td.f_vst : a.S + td.s_pool + vec * td.s_vst, 0, td.m[0], v);
+        if (fam) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[r] = cscale(v[r], sc[r]);
+        }
+    };
 
     double2 v[R];
     if (MODE == CM_SPEC || MODE == CM_APPLY_LOCAL || MODE == CM_ADJ_LOCAL) {
@@ -366,27 +390,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
         const int vec = item % nvec;
         const double2* S_item = MODE == CM_SPEC ? a.S + (int64_t)item * a.S_stride : a.S + td.s_pool + vec * td.s_vst;
         if (MODE == CM_SPEC) load_in(S_item, 0, P0, v);
-        else if (MODE == CM_APPLY_LOCAL) {
-            // family term (2-D): the family's shared rows scaled by A_k(row).  All row and factor
-            // loads are issued before the first multiply (no per-element load -> use chains).
-            const bool fam = a.D == 2 && td.a_off >= 0;
-            double sc[R];
-            if (fam) {
-                const double* av = a.a_pool + td.a_off;
-#pragma unroll
-                for (int b = 0; b < R / RF; ++b)
-#pragma unroll
-                    for (int r = 0; r < RF; ++r) {
-                        const int p = FirstPos<P0>::pos(tl, b, r);
-                        sc[b * RF + r] = p < td.m[0] ? __ldg(&av[p]) : 0.0;
-                    }
-            }
-            load_in(fam ? a.S + td.f_off + vec * td.f_vst : S_item, 0, td.m[0], v);
-            if (fam) {
-#pragma unroll
-                for (int r = 0; r < R; ++r) v[r] = cscale(v[r], sc[r]);
-            }
-        }
+        else if (MODE == CM_APPLY_LOCAL) load_apply(td, vec, v);
         else load_in(S_item, td.o_lo[0], td.o_cnt[0], v);
         fft_fwd_order<P0, -1, NL, PSH<NL>>(v, buf, l, tl, tw0);
         double2* spec = a.spec_pool + td.spec_off + tile_off;
@@ -406,6 +410,47 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
         double2* T_item = a.T + td.t_pool + vec * td.t_vst;
         if (MODE == CM_APPLY_LOCAL) store_out(T_item, td.o_lo[0], td.o_cnt[0], v);
         else store_out(T_item, 0, td.m[0], v);
+        return;
+    }
+
+    if (MODE == CM_APPLY_CHAIN) {
+        // column chain: the members' products FFT(w_k f) . Phi_k (each Phi_k placed at the chain
+        // origin) summed in registers, one inverse per (chain, vector, column tile)
+        double2* sspec = buf + smem_words<P0, NL>();
+        const int slot = item / nvec;
+        const int vec = item % nvec;
+        const int cid = a.slots[slot];
+        const TermDesc& ch = a.chains[cid];
+        double2 acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = czero();
+        constexpr bool STAGE = PCB_CHAIN_STAGE && P0 <= 512;
+        const int m_end = a.chain_ptr[cid + 1];
+        for (int mi = a.chain_ptr[cid]; mi < m_end; ++mi) {
+            const TermDesc& td = a.terms[a.chain_terms[mi]];
+            const double2* tile = a.spec_pool + td.spec_off + (c0 / NL) * (int64_t)P0 * NL;
+            if (STAGE) {
+                __syncthreads();  // previous member's product finished reading sspec
+                for (int i = threadIdx.x; i < P0 * NL; i += NL * FftCfg<P0>::TPL) cp_async16(&sspec[i], tile + i);
+                asm volatile("cp.async.commit_group;\n" ::);
+            }
+            load_apply(td, vec, v);
+            fft_fwd_order<P0, -1, NL, PSH<NL>>(v, buf, l, tl, tw0);
+            if (STAGE) {
+                asm volatile("cp.async.wait_group 0;\n" ::);
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < R; ++r) acc[r] = cadd(acc[r], cmul(v[r], sspec[fpos(r) * NL + l]));
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const double2 ph = cvalid ? __ldg(&tile[(int64_t)fpos(r) * NL + l]) : czero();
+                    acc[r] = cadd(acc[r], cmul(v[r], ph));
+                }
+            }
+        }
+        fft_rev_order<P0, +1, NL, PSH<NL>>(acc, buf, l, tl, tw0);
+        store_out(a.T + ch.t_pool + vec * ch.t_vst, ch.o_lo[0], ch.o_cnt[0], acc);
         return;
     }
 

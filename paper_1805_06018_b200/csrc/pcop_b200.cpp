@@ -22,6 +22,7 @@
 #include <tuple>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -113,6 +114,12 @@ struct PlanSwitches {
     bool mixed_last = false;
     bool bundle = true;
     bool families = true;  // PCB_FAMILIES=0: per-term row transforms even for separable weights
+    // PCB_CHAINS=1: column chains in the 2-D LOCAL apply.  Measured on B200 (c3): the gather gets
+    // 10-17% faster but the chained column pass loses more (one S-load latency per member per CTA
+    // without an inverse FFT to hide it), net -1..-2%; off by default, kept tested.
+    bool chains = false;
+    double chain_beta = 24.0;  // PCB_CHAIN_BETA: modelled cost of one T row element, in column-FFT units
+    bool chain_grow = false;   // PCB_CHAIN_GROW=1: a chain may use a larger FFT than its members' own
 };
 
 // Smallest compiled FFT size >= max(v, 16): 2^a * {1, 3, 9}.  The last (R2C) axis also needs its
@@ -154,6 +161,8 @@ struct Group {
     int64_t Lt = 0;  // L rounded up to the tile width
     std::vector<int> terms;
     DevBuf<int32_t> slots;
+    std::vector<int> chains;  // column chains of the group (2-D LOCAL apply), indices into pcb_op::chains
+    DevBuf<int32_t> chain_slots;
 };
 
 // Terms with the same last-axis length: the row passes (R2C / gathered C2R) run per class, so
@@ -169,6 +178,7 @@ struct Class {
     Csr apply, adj;
     // row families (LOCAL apply): rows_fwd runs over these descriptors instead of the terms
     std::vector<int> fams;  // indices into pcb_op::fams
+    std::vector<int> chains;  // column chains of the class: the apply gather reads their T rows
     DevBuf<int32_t> fam_slots;
     int fam_lines = 1;      // max rows_fwd lines per family
 };
@@ -197,6 +207,11 @@ struct pcb_op {
     pcb::TermDesc gdesc{};
     pcb::DevBuf<pcb::TermDesc> d_terms, d_gdesc, d_fams;
     std::vector<pcb::TermDesc> fams;  // row-family descriptors (rows_fwd items of family classes)
+    // column chains: output descriptor (s, o_lo/o_cnt, T region; m[ax] = axis-1 support) + members
+    std::vector<pcb::TermDesc> chains;
+    std::vector<std::vector<int>> chain_members;
+    pcb::DevBuf<pcb::TermDesc> d_chains;
+    pcb::DevBuf<int32_t> chain_ptr, chain_terms;
     pcb::DevBuf<double> w_pool, phi_pool, a_pool;
     pcb::DevBuf<double2> spec_pool, tw;
     std::vector<pcb::Group> groups;
@@ -282,6 +297,9 @@ PassArgs base_args(pcb_op* op, const int* P, int W, int64_t L, int nl) {
     a.w_pool = op->w_pool.p;
     a.phi_pool = op->phi_pool.p;
     a.a_pool = op->a_pool.p;
+    a.chains = op->d_chains.p;
+    a.chain_ptr = op->chain_ptr.p;
+    a.chain_terms = op->chain_terms.p;
     a.spec_pool = op->spec_pool.p;
     a.tw = op->tw.p;
     double sc = 1.0;
@@ -338,9 +356,8 @@ void build_csr(pcb_op* op, Class& c, bool global, const std::vector<double>& ter
         return D == 2 ? c0 - op->dom_lo[0] : (c0 - op->dom_lo[0]) * op->n[1] + (c1 - op->dom_lo[1]);
     };
     // entry's output range along the last axis (domain-relative) and its line shift
-    auto finish = [&](GatherEntry& e, const TermDesc& t, bool adjoint, int64_t w_row) {
-        const int64_t k = &t - op->terms.data();
-        e.scale = (k >= 0 && k < (int64_t)op->terms.size()) ? term_scale[k] : term_scale.back();
+    auto finish = [&](GatherEntry& e, const TermDesc& t, bool adjoint, int64_t w_row, double scale) {
+        e.scale = scale;
         if (!adjoint) {
             e.sh = (int)(t.s[ax] - op->dom_lo[ax]);
             e.lo = e.sh + t.o_lo[ax];
@@ -356,7 +373,7 @@ void build_csr(pcb_op* op, Class& c, bool global, const std::vector<double>& ter
         e.hi = std::min(e.hi, op->n[ax]);
     };
     std::vector<std::vector<GatherEntry>> ap(n_lines), ad(n_lines);
-    std::vector<std::vector<int>> apk(n_lines);  // term of each apply entry (bundling)
+    std::vector<std::vector<const TermDesc*>> apk(n_lines);  // output descriptor of each apply entry (bundling)
     for (int k : c.terms) {
         const TermDesc& t = op->terms[k];
         const int64_t plane = D == 2 ? c.W : (int64_t)t.P1 * c.W;
@@ -367,24 +384,38 @@ void build_csr(pcb_op* op, Class& c, bool global, const std::vector<double>& ter
                 GatherEntry e{};
                 e.t_off = t.t_pool + (int64_t)u0 * plane + (int64_t)u1 * c.W;
                 e.t_vst = t.t_vst;
-                finish(e, t, true, D == 3 ? u0 * t.m[1] + u1 : u0);
+                finish(e, t, true, D == 3 ? u0 * t.m[1] + u1 : u0, term_scale[k]);
                 ad[line_of(t.x_lo[0] + u0, D == 3 ? t.x_lo[1] + u1 : 0)].push_back(e);
             }
-        if (!global) {
+        if (!global && c.chains.empty()) {
             const int o1n = D == 3 ? t.o_cnt[1] : 1;
             for (int j0 = 0; j0 < t.o_cnt[0]; ++j0)
                 for (int j1 = 0; j1 < o1n; ++j1) {
                     GatherEntry e{};
                     e.t_off = t.t_pool + (int64_t)j0 * plane + (int64_t)j1 * c.W;
                     e.t_vst = t.t_vst;
-                    finish(e, t, false, 0);
+                    finish(e, t, false, 0, term_scale[k]);
                     const int64_t y0 = t.s[0] + t.o_lo[0] + j0;
                     const int64_t y1 = D == 3 ? t.s[1] + t.o_lo[1] + j1 : 0;
                     ap[line_of(y0, y1)].push_back(e);
-                    apk[line_of(y0, y1)].push_back(k);
+                    apk[line_of(y0, y1)].push_back(&t);
                 }
         }
     }
+    if (!global)  // column chains (2-D): one T row set per chain, in chain order
+        for (int ci : c.chains) {
+            const TermDesc& ch = op->chains[ci];
+            const double sc = term_scale[op->chain_members[ci][0]];
+            for (int j0 = 0; j0 < ch.o_cnt[0]; ++j0) {
+                GatherEntry e{};
+                e.t_off = ch.t_pool + (int64_t)j0 * c.W;
+                e.t_vst = ch.t_vst;
+                finish(e, ch, false, 0, sc);
+                const int64_t y0 = ch.s[0] + ch.o_lo[0] + j0;
+                ap[line_of(y0, 0)].push_back(e);
+                apk[line_of(y0, 0)].push_back(&ch);
+            }
+        }
     if (global) {
         const TermDesc& g = op->gdesc;
         const int64_t plane = D == 2 ? c.W : (int64_t)g.P1 * c.W;
@@ -394,7 +425,7 @@ void build_csr(pcb_op* op, Class& c, bool global, const std::vector<double>& ter
             const int64_t j1 = D == 2 ? 0 : ln % op->n[1];
             e.t_off = g.t_pool + j0 * plane + j1 * c.W;
             e.t_vst = g.t_vst;
-            finish(e, g, false, 0);
+            finish(e, g, false, 0, term_scale.back());
             ap[ln].push_back(e);
         }
     }
@@ -467,7 +498,7 @@ void build_csr(pcb_op* op, Class& c, bool global, const std::vector<double>& ter
                 size_t j = i;
                 while (j < idx.size()) {
                     const GatherEntry& e = L[idx[j]];
-                    const TermDesc& t = op->terms[apk[ln][idx[j]]];
+                    const TermDesc& t = *apk[ln][idx[j]];
                     // the whole support of the line's C2R (not only its in-domain part) must stay
                     // inside the period, or the out-of-domain tail would wrap onto the window
                     const int end = e.sh - sh0 + t.m[ax] + t.k_ext[ax] - 1;
@@ -653,7 +684,9 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
         // GLOBAL: 3-smooth sizes on every axis (its row passes are not the bottleneck)
         Pg[a] = fft_size_at_least(op->n[a] + mmax - 1, a == D - 1, true, op->sw.pow2_only);
     }
+    std::vector<std::array<int64_t, 3>> chainP(r, std::array<int64_t, 3>{0, 0, 0});
     auto local_P = [&](int k, int a) {
+        if (chainP[k][a] > 0) return chainP[k][a];
         return fft_size_at_least((int64_t)op->terms[k].m[a] + op->terms[k].k_ext[a] - 1, a == D - 1,
                                  op->sw.mixed_last, op->sw.pow2_only);
     };
@@ -724,6 +757,101 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             t.o_cnt[a] = 1;
         }
     }
+    // Column chains (2-D LOCAL apply).  Terms of one lattice column (same axis-1 window) whose full
+    // output supports fit one period on both axes can share their axis-0 inverse: with every
+    // member's Phi_k placed at the chain origin s_c, IFFT(sum_k Phi_k . FFT(w_k f)) is the sum of
+    // the members' linear convolutions, none of which wraps (support union <= P).  The cols pass
+    // accumulates the members' products in registers and writes ONE T region per chain, so the
+    // gather reads one set of rows per chain.  Consecutive terms (by s_0) are chained by dynamic
+    // programming on a modelled cost: column FFTs W * (members + 1) * P0 log2 P0 plus chain_beta
+    // per T row element (its write, read and C2R).  Chains of one are the plain LOCAL plan.
+    std::vector<int> term_chain(r, -1);
+    if (mode == PCB_MODE_LOCAL && D == 2 && op->sw.chains) {
+        std::map<std::pair<int64_t, int32_t>, std::vector<int>> clusters;
+        for (int k : mine) clusters[{op->terms[k].x_lo[1], op->terms[k].m[1]}].push_back(k);
+        struct Ch {
+            int64_t lo[2], hi[2], P[2];
+        };
+        auto eval = [&](const std::vector<int>& ks, size_t i, size_t j, Ch& ch) -> double {
+            for (int a = 0; a < 2; ++a) {
+                ch.lo[a] = INT64_MAX;
+                ch.hi[a] = INT64_MIN;
+                for (size_t q = i; q < j; ++q) {
+                    const TermDesc& t = op->terms[ks[q]];
+                    const int64_t s0 = t.x_lo[a] + t.k_lo[a];
+                    ch.lo[a] = std::min(ch.lo[a], s0);
+                    ch.hi[a] = std::max<int64_t>(ch.hi[a], s0 + t.m[a] + t.k_ext[a] - 1);
+                }
+                ch.P[a] = fft_size_at_least(ch.hi[a] - ch.lo[a], a == 1, op->sw.mixed_last, op->sw.pow2_only);
+            }
+            if (ch.P[0] > 2048 || ch.P[1] > 4096) return 1e300;
+            if (!op->sw.chain_grow && j - i > 1) {  // no larger FFT than the members' own
+                for (int a = 0; a < 2; ++a) {
+                    int64_t own = 0;
+                    for (size_t q = i; q < j; ++q) own = std::max(own, local_P(ks[q], a));
+                    if (ch.P[a] > own) return 1e300;
+                }
+            }
+            const double W = (double)(ch.P[1] / 2 + 1);
+            const double rows = (double)std::max<int64_t>(
+                0, std::min<int64_t>(ch.hi[0], op->dom_lo[0] + op->n[0]) - std::max<int64_t>(ch.lo[0], op->dom_lo[0]));
+            const double P0 = (double)ch.P[0];
+            return W * (double)(j - i + 1) * P0 * std::log2(P0) + op->sw.chain_beta * rows * W;
+        };
+        const size_t max_len = 8;
+        for (auto& kv : clusters) {
+            std::vector<int> ks = kv.second;
+            std::stable_sort(ks.begin(), ks.end(), [&](int x, int y) {
+                return op->terms[x].x_lo[0] + op->terms[x].k_lo[0] < op->terms[y].x_lo[0] + op->terms[y].k_lo[0];
+            });
+            const size_t n = ks.size();
+            std::vector<double> dp(n + 1, 1e300);
+            std::vector<size_t> from(n + 1, 0);
+            dp[0] = 0.0;
+            Ch ch;
+            for (size_t j = 1; j <= n; ++j)
+                for (size_t i = j > max_len ? j - max_len : 0; i < j; ++i) {
+                    const double c = dp[i] + eval(ks, i, j, ch);
+                    if (c < dp[j]) {
+                        dp[j] = c;
+                        from[j] = i;
+                    }
+                }
+            std::vector<std::pair<size_t, size_t>> parts;
+            for (size_t j = n; j > 0; j = from[j]) parts.emplace_back(from[j], j);
+            std::reverse(parts.begin(), parts.end());
+            for (auto [i, j] : parts) {
+                eval(ks, i, j, ch);
+                TermDesc d{};
+                d.f_off = d.f_vst = d.a_off = -1;
+                for (int a = 0; a < 2; ++a) {
+                    const int64_t full = ch.hi[a] - ch.lo[a];
+                    d.s[a] = ch.lo[a];
+                    const int64_t lo = std::max<int64_t>(0, op->dom_lo[a] - d.s[a]);
+                    const int64_t hi = std::min<int64_t>(full - 1, op->dom_lo[a] + op->n[a] - 1 - d.s[a]);
+                    d.o_lo[a] = (int32_t)lo;
+                    d.o_cnt[a] = (int32_t)std::max<int64_t>(0, hi - lo + 1);
+                }
+                d.m[1] = (int32_t)(ch.hi[1] - ch.lo[1]);  // axis-1 support (the gather's bundle check)
+                d.k_ext[1] = 1;
+                d.o_lo[2] = 0;
+                d.o_cnt[2] = 1;
+                const int cid = (int)op->chains.size();
+                op->chains.push_back(d);
+                op->chain_members.emplace_back(ks.begin() + i, ks.begin() + j);
+                for (size_t q = i; q < j; ++q) {
+                    TermDesc& t = op->terms[ks[q]];
+                    term_chain[ks[q]] = cid;
+                    for (int a = 0; a < 2; ++a) {
+                        t.s[a] = d.s[a];
+                        t.o_lo[a] = d.o_lo[a];
+                        t.o_cnt[a] = d.o_cnt[a];
+                        chainP[ks[q]][a] = ch.P[a];
+                    }
+                }
+            }
+        }
+    }
     // global pseudo term
     {
         TermDesc& gd = op->gdesc;
@@ -758,6 +886,13 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
         }
         op->groups[it->second].terms.push_back(k);
         op->classes[cid[key[D - 1]]].terms.push_back(k);
+    }
+    for (size_t ci = 0; ci < op->chains.size(); ++ci) {  // a chain's members share one FFT shape
+        const int k0 = op->chain_members[ci][0];
+        std::vector<int> key(3, 1);
+        for (int a = 0; a < D; ++a) key[a] = (int)local_P(k0, a);
+        op->groups[gid.at(key)].chains.push_back((int)ci);
+        op->classes[cid.at(key[D - 1])].chains.push_back((int)ci);
     }
     // Row families (LOCAL apply).  A term whose weight factors exactly as w_k[u] = A_k(u_lead) *
     // c(u_last) (tensor-product tents, pc_operator.cpp:221-248) has last-axis row transforms
@@ -905,6 +1040,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             const TermDesc& f = op->fams[fi];
             s_sum += (D == 2 ? (int64_t)f.m[0] : (int64_t)f.m[0] * f.m[1]) * c.W;
         }
+        for (int ci : c.chains) t_sum += (int64_t)op->chains[ci].o_cnt[0] * c.W;
         for (int gi : c.groups) c.P0max = std::max(c.P0max, op->groups[gi].P[0]);
         if (mode == PCB_MODE_GLOBAL) {
             const int64_t plane = D == 2 ? c.W : (int64_t)op->gdesc.P1 * c.W;
@@ -942,6 +1078,12 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
                 to += reg * vb;
             }
         }
+        for (int ci : c.chains) {  // chain T regions after the term regions (2-D)
+            TermDesc& ch = op->chains[ci];
+            ch.t_pool = to;
+            ch.t_vst = (int64_t)ch.o_cnt[0] * c.W;
+            to += ch.t_vst * vb;
+        }
         for (int fi : c.fams) {  // family rows after the term regions
             TermDesc& f = op->fams[fi];
             f.s_pool = so;
@@ -977,6 +1119,19 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     op->w_pool.upload(wpool);
     op->phi_pool.upload(ppool);
     op->d_fams.upload(op->fams.empty() ? std::vector<TermDesc>(1) : op->fams);
+    {
+        std::vector<int32_t> cp(1, 0), ct;
+        for (const auto& mem : op->chain_members) {
+            ct.insert(ct.end(), mem.begin(), mem.end());
+            cp.push_back((int32_t)ct.size());
+        }
+        if (ct.empty()) ct.push_back(0);
+        op->d_chains.upload(op->chains.empty() ? std::vector<TermDesc>(1) : op->chains);
+        op->chain_ptr.upload(cp);
+        op->chain_terms.upload(ct);
+        for (Group& g : op->groups)
+            if (!g.chains.empty()) g.chain_slots.upload(std::vector<int32_t>(g.chains.begin(), g.chains.end()));
+    }
     op->a_pool.upload(apool.empty() ? std::vector<double>(1, 0.0) : apool);
     for (Group& g : op->groups) g.slots.upload(std::vector<int32_t>(g.terms.begin(), g.terms.end()));
     // 1 / prod P per term (its group's FFT size); the last slot serves the global pseudo term
@@ -1060,6 +1215,10 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     in.flops_per_vector = mode == PCB_MODE_GLOBAL ? g_fl : l_fl;
     in.launches_per_batch = (int)(2 * op->classes.size() + op->groups.size() * (D == 3 ? 3 : 1));
     in.n_row_families = (int32_t)op->fams.size();
+    in.n_column_chains = (int32_t)op->chains.size();
+    in.n_chained_terms = 0;
+    for (const auto& mem : op->chain_members)
+        if (mem.size() > 1) in.n_chained_terms += (int32_t)mem.size();
     // per-kernel compulsory bytes and nominal flops per vector (apply)
     for (int i = 0; i < 4; ++i) in.kernel_bytes[i] = in.kernel_flops[i] = 0.0;
     for (const Class& c : op->classes)
@@ -1088,13 +1247,21 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
                     in.kernel_bytes[1] += 2.0 * t.m[0] * P1 * Nc * 16.0;
                     in.kernel_flops[1] += t.m[0] * Nc * fft_flops_c(P1) + (gl ? 0.0 : t.o_cnt[0] * Nc * fft_flops_c(P1));
                 }
+                const bool chained = term_chain[k] >= 0;  // (T out, inverse, gather: per chain below)
                 in.kernel_bytes[2] += (t.m[0] * lines_cols + P0 * lines_cols) * 16.0 +  // S in, spectrum
-                                      (gl ? 0.0 : t.o_cnt[0] * lines_cols * 16.0);      // T out (local)
-                in.kernel_flops[2] += lines_cols * (fft_flops_c(P0) * (gl ? 1.0 : 2.0) + 8.0 * P0);
-                if (!gl) {
+                                      (gl || chained ? 0.0 : t.o_cnt[0] * lines_cols * 16.0);  // T out (local)
+                in.kernel_flops[2] += lines_cols * (fft_flops_c(P0) * (gl || chained ? 1.0 : 2.0) + 8.0 * P0);
+                if (!gl && !chained) {
                     in.kernel_bytes[3] += olead * (Nc * 16.0 + t.o_cnt[D - 1] * 8.0);  // T in, contributions
                     in.kernel_flops[3] += olead * fft_flops_r(Pl);
                 }
+            }
+            for (int ci : g.chains) {
+                const TermDesc& ch = op->chains[ci];
+                in.kernel_bytes[2] += ch.o_cnt[0] * lines_cols * 16.0;
+                in.kernel_flops[2] += lines_cols * fft_flops_c(P0);
+                in.kernel_bytes[3] += (double)ch.o_cnt[0] * (Nc * 16.0 + ch.o_cnt[1] * 8.0);
+                in.kernel_flops[3] += (double)ch.o_cnt[0] * fft_flops_r(Pl);
             }
             if (gl) {  // the single inverse per vector
                 const double lead = D == 2 ? op->n[0] : (double)op->n[0] * op->n[1];
@@ -1180,8 +1347,14 @@ void run_batch(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG
                 ga.global = global;
                 if (!adjoint) {
                     if (D == 3) launch(op, st, "mid(fwd apply)", [&] { return launch_mid(ga, MM_FWD_APPLY, st); });
-                    launch(op, st, global ? "cols(apply,global)" : "cols(apply,local)",
-                           [&] { return launch_cols(ga, global ? CM_APPLY_GLOBAL : CM_APPLY_LOCAL, st); });
+                    if (!g.chains.empty()) {
+                        ga.slots = g.chain_slots.p;
+                        ga.n_slots = (int)g.chains.size();
+                        launch(op, st, "cols(apply,chain)", [&] { return launch_cols(ga, CM_APPLY_CHAIN, st); });
+                    } else {
+                        launch(op, st, global ? "cols(apply,global)" : "cols(apply,local)",
+                               [&] { return launch_cols(ga, global ? CM_APPLY_GLOBAL : CM_APPLY_LOCAL, st); });
+                    }
                     if (D == 3) launch(op, st, "mid(inv apply)", [&] { return launch_mid(ga, MM_INV_APPLY, st); });
                 } else {
                     if (D == 3) launch(op, st, "mid(fwd adjoint)", [&] { return launch_mid(ga, MM_FWD_ADJ, st); });
@@ -1292,6 +1465,9 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
         op->sw.bundle = dim == 2;
         if (const char* e = getenv("PCB_BUNDLE")) op->sw.bundle = atoi(e) != 0;
         if (const char* e = getenv("PCB_FAMILIES")) op->sw.families = atoi(e) != 0;
+        if (const char* e = getenv("PCB_CHAINS")) op->sw.chains = atoi(e) != 0;
+        if (const char* e = getenv("PCB_CHAIN_BETA")) op->sw.chain_beta = atof(e);
+        if (const char* e = getenv("PCB_CHAIN_GROW")) op->sw.chain_grow = atoi(e) != 0;
 
         PCB_CK(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
 

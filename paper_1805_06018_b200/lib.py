@@ -45,7 +45,8 @@ class Info(ctypes.Structure):
     _fields_ = [("dim", i32), ("rank", i32), ("rank_active", i32), ("mode", i32), ("n_groups", i32),
                 ("fft_size", i32 * 3), ("n_points", i64), ("spectra_bytes", i64), ("device_bytes", i64),
                 ("bytes_per_vector", dbl), ("flops_per_vector", dbl), ("launches_per_batch", i32),
-                ("n_row_families", i32), ("kernel_bytes", dbl * 4), ("kernel_flops", dbl * 4)]
+                ("n_row_families", i32), ("kernel_bytes", dbl * 4), ("kernel_flops", dbl * 4),
+                ("n_column_chains", i32), ("n_chained_terms", i32)]
 
     def as_dict(self) -> dict:
         return {"dim": self.dim, "rank": self.rank, "rank_active": self.rank_active,
@@ -54,6 +55,7 @@ class Info(ctypes.Structure):
                 "spectra_bytes": self.spectra_bytes, "device_bytes": self.device_bytes,
                 "bytes_per_vector": self.bytes_per_vector, "flops_per_vector": self.flops_per_vector,
                 "launches_per_batch": self.launches_per_batch, "n_row_families": self.n_row_families,
+                "n_column_chains": self.n_column_chains, "n_chained_terms": self.n_chained_terms,
                 "kernel_bytes": dict(zip(KERNEL_FAMILIES, list(self.kernel_bytes))),
                 "kernel_flops": dict(zip(KERNEL_FAMILIES, list(self.kernel_flops)))}
 
