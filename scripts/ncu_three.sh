@@ -7,5 +7,5 @@ mkdir -p gpurun_out
 $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
     -k "regex:k_rows_inv_b<.int.128, .int.4>|k_cols<.int.256, .int.4, .int.1>|k_rows_fwd<.int.128, .int.4, .int.0>" \
-    -s 15 -c 5 -o gpurun_out/$TAG $CMD > gpurun_out/ncu_three.log 2>&1
+    -s 15 -c ${NCU_C:-5} -o gpurun_out/$TAG $CMD > gpurun_out/ncu_three.log 2>&1
 echo "ncu rc=$?"; tail -3 gpurun_out/ncu_three.log; ls -la gpurun_out/$TAG.ncu-rep
