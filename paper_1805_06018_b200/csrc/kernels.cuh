@@ -38,7 +38,8 @@ struct TermDesc {
     int32_t P1;        // axis-1 FFT size of the term (3-D plane stride); 1 in 2-D.  A family
                        // descriptor (rows_fwd item) holds its lead-axis-1 line count here
     int32_t wrow0;     // 1: one weight row (w_off) serves every line (family descriptors)
-    int32_t pad_;
+    int32_t cols_f;    // 1: the axis-0 (cols) pass loads rows f_off (+ f_vst per vector) x a_pool[a_off]
+                       // (2-D row families; 3-D plane families) instead of the term's S region
 };
 
 // rows_inv gather list entry: one C2R line of T contributing to one output line.

@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
     // apply input of term td, vector vec: its S rows, or (2-D family term) the family's shared rows
     // scaled by A_k(row).  All row and factor loads are issued before the first multiply.
     auto load_apply = [&](const TermDesc& td, int vec, double2* v) {
-        const bool fam = a.D == 2 && td.a_off >= 0;
+        const bool fam = td.cols_f != 0;
         double sc[R];
         if (fam) {
             const double* av = a.a_pool + td.a_off;
@@ -390,7 +390,26 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
         const int vec = item % nvec;
         const double2* S_item = MODE == CM_SPEC ? a.S + (int64_t)item * a.S_stride : a.S + td.s_pool + vec * td.s_vst;
         if (MODE == CM_SPEC) load_in(S_item, 0, P0, v);
-        else if (MODE == CM_APPLY_LOCAL) load_apply(td, vec, v);
+        else if (MODE == CM_APPLY_LOCAL) {
+            // family term: the shared rows scaled by its lead factor (all loads before the multiply)
+            const bool fam = td.cols_f != 0;
+            double sc[R];
+            if (fam) {
+                const double* av = a.a_pool + td.a_off;
+#pragma unroll
+                for (int b = 0; b < R / RF; ++b)
+#pragma unroll
+                    for (int r = 0; r < RF; ++r) {
+                        const int p = FirstPos<P0>::pos(tl, b, r);
+                        sc[b * RF + r] = p < td.m[0] ? __ldg(&av[p]) : 0.0;
+                    }
+            }
+            load_in(fam ? a.S + td.f_off + vec * td.f_vst : S_item, 0, td.m[0], v);
+            if (fam) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[r] = cscale(v[r], sc[r]);
+            }
+        }
         else load_in(S_item, td.o_lo[0], td.o_cnt[0], v);
         fft_fwd_order<P0, -1, NL, PSH<NL>>(v, buf, l, tl, tw0);
         double2* spec = a.spec_pool + td.spec_off + tile_off;

@@ -118,6 +118,7 @@ struct PlanSwitches {
     // 10-17% faster but the chained column pass loses more (one S-load latency per member per CTA
     // without an inverse FFT to hide it), net -1..-2%; off by default, kept tested.
     bool chains = false;
+    bool plane_families = true;  // PCB_PLANE_FAMILIES=0: per-term mid forward pass in 3-D
     double chain_beta = 24.0;  // PCB_CHAIN_BETA: modelled cost of one T row element, in column-FFT units
     bool chain_grow = false;   // PCB_CHAIN_GROW=1: a chain may use a larger FFT than its members' own
 };
@@ -181,6 +182,13 @@ struct Class {
     std::vector<int> chains;  // column chains of the class: the apply gather reads their T rows
     DevBuf<int32_t> fam_slots;
     int fam_lines = 1;      // max rows_fwd lines per family
+    // 3-D plane families: the axis-1 (mid) forward pass runs over these, one launch per P1
+    struct PfSet {
+        int P1 = 0, planes = 1;
+        std::vector<int> ids;  // indices into pcb_op::pfams
+        DevBuf<int32_t> slots;
+    };
+    std::vector<PfSet> pfsets;
 };
 
 std::atomic<long long> g_launches{0};
@@ -207,6 +215,8 @@ struct pcb_op {
     pcb::TermDesc gdesc{};
     pcb::DevBuf<pcb::TermDesc> d_terms, d_gdesc, d_fams;
     std::vector<pcb::TermDesc> fams;  // row-family descriptors (rows_fwd items of family classes)
+    std::vector<pcb::TermDesc> pfams; // 3-D plane-family descriptors (mid forward items)
+    pcb::DevBuf<pcb::TermDesc> d_pfams;
     // column chains: output descriptor (s, o_lo/o_cnt, T region; m[ax] = axis-1 support) + members
     std::vector<pcb::TermDesc> chains;
     std::vector<std::vector<int>> chain_members;
@@ -904,6 +914,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
         t.f_off = t.f_vst = t.a_off = -1;
         t.f_ps = 0;
         t.wrow0 = 0;
+        t.cols_f = 0;
     }
     std::vector<double> apool;
     std::vector<int> term_fam(r, -1);
@@ -986,6 +997,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
                 wpool.insert(wpool.end(), cf[members[f][0]].begin(), cf[members[f][0]].end());
                 for (int i : members[f]) {
                     TermDesc& t = op->terms[c.terms[i]];
+                    t.cols_f = D == 2 ? 1 : 0;  // 3-D: the mid pass applies A_k (or a plane family, below)
                     t.a_off = (int64_t)apool.size();
                     apool.insert(apool.end(), A[i].begin(), A[i].end());
                     term_fam[c.terms[i]] = (int)op->fams.size();
@@ -996,6 +1008,108 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             }
         }
     }
+
+    // Plane families (3-D LOCAL apply).  When a row-family term's lead factor factors again,
+    // A_k(x0, x1) = a_k(x0) * b(x1), its axis-1 transforms are a_k(x0) * FFT_1(b * rows of its row
+    // family).  Terms of one row family with the same axis-1 window, factor b (bitwise) and axis-1
+    // FFT size share those transforms over the union of their x0 ranges; the cols pass then
+    // applies a_k(x0) as it loads each plane.
+    std::vector<int> term_pf(r, -1);
+    if (D == 3 && op->sw.plane_families)
+        for (Class& c : op->classes) {
+            if (c.fams.empty()) continue;
+            std::vector<std::vector<double>> av(c.terms.size()), bv(c.terms.size());
+            bool ok = true;
+            for (size_t i = 0; i < c.terms.size() && ok; ++i) {
+                const TermDesc& t = op->terms[c.terms[i]];
+                const int64_t m0 = t.m[0], m1 = t.m[1];
+                const double* A = apool.data() + t.a_off;
+                int64_t piv = -1;
+                double pv = 0.0;
+                for (int64_t j = 0; j < m0 * m1; ++j)
+                    if (std::fabs(A[j]) > pv) {
+                        pv = std::fabs(A[j]);
+                        piv = j;
+                    }
+                if (piv < 0) {
+                    ok = false;
+                    break;
+                }
+                const int64_t p0 = piv / m1, q0 = piv % m1;
+                bv[i].assign(A + p0 * m1, A + p0 * m1 + m1);
+                av[i].resize(m0);
+                for (int64_t x = 0; x < m0; ++x) av[i][x] = A[x * m1 + q0] / A[piv];
+                for (int64_t x = 0; x < m0 && ok; ++x)
+                    for (int64_t y = 0; y < m1; ++y) {
+                        const double ref = A[x * m1 + y];
+                        if (std::fabs(av[i][x] * bv[i][y] - ref) > 4.0 * DBL_EPSILON * std::fabs(ref)) {
+                            ok = false;
+                            break;
+                        }
+                    }
+            }
+            if (!ok) continue;
+            std::map<std::tuple<int, int64_t, int32_t, int64_t, std::vector<double>>, int> pid;
+            std::vector<std::vector<int>> members;
+            for (size_t i = 0; i < c.terms.size(); ++i) {
+                const int k = c.terms[i];
+                const TermDesc& t = op->terms[k];
+                auto key = std::make_tuple(term_fam[k], t.x_lo[1], t.m[1], local_P(k, 1), bv[i]);
+                auto it = pid.find(key);
+                if (it == pid.end()) {
+                    it = pid.emplace(key, (int)members.size()).first;
+                    members.emplace_back();
+                }
+                members[it->second].push_back((int)i);
+            }
+            int64_t planes_terms = 0, planes_pf = 0;
+            std::vector<TermDesc> pd(members.size());
+            for (size_t f = 0; f < members.size(); ++f) {
+                const TermDesc& t0 = op->terms[c.terms[members[f][0]]];
+                TermDesc& d = pd[f];
+                d = TermDesc{};
+                int64_t lo = INT64_MAX, hi = INT64_MIN;
+                for (int i : members[f]) {
+                    const TermDesc& t = op->terms[c.terms[i]];
+                    lo = std::min<int64_t>(lo, t.x_lo[0]);
+                    hi = std::max<int64_t>(hi, t.x_lo[0] + t.m[0]);
+                    planes_terms += t.m[0];
+                }
+                d.x_lo[0] = lo;
+                d.m[0] = (int32_t)(hi - lo);
+                for (int a = 1; a < 3; ++a) {
+                    d.x_lo[a] = t0.x_lo[a];
+                    d.m[a] = t0.m[a];
+                }
+                d.P1 = (int32_t)local_P(c.terms[members[f][0]], 1);
+                d.f_off = d.f_vst = -1;
+                planes_pf += d.m[0];
+            }
+            if (members.size() == c.terms.size() || (double)planes_terms < 1.2 * (double)planes_pf) continue;
+            for (size_t f = 0; f < members.size(); ++f) {
+                TermDesc& d = pd[f];
+                d.a_off = (int64_t)apool.size();  // b(x1) for every plane of the union
+                for (int x = 0; x < d.m[0]; ++x)
+                    apool.insert(apool.end(), bv[members[f][0]].begin(), bv[members[f][0]].end());
+                const int id = (int)op->pfams.size();
+                for (int i : members[f]) {
+                    TermDesc& t = op->terms[c.terms[i]];
+                    t.a_off = (int64_t)apool.size();  // a_k(x0), applied by the cols pass
+                    apool.insert(apool.end(), av[i].begin(), av[i].end());
+                    t.cols_f = 1;
+                    term_pf[c.terms[i]] = id;
+                }
+                auto ps = std::find_if(c.pfsets.begin(), c.pfsets.end(), [&](const Class::PfSet& q) { return q.P1 == d.P1; });
+                if (ps == c.pfsets.end()) {
+                    c.pfsets.emplace_back();
+                    ps = c.pfsets.end() - 1;
+                    ps->P1 = d.P1;
+                }
+                ps->ids.push_back(id);
+                ps->planes = std::max(ps->planes, (int)d.m[0]);
+                op->pfams.push_back(d);
+            }
+        }
 
     // layout: spectra per group; scratch regions per term (pools reused class by class)
     int64_t spec_total = 0;
@@ -1041,6 +1155,8 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             s_sum += (D == 2 ? (int64_t)f.m[0] : (int64_t)f.m[0] * f.m[1]) * c.W;
         }
         for (int ci : c.chains) t_sum += (int64_t)op->chains[ci].o_cnt[0] * c.W;
+        for (const Class::PfSet& ps : c.pfsets)
+            for (int id : ps.ids) s_sum += (int64_t)op->pfams[id].m[0] * op->pfams[id].P1 * c.W;
         for (int gi : c.groups) c.P0max = std::max(c.P0max, op->groups[gi].P[0]);
         if (mode == PCB_MODE_GLOBAL) {
             const int64_t plane = D == 2 ? c.W : (int64_t)op->gdesc.P1 * c.W;
@@ -1100,6 +1216,26 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             t.f_vst = f.s_vst;
             t.f_ps = D == 3 ? f.m[1] : 0;
         }
+        for (const Class::PfSet& ps : c.pfsets)  // plane families: their mid output regions
+            for (int id : ps.ids) {
+                TermDesc& d = op->pfams[id];
+                d.s_pool = so;
+                d.s_vst = (int64_t)d.m[0] * d.P1 * c.W;
+                so += d.s_vst * vb;
+            }
+        for (int k : c.terms) {
+            if (term_pf[k] < 0) continue;
+            TermDesc& t = op->terms[k];
+            TermDesc& d = op->pfams[term_pf[k]];
+            if (d.f_off < 0) {  // the plane family reads its row family's rows
+                const TermDesc& f = op->fams[term_fam[k]];
+                d.f_off = f.s_pool + ((d.x_lo[0] - f.x_lo[0]) * f.m[1] + (d.x_lo[1] - f.x_lo[1])) * c.W;
+                d.f_vst = f.s_vst;
+                d.f_ps = f.m[1];
+            }
+            t.f_off = d.s_pool + (t.x_lo[0] - d.x_lo[0]) * (int64_t)d.P1 * c.W;
+            t.f_vst = d.s_vst;
+        }
     }
     if (mode == PCB_MODE_GLOBAL) {
         TermDesc& g = op->gdesc;
@@ -1119,6 +1255,9 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     op->w_pool.upload(wpool);
     op->phi_pool.upload(ppool);
     op->d_fams.upload(op->fams.empty() ? std::vector<TermDesc>(1) : op->fams);
+    op->d_pfams.upload(op->pfams.empty() ? std::vector<TermDesc>(1) : op->pfams);
+    for (Class& c : op->classes)
+        for (Class::PfSet& ps : c.pfsets) ps.slots.upload(std::vector<int32_t>(ps.ids.begin(), ps.ids.end()));
     {
         std::vector<int32_t> cp(1, 0), ct;
         for (const auto& mem : op->chain_members) {
@@ -1336,6 +1475,16 @@ void run_batch(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG
                 launch(op, st, adjoint ? "rows_fwd(adjoint)" : "rows_fwd(apply)",
                        [&] { return launch_rows_fwd(a, adjoint ? RF_ADJ : RF_APPLY, st); });
             }
+            if (!adjoint)
+                for (const Class::PfSet& ps : c.pfsets) {  // 3-D plane families: shared mid forward
+                    PassArgs pa = a;
+                    pa.terms = op->d_pfams.p;
+                    pa.slots = ps.slots.p;
+                    pa.n_slots = (int)ps.ids.size();
+                    pa.P[0] = ps.planes;
+                    pa.P[1] = ps.P1;
+                    launch(op, st, "mid(fwd apply)", [&] { return launch_mid(pa, MM_FWD_APPLY, st); });
+                }
             for (int gi : c.groups) {
                 const Group& g = op->groups[gi];
                 PassArgs ga = group_args(op, g);
@@ -1346,7 +1495,8 @@ void run_batch(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG
                 ga.n_slots = (int)g.terms.size();
                 ga.global = global;
                 if (!adjoint) {
-                    if (D == 3) launch(op, st, "mid(fwd apply)", [&] { return launch_mid(ga, MM_FWD_APPLY, st); });
+                    if (D == 3 && c.pfsets.empty())
+                        launch(op, st, "mid(fwd apply)", [&] { return launch_mid(ga, MM_FWD_APPLY, st); });
                     if (!g.chains.empty()) {
                         ga.slots = g.chain_slots.p;
                         ga.n_slots = (int)g.chains.size();
@@ -1466,6 +1616,7 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
         if (const char* e = getenv("PCB_BUNDLE")) op->sw.bundle = atoi(e) != 0;
         if (const char* e = getenv("PCB_FAMILIES")) op->sw.families = atoi(e) != 0;
         if (const char* e = getenv("PCB_CHAINS")) op->sw.chains = atoi(e) != 0;
+        if (const char* e = getenv("PCB_PLANE_FAMILIES")) op->sw.plane_families = atoi(e) != 0;
         if (const char* e = getenv("PCB_CHAIN_BETA")) op->sw.chain_beta = atof(e);
         if (const char* e = getenv("PCB_CHAIN_GROW")) op->sw.chain_grow = atoi(e) != 0;
 

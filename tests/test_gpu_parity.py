@@ -431,3 +431,22 @@ def test_column_chains_match_per_term_inverse(gpu, name, monkeypatch):
         for i in range(2):
             assert rel(b[i], ref.apply(F[i])) <= APPLY_TOL
             assert rel(ba[i], ref.apply_adjoint(F[i])) <= APPLY_TOL
+
+
+@pytest.mark.parametrize("name", ["c4", "small3d"])
+def test_plane_families_match_per_term_mid(gpu, name, monkeypatch):
+    """3-D plane families (terms of one row family sharing the axis-1 factor share the axis-1
+    forward transforms; the cols pass applies a_k(x0)) give the same operator as per-term mid
+    passes (PCB_PLANE_FAMILIES=0) and as the oracle."""
+    inp = inputs.make_config(name) if name.startswith("c") else inputs.small_lattice(**SMALL[name])
+    F = normal_vectors(12, 2, inp.n_points)
+    monkeypatch.setenv("PCB_PLANE_FAMILIES", "0")
+    a = ProductConvolutionOperator.from_inputs(inp, mode="local").apply_batch(F)
+    monkeypatch.setenv("PCB_PLANE_FAMILIES", "1")
+    b = ProductConvolutionOperator.from_inputs(inp, mode="local").apply_batch(F)
+    for i in range(2):
+        assert rel(b[i], a[i]) <= 1e-14
+    if name.startswith("small"):
+        ref = O.PCOperator.from_inputs(inp)
+        for i in range(2):
+            assert rel(b[i], ref.apply(F[i])) <= APPLY_TOL
