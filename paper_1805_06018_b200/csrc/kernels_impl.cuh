@@ -37,6 +37,12 @@
 #ifndef PCB_BUNDLE_DB
 #define PCB_BUNDLE_DB 1  // 1: double-buffered member staging (c3 +1.7% over MB = 2 single-buffered)
 #endif
+#ifndef PCB_BUNDLE_XPF
+#define PCB_BUNDLE_XPF 1  // 1: next batch's headers and first members issued before this batch's C2R
+#endif
+#if PCB_BUNDLE_XPF && !PCB_BUNDLE_DB
+#error "PCB_BUNDLE_XPF needs PCB_BUNDLE_DB"
+#endif
 #ifndef PCB_ROWS_MINB_MIXED
 #define PCB_ROWS_MINB_MIXED 1
 #endif
@@ -674,6 +680,114 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
     const int tl = threadIdx.x / NL;
     for (int i = ulo + threadIdx.x; i < uhi; i += NT) acc[i - ulo] = 0.0;
 
+#if PCB_BUNDLE_XPF
+    // Cross-batch prefetch: the next batch's bundle headers and first members are issued before
+    // this batch's C2R, so the transform hides their load latency (stage buffer 0 is free then).
+    GatherEntry* metaN = meta + NL;
+    auto issue = [&](const BundleMember* mb, int cnt, int m0, int buf_i) {
+#pragma unroll
+        for (int j = 0; j < MB; ++j)
+            if (m0 + j < cnt) {
+                const double2* src = a.T + mb[m0 + j].t_off + vec * mb[m0 + j].t_vst;
+                double2* dst = stg + ((buf_i * NL + l) * MB + j) * SL;
+                for (int i = tl; i < SL; i += TPL) cp_async16(&dst[i], src + i);
+            }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    auto lane_of = [&](const GatherEntry* mt, int nb, int& cnt) {
+        cnt = l < nb ? mt[l].pad_ : 0;
+        return a.members + (l < nb ? mt[l].t_off : 0);
+    };
+    if (b_beg < b_end) {
+        const int nb = (int)((b_end - b_beg) < NL ? (b_end - b_beg) : NL);
+        if (threadIdx.x < nb) meta[threadIdx.x] = a.entries[b_beg + threadIdx.x];
+        __syncthreads();
+        int cnt;
+        const BundleMember* mb = lane_of(meta, nb, cnt);
+        issue(mb, cnt, 0, 0);
+    }
+    for (int64_t b0 = b_beg; b0 < b_end; b0 += NL) {
+        const int nb = (int)((b_end - b0) < NL ? (b_end - b0) : NL);
+        int mmax = 0;
+        for (int ll = 0; ll < nb; ++ll) mmax = max(mmax, meta[ll].pad_);
+        int cnt;
+        const BundleMember* mb = lane_of(meta, nb, cnt);
+        double2 zk[R], zn[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) zk[r] = zn[r] = czero();
+        int cur = 0;  // members [0, MB) are already in flight in buffer 0
+        for (int m0 = 0; m0 < mmax; m0 += MB) {
+            if (m0 + MB < mmax) {
+                issue(mb, cnt, m0 + MB, cur ^ 1);
+                asm volatile("cp.async.wait_group 1;\n" ::);
+            } else {
+                asm volatile("cp.async.wait_group 0;\n" ::);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < MB; ++j)
+                if (m0 + j < cnt) {
+                    const double2* x = stg + ((cur * NL + l) * MB + j) * SL;
+                    const double sc = mb[m0 + j].scale;
+                    const int dl = mb[m0 + j].delta;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int k = tl + r * TPL;
+                        double2 xk = x[k], xn = x[N - k];
+                        if (dl != 0) {
+                            xk = cmul(xk, __ldg(&twP[(k * dl) % P]));
+                            xn = cmul(xn, __ldg(&twP[((N - k) * dl) % P]));
+                        }
+                        zk[r] = make_double2(fma(sc, xk.x, zk[r].x), fma(sc, xk.y, zk[r].y));
+                        zn[r] = make_double2(fma(sc, xn.x, zn[r].x), fma(sc, xn.y, zn[r].y));
+                    }
+                }
+            __syncthreads();  // stage buffer `cur` free
+            cur ^= 1;
+        }
+        if (mmax == 0) asm volatile("cp.async.wait_group 0;\n" ::);
+        __syncthreads();  // every thread is done with metaN (last read two batches ago)
+        const int64_t b1 = b0 + NL;
+        if (b1 < b_end) {
+            const int nb1 = (int)((b_end - b1) < NL ? (b_end - b1) : NL);
+            if (threadIdx.x < nb1) metaN[threadIdx.x] = a.entries[b1 + threadIdx.x];
+            __syncthreads();
+            int cnt1;
+            const BundleMember* mb1 = lane_of(metaN, nb1, cnt1);
+            issue(mb1, cnt1, 0, 0);
+        }
+        double2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int k = tl + r * TPL;
+            const double2 E = make_double2(zk[r].x + zn[r].x, zk[r].y - zn[r].y);   // Z[k] + conj Z[N-k]
+            const double2 Dd = make_double2(zk[r].x - zn[r].x, zk[r].y + zn[r].y);  // Z[k] - conj Z[N-k]
+            const double2 O = cmulc(Dd, __ldg(&twP[k]));                            // * exp(+2 pi i k / P)
+            v[r] = make_double2(E.x - O.y, E.y + O.x);                              // E + i O
+        }
+        fft_rev_order<N, +1, NL, PSH<NL>>(v, buf, l, tl, twtab<N>(a.tw));
+        __syncthreads();
+#pragma unroll
+        for (int bb = 0; bb < R / RL; ++bb)
+#pragma unroll
+            for (int r = 0; r < RL; ++r) {
+                const int p = LastPos<N>::pos(tl, bb, r);
+                xs[l * XS + 2 * p] = v[bb * RL + r].x;
+                xs[l * XS + 2 * p + 1] = v[bb * RL + r].y;
+            }
+        __syncthreads();
+        for (int ll = 0; ll < nb; ++ll) {
+            const int lo = meta[ll].lo, hi = meta[ll].hi;
+            const double* x = xs + ll * XS - meta[ll].sh;
+            int p = lo + (int)((threadIdx.x + NT - (unsigned)(lo % NT)) % NT);
+            for (; p < hi; p += NT) acc[p - ulo] += x[p];
+        }
+        __syncthreads();  // xs (the FFT buffer) and meta are free
+        GatherEntry* t = meta;
+        meta = metaN;
+        metaN = t;
+    }
+#else
     for (int64_t b0 = b_beg; b0 < b_end; b0 += NL) {
         const int nb = (int)((b_end - b0) < NL ? (b_end - b0) : NL);
         __syncthreads();  // previous batch finished with meta / xs
@@ -757,6 +871,7 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
             for (; p < hi; p += NT) acc[p - ulo] += x[p];
         }
     }
+#endif
     __syncthreads();
     double* g = a.out + (int64_t)vec * a.N + line * a.n[ax];
     for (int i = ulo + threadIdx.x; i < uhi; i += NT) g[i] = a.accumulate ? g[i] + acc[i - ulo] : acc[i - ulo];

@@ -43,7 +43,7 @@ cudaError_t rows_inv_b_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
                                                                           : (NL * (2 * N + 1) + 1) / 2;
     dim3 grid((unsigned)n_lines, (unsigned)a.B);
     const size_t smem = sizeof(double2) * (BUFW + (size_t)(1 + PCB_BUNDLE_DB) * NL * PCB_BUNDLE_MB * (N + 1)) +
-                        sizeof(double) * ((size_t)a.n[a.D - 1] + 1) + NL * sizeof(GatherEntry) + 16;
+                        sizeof(double) * ((size_t)a.n[a.D - 1] + 1) + (1 + PCB_BUNDLE_XPF) * NL * sizeof(GatherEntry) + 16;
     return launch_dyn(k_rows_inv_b<N, NL>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
 }
 
