@@ -1720,11 +1720,11 @@ static pcb_status apply_host_common(pcb_op* op, bool adjoint, int32_t B, const d
         op->st_in.ensure(cnt);
         op->st_out.ensure(cnt);
         // Sub-batches overlap H2D(j+1) and D2H(j-1) with the kernels of sub-batch j (PCIe is full duplex,
-        // ~55 GB/s per direction).  ~sub_mb MiB each; the first and the last are half size so the
+        // ~55 GB/s per direction).  ~sub_mb MiB each (geometric ramps at the ends measured no better); the first and the last are half size so the
         // unoverlapped fill (first H2D) and drain (last D2H) stay short.
         static const double sub_mb = [] {
             const char* e = std::getenv("PCB_SUB_MB");
-            return e ? std::max(1.0, std::atof(e)) : 64.0;
+            return e ? std::max(1.0, std::atof(e)) : 48.0;  // c3 sweep 16-64 MiB: 48 best (scripts/e2e_sweep.sh)
         }();
         const double vec_mb = (double)op->N * 8.0 / (1 << 20);
         const int per = (int)std::max(1.0, std::floor(sub_mb / vec_mb));
