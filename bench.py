@@ -163,6 +163,8 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
+    for _ in range(args.warmup):  # untimed samples (page-in, thread spin-up)
+        cpu_reference_sample(args.config, threads)
     vals = []
     for _ in range(max(1, args.steps)):
         cb = cpu_reference_sample(args.config, threads)
@@ -209,7 +211,10 @@ def main():
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    # PCB_BENCH_FORCE_DIST=1: run the process-group path (init, barriers, max-over-ranks
+    # all-reduces, the k-shard all-reduce) even at world size 1, to exercise it on one GPU
+    use_dist = world > 1 or os.environ.get("PCB_BENCH_FORCE_DIST") == "1"
+    if use_dist:
         dist.init_process_group("nccl", device_id=dev)
 
     cfg = args.config
@@ -242,7 +247,7 @@ def main():
 
     def step():
         op.apply_batch_dev(Bl, F.data_ptr(), G.data_ptr(), sptr)
-        if args.shard == "k" and world > 1:
+        if args.shard == "k" and use_dist:
             dist.all_reduce(G)
 
     for _ in range(args.warmup):
@@ -260,7 +265,7 @@ def main():
     time.sleep(0.3)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = lib.launch_count()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     for i in range(args.steps):
@@ -269,13 +274,13 @@ def main():
         step()
         ev[i][1].record(stream)
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     launches = lib.launch_count() - launches0
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = float(np.sum(step_ms))
-    if world > 1:
+    if use_dist:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -325,12 +330,12 @@ def main():
         b.record(stream)
         torch.cuda.synchronize()
         lib.check(rc)
-        if args.shard == "k" and world > 1:
+        if args.shard == "k" and use_dist:
             t = torch.from_numpy(Gn).to(dev)
             dist.all_reduce(t)
         e2e_ms.append(a.elapsed_time(b))
     e2e_total = float(np.sum(e2e_ms))
-    if world > 1:
+    if use_dist:
         t = torch.tensor([e2e_total], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
@@ -377,7 +382,7 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
 
