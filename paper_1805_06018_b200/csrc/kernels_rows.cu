@@ -42,8 +42,13 @@ cudaError_t rows_inv_b_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
     constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
                                                                           : (NL * (2 * N + 1) + 1) / 2;
     dim3 grid((unsigned)n_lines, (unsigned)a.B);
-    const size_t smem = sizeof(double2) * (BUFW + (size_t)(1 + PCB_BUNDLE_DB) * NL * PCB_BUNDLE_MB * (N + 1)) +
-                        sizeof(double) * ((size_t)a.n[a.D - 1] + 1) + (1 + PCB_BUNDLE_XPF) * NL * sizeof(GatherEntry) + 16;
+#if PCB_BUNDLE_XPF && PCB_BUNDLE_ALIAS
+    const size_t stage_words = (size_t)2 * NL * PCB_BUNDLE_MB * stage_stride_b<N, NL>();
+#else
+    const size_t stage_words = BUFW + (size_t)(1 + PCB_BUNDLE_DB) * NL * PCB_BUNDLE_MB * (N + 1);
+#endif
+    const size_t smem = sizeof(double2) * stage_words + sizeof(double) * ((size_t)a.n[a.D - 1] + 1) +
+                        (1 + PCB_BUNDLE_XPF) * NL * sizeof(GatherEntry) + 16;
     return launch_dyn(k_rows_inv_b<N, NL>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
 }
 
