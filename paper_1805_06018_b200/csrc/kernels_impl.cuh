@@ -40,6 +40,9 @@
 #ifndef PCB_BUNDLE_XPF
 #define PCB_BUNDLE_XPF 1  // 1: next batch's headers and first members issued before this batch's C2R
 #endif
+#ifndef PCB_RINV_ALIAS
+#define PCB_RINV_ALIAS 1  // per-entry gather: split straight into registers, stage doubles as FFT buffer
+#endif
 #ifndef PCB_BUNDLE_ALIAS
 #define PCB_BUNDLE_ALIAS 1  // with XPF: stage buffer 1 doubles as the FFT / xs buffer (smem per CTA)
 #endif
@@ -582,10 +585,22 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
     const int ax = a.D - 1;
     const int64_t line = a.line_id[aline];
     const int ulo = a.line_rng[2 * aline], uhi = a.line_rng[2 * aline + 1];
+#if PCB_RINV_ALIAS
+    // layout: stage [NL][SLS] (also the FFT exchange / xs buffer) | acc [n_last] | meta [NL].  The
+    // even/odd split reads the staged lines straight into the inverse FFT's registers, so the
+    // stage is free for the transform (one buffer less per CTA)
+    constexpr int SLS = stage_stride_b<N, NL>();
+    double2* stage = buf;
+    double2* fbuf = buf;
+    double* acc = reinterpret_cast<double*>(stage + NL * SLS);
+#else
     // layout: buf [BUFW] (FFT; reused as xs) | stage [NL][N+1] | acc [n_last] | meta [NL]
-    double* xs = reinterpret_cast<double*>(buf);
+    constexpr int SLS = N + 1;
+    double2* fbuf = buf;
     double2* stage = buf + BUFW;
     double* acc = reinterpret_cast<double*>(stage + NL * (N + 1));
+#endif
+    double* xs = reinterpret_cast<double*>(fbuf);
     GatherEntry* meta = reinterpret_cast<GatherEntry*>(acc + a.n[ax] + (a.n[ax] & 1));
     const int64_t e_beg = a.line_ptr[aline];
     const int64_t e_end = a.line_ptr[aline + 1];
@@ -602,10 +617,28 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
         for (int idx = threadIdx.x; idx < ne * (N + 1); idx += NT) {
             const int ll = idx / (N + 1);
             const int k = idx - ll * (N + 1);
-            cp_async16(&stage[idx], a.T + meta[ll].t_off + vec * meta[ll].t_vst + k);
+            cp_async16(&stage[ll * SLS + k], a.T + meta[ll].t_off + vec * meta[ll].t_vst + k);
         }
         cp_async_wait_all();
         __syncthreads();
+        double2 v[R];
+#if PCB_RINV_ALIAS
+#pragma unroll
+        for (int r = 0; r < R; ++r) {  // z[k], k = mid_pos(tl, r), of line l: the FFT's input registers
+            const int k = mid_pos<N>(tl, r);
+            double2 z = czero();
+            if (l < ne) {
+                const double2 xk = stage[l * SLS + k];
+                const double2 xn = stage[l * SLS + N - k];
+                const double2 E = make_double2(xk.x + xn.x, xk.y - xn.y);   // X[k] + conj X[N-k]
+                const double2 Dd = make_double2(xk.x - xn.x, xk.y + xn.y);  // X[k] - conj X[N-k]
+                const double2 O = cmulc(Dd, __ldg(&twP[k]));                // * exp(+2 pi i k / P)
+                z = make_double2(E.x - O.y, E.y + O.x);                     // E + i O
+            }
+            v[r] = z;
+        }
+        __syncthreads();  // the stage is read out: the transform may reuse it
+#else
         for (int idx = threadIdx.x; idx < NL * N; idx += NT) {
             const int ll = idx / N;
             const int k = idx - ll * N;
@@ -621,13 +654,13 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
             buf[sidx<NL, PSH<NL>>(k, ll)] = z;
         }
         __syncthreads();
-        double2 v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int pos = mid_pos<N>(tl, r);
             v[r] = buf[sidx<NL, PSH<NL>>(pos, l)];
         }
-        fft_rev_order<N, +1, NL, PSH<NL>>(v, buf, l, tl, twtab<N>(a.tw));
+#endif
+        fft_rev_order<N, +1, NL, PSH<NL>>(v, fbuf, l, tl, twtab<N>(a.tw));
         __syncthreads();
 #pragma unroll
         for (int bb = 0; bb < R / RL; ++bb)

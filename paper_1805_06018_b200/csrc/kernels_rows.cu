@@ -31,7 +31,12 @@ cudaError_t rows_inv_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
     constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
                                                                           : (NL * (2 * N + 1) + 1) / 2;
     dim3 grid((unsigned)n_lines, (unsigned)a.B);
-    const size_t smem = sizeof(double2) * (BUFW + NL * (N + 1)) + sizeof(double) * ((size_t)a.n[a.D - 1] + 1) +
+#if PCB_RINV_ALIAS
+    const size_t stage_words = (size_t)NL * stage_stride_b<N, NL>();
+#else
+    const size_t stage_words = BUFW + (size_t)NL * (N + 1);
+#endif
+    const size_t smem = sizeof(double2) * stage_words + sizeof(double) * ((size_t)a.n[a.D - 1] + 1) +
                         NL * sizeof(GatherEntry) + 16;
     return launch_dyn(k_rows_inv<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
 }
