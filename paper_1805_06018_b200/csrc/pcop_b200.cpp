@@ -119,6 +119,7 @@ struct PlanSwitches {
     // without an inverse FFT to hide it), net -1..-2%; off by default, kept tested.
     bool chains = false;
     bool plane_families = true;  // PCB_PLANE_FAMILIES=0: per-term mid forward pass in 3-D
+    bool graphs = true;          // PCB_GRAPHS=0: device-pointer applies launch kernel by kernel
     double chain_beta = 24.0;  // PCB_CHAIN_BETA: modelled cost of one T row element, in column-FFT units
     bool chain_grow = false;   // PCB_CHAIN_GROW=1: a chain may use a larger FFT than its members' own
 };
@@ -229,6 +230,17 @@ struct pcb_op {
     int vb = 1;                 // vectors per pass (scratch pools are sized for vb vectors)
     pcb::DevBuf<double2> S, T;  // scratch pools
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // host-buffer calls: copy streams
+    // device-pointer applies: one CUDA graph per (adjoint, B, F, G), replayed on op->stream
+    struct GraphRec {
+        bool adjoint;
+        int32_t B;
+        const double* F;
+        double* G;
+        cudaGraphExec_t exec;
+        long long launches;
+    };
+    std::vector<GraphRec> graphs;
+    cudaEvent_t ev_g[2] = {nullptr, nullptr};
     cudaEvent_t ev_io[8] = {};
     // entry gather
     int32_t bucket[3] = {1, 1, 1}, nb[3] = {1, 1, 1};
@@ -1617,6 +1629,7 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
         if (const char* e = getenv("PCB_FAMILIES")) op->sw.families = atoi(e) != 0;
         if (const char* e = getenv("PCB_CHAINS")) op->sw.chains = atoi(e) != 0;
         if (const char* e = getenv("PCB_PLANE_FAMILIES")) op->sw.plane_families = atoi(e) != 0;
+        if (const char* e = getenv("PCB_GRAPHS")) op->sw.graphs = atoi(e) != 0;
         if (const char* e = getenv("PCB_CHAIN_BETA")) op->sw.chain_beta = atof(e);
         if (const char* e = getenv("PCB_CHAIN_GROW")) op->sw.chain_grow = atoi(e) != 0;
 
@@ -1650,6 +1663,9 @@ PCB_API pcb_status pcb_destroy(pcb_op* op) {
         cudaEventDestroy(r.b);
     }
     for (auto e : op->ev_pool) cudaEventDestroy(e);
+    for (auto& g : op->graphs) cudaGraphExecDestroy(g.exec);
+    for (cudaEvent_t e : op->ev_g)
+        if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : op->ev_io)
         if (e) cudaEventDestroy(e);
     for (cudaStream_t s : {op->s_h2d, op->s_d2h})
@@ -1683,6 +1699,67 @@ PCB_API pcb_status pcb_get_info(const pcb_op* op, pcb_info* info) {
     return PCB_OK;
 }
 
+// Device-pointer apply: the launch sequence of run_batch (one per class and group: 17 kernels at
+// c3) is captured once per (adjoint, B, F, G) into a CUDA graph and replayed on the handle's
+// stream, ordered after / before the caller's stream by events.  Graphs are skipped while the
+// per-kernel profile is on and when the caller's stream is itself being captured; a capture
+// failure turns them off for the handle.
+static void run_dev(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (st) PCB_CK(cudaStreamIsCapturing(st, &cs));
+    if (!op->sw.graphs || op->prof || cs != cudaStreamCaptureStatusNone) {
+        run_batch(op, adjoint, B, dF, dG, st);
+        return;
+    }
+    if (!op->ev_g[0])
+        for (auto& e : op->ev_g) PCB_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    pcb_op::GraphRec* rec = nullptr;
+    for (auto& g : op->graphs)
+        if (g.adjoint == adjoint && g.B == B && g.F == dF && g.G == dG) rec = &g;
+    if (!rec) {
+        const long long l0 = g_launches.load();
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        bool ok = cudaStreamBeginCapture(op->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            try {
+                run_batch(op, adjoint, B, dF, dG, op->stream);
+            } catch (...) {
+                ok = false;
+            }
+            ok = cudaStreamEndCapture(op->stream, &graph) == cudaSuccess && ok;
+            ok = ok && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+            if (graph) cudaGraphDestroy(graph);
+        }
+        const long long captured = g_launches.load() - l0;
+        g_launches.fetch_sub(captured);  // counted when replayed
+        if (!ok) {
+            cudaGetLastError();
+            if (exec) cudaGraphExecDestroy(exec);
+            op->sw.graphs = false;
+            run_batch(op, adjoint, B, dF, dG, st);
+            return;
+        }
+        if (op->graphs.size() >= 32) {
+            cudaGraphExecDestroy(op->graphs.front().exec);
+            op->graphs.erase(op->graphs.begin());
+        }
+        op->graphs.push_back({adjoint, B, dF, dG, exec, captured});
+        rec = &op->graphs.back();
+    }
+    if (st == op->stream) {  // the host path's sub-batches
+        PCB_CK(cudaGraphLaunch(rec->exec, op->stream));
+        g_launches.fetch_add(rec->launches);
+        return;
+    }
+    PCB_CK(cudaEventRecord(op->ev_g[0], st));
+    PCB_CK(cudaStreamWaitEvent(op->stream, op->ev_g[0], 0));
+    PCB_CK(cudaGraphLaunch(rec->exec, op->stream));
+    g_launches.fetch_add(rec->launches);
+    PCB_CK(cudaEventRecord(op->ev_g[1], op->stream));
+    PCB_CK(cudaStreamWaitEvent(st, op->ev_g[1], 0));
+}
+
 static pcb_status apply_dev_common(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG, void* stream) {
     if (!op) {
         set_err("null handle");
@@ -1694,7 +1771,7 @@ static pcb_status apply_dev_common(pcb_op* op, bool adjoint, int32_t B, const do
         if (B == 0) return;
         if (!dF || !dG) fail(PCB_EINVAL, "null vector pointer");
         set_device(op);
-        run_batch(op, adjoint, B, dF, dG, (cudaStream_t)stream);
+        run_dev(op, adjoint, B, dF, dG, (cudaStream_t)stream);
     });
 }
 
@@ -1754,7 +1831,7 @@ static pcb_status apply_host_common(pcb_op* op, bool adjoint, int32_t B, const d
             PCB_CK(cudaMemcpyAsync(op->st_in.p + off, F + off, n * sizeof(double), cudaMemcpyHostToDevice, op->s_h2d));
             PCB_CK(cudaEventRecord(op->ev_io[2 * (j & 1)], op->s_h2d));
             PCB_CK(cudaStreamWaitEvent(op->stream, op->ev_io[2 * (j & 1)], 0));
-            run_batch(op, adjoint, b1 - b0, op->st_in.p + off, op->st_out.p + off, op->stream);
+            run_dev(op, adjoint, b1 - b0, op->st_in.p + off, op->st_out.p + off, op->stream);
             PCB_CK(cudaEventRecord(op->ev_io[2 * (j & 1) + 1], op->stream));
             PCB_CK(cudaStreamWaitEvent(op->s_d2h, op->ev_io[2 * (j & 1) + 1], 0));
             PCB_CK(cudaMemcpyAsync(G + off, op->st_out.p + off, n * sizeof(double), cudaMemcpyDeviceToHost, op->s_d2h));

@@ -450,3 +450,38 @@ def test_plane_families_match_per_term_mid(gpu, name, monkeypatch):
         ref = O.PCOperator.from_inputs(inp)
         for i in range(2):
             assert rel(b[i], ref.apply(F[i])) <= APPLY_TOL
+
+
+@pytest.mark.parametrize("name", ["c1", "small3d"])
+def test_graph_replay_matches_direct_launches(gpu, name, monkeypatch):
+    """Device-pointer applies replay a captured CUDA graph per (adjoint, B, F, G): bitwise equal to
+    kernel-by-kernel launches (PCB_GRAPHS=0), on repeated calls, new inputs in the same buffers,
+    other buffers, the adjoint, and on a side stream."""
+    import torch
+
+    inp = inputs.make_config(name) if name.startswith("c") else inputs.small_lattice(**SMALL[name])
+    F = torch.from_numpy(normal_vectors(3, 3, inp.n_points)).cuda()
+    s = torch.cuda.current_stream().cuda_stream
+    monkeypatch.setenv("PCB_GRAPHS", "0")
+    direct = ProductConvolutionOperator.from_inputs(inp, mode="local")
+    monkeypatch.setenv("PCB_GRAPHS", "1")
+    graph = ProductConvolutionOperator.from_inputs(inp, mode="local")
+    Gd, Gg = torch.empty_like(F), torch.empty_like(F)
+    for adjoint in (False, True):
+        direct.apply_batch_dev(3, F.data_ptr(), Gd.data_ptr(), s, adjoint=adjoint)
+        for _ in range(3):
+            Gg.zero_()
+            graph.apply_batch_dev(3, F.data_ptr(), Gg.data_ptr(), s, adjoint=adjoint)
+            torch.cuda.synchronize()
+            assert torch.equal(Gg, Gd)
+    F2 = F.flip(0).contiguous()
+    G2 = torch.empty_like(F)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        graph.apply_batch_dev(3, F2.data_ptr(), G2.data_ptr(), side.cuda_stream)
+        F.copy_(F2)  # same buffer, new inputs
+        graph.apply_batch_dev(3, F.data_ptr(), Gg.data_ptr(), side.cuda_stream)
+    torch.cuda.synchronize()
+    direct.apply_batch_dev(3, F2.data_ptr(), Gd.data_ptr(), s)
+    torch.cuda.synchronize()
+    assert torch.equal(G2, Gd) and torch.equal(Gg, Gd)
