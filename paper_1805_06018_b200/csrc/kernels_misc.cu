@@ -1,5 +1,7 @@
 // Entry / block gathers (K6), block apply (direct form), estimator reductions (K5).
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "fft.cuh"
 #include "kernels.cuh"
@@ -189,6 +191,184 @@ __global__ void k_zero(double* p, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = 0.0;
 }
 
+// K6 for dense blocks, tiled: one CTA per block (T x S, boxes of shape bs).  The terms that can
+// contribute are those listed in the buckets covering S; their weights on S and the window of
+// phi_k^E over the offsets T - S ((2 bs - 1) per axis) are staged in shared memory, then every
+// entry sums over the staged terms in ascending k with the reference's IEEE mul/add -- the same
+// terms in the same order as entry_value, so the result is bit-identical.  Blocks that leave
+// the domain or have too many candidate terms take the per-entry path.
+constexpr int BT_CAP = 32;  // max staged candidate terms per block (shared cand[] array)
+constexpr int BT_IDS = 64;  // gathered bucket entries (with duplicates) per block
+
+__global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk, const int64_t* __restrict__ t_origin,
+                                                      const int64_t* __restrict__ s_origin, int bs0, int bs1, int bs2,
+                                                      int cap, double* __restrict__ out, int32_t* bad) {
+    extern __shared__ double sm[];
+    __shared__ int64_t s_t[3], s_s[3];
+    __shared__ int s_n, s_nc, s_fb;
+    __shared__ int ids[BT_IDS];
+    __shared__ int first[BT_IDS];
+    __shared__ int cand[BT_CAP];
+    const int D = a.D;
+    const int bs[3] = {bs0, bs1, bs2};
+    int npx = 1, win = 1;
+    for (int i = 0; i < D; ++i) {
+        npx *= bs[i];
+        win *= 2 * bs[i] - 1;
+    }
+    double* W = sm;               // [cap][npx]
+    double* PH = sm + cap * npx;  // [cap][win]
+    const int tid = threadIdx.x;
+    for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        if (tid == 0) {
+            int fb = 0;
+            for (int i = 0; i < 3; ++i) {
+                s_t[i] = i < D ? t_origin[(int64_t)blk * D + i] : 0;
+                s_s[i] = i < D ? s_origin[(int64_t)blk * D + i] : 0;
+                if (i < D && (s_t[i] < a.dom_lo[i] || s_t[i] + bs[i] > a.dom_lo[i] + a.n[i] || s_s[i] < a.dom_lo[i] ||
+                              s_s[i] + bs[i] > a.dom_lo[i] + a.n[i]))
+                    fb = 1;
+            }
+            s_fb = fb;
+            s_n = 0;
+        }
+        __syncthreads();
+        if (tid < 32 && !s_fb) {  // warp 0: the candidate terms from the buckets covering S
+            int blo[3] = {0, 0, 0}, bn[3] = {1, 1, 1}, nbk = 1;
+            for (int i = 0; i < D; ++i) {
+                blo[i] = (int)((s_s[i] - a.dom_lo[i]) / a.bucket[i]);
+                bn[i] = (int)((s_s[i] + bs[i] - 1 - a.dom_lo[i]) / a.bucket[i]) - blo[i] + 1;
+                nbk *= bn[i];
+            }
+            int64_t beg = 0;
+            int cnt = 0;
+            if (nbk <= 32 && tid < nbk) {
+                int r = tid, c[3] = {0, 0, 0};
+                for (int i = D - 1; i >= 0; --i) {
+                    c[i] = blo[i] + r % bn[i];
+                    r /= bn[i];
+                }
+                int64_t bl = 0;
+                for (int i = 0; i < D; ++i) bl = bl * a.nb[i] + c[i];
+                beg = a.bucket_ptr[bl];
+                cnt = (int)(a.bucket_ptr[bl + 1] - beg);
+            }
+            int off = cnt;  // inclusive warp prefix sum
+            for (int d = 1; d < 32; d <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, off, d);
+                if (tid >= d) off += v;
+            }
+            const int total = __shfl_sync(0xffffffffu, off, 31);
+            off -= cnt;
+            if (nbk > 32 || total > BT_IDS) {
+                if (tid == 0) s_fb = 1;
+            } else {
+                for (int q = 0; q < cnt; ++q) ids[off + q] = a.bucket_terms[beg + q];
+                if (tid == 0) s_n = total;
+            }
+        }
+        __syncthreads();
+        const int n = s_n;
+        if (!s_fb && tid < n) {  // first occurrences
+            const int id = ids[tid];
+            int f = 1;
+            for (int j = 0; j < tid; ++j) f &= ids[j] != id;
+            first[tid] = f;
+        }
+        __syncthreads();
+        if (!s_fb && tid < n && first[tid]) {  // ascending rank among the distinct ids
+            const int id = ids[tid];
+            int rank = 0;
+            for (int j = 0; j < n; ++j) rank += first[j] && ids[j] < id;
+            if (rank < cap) cand[rank] = id;
+        }
+        if (tid == 0 && !s_fb) {
+            int nc = 0;
+            for (int j = 0; j < n; ++j) nc += first[j];
+            s_nc = nc;
+            if (nc > cap) s_fb = 1;
+        }
+        __syncthreads();
+        double* ob = out + (int64_t)blk * npx * npx;
+        if (s_fb) {  // per-entry path (out-of-domain entries flag `bad`)
+            for (int e = tid; e < npx * npx; e += blockDim.x) {
+                int i = e / npx, j = e - (e / npx) * npx;
+                int64_t y[3], x[3];
+                for (int d = D - 1; d >= 0; --d) {
+                    y[d] = s_t[d] + i % bs[d];
+                    i /= bs[d];
+                    x[d] = s_s[d] + j % bs[d];
+                    j /= bs[d];
+                }
+                bool b = false;
+                ob[e] = entry_value(a, y, x, b);
+                if (b) atomicOr(bad, 1);
+            }
+            __syncthreads();
+            continue;
+        }
+        const int nc = s_nc;
+        for (int idx = tid; idx < nc * npx; idx += blockDim.x) {  // w_k on S (0 outside X_k)
+            const int c = idx / npx;
+            int j = idx - c * npx;
+            const TermDesc& t = a.terms[cand[c]];
+            int64_t u[3];
+            bool in = true;
+            for (int d = D - 1; d >= 0; --d) {
+                u[d] = s_s[d] + j % bs[d] - t.x_lo[d];
+                j /= bs[d];
+                in = in && u[d] >= 0 && u[d] < t.m[d];
+            }
+            double wv = 0.0;
+            if (in) {
+                int64_t wl = 0;
+                for (int d = 0; d < D; ++d) wl = wl * t.m[d] + u[d];
+                wv = a.w_pool[t.w_off + wl];
+            }
+            W[c * npx + (idx - c * npx)] = wv;
+        }
+        for (int idx = tid; idx < nc * win; idx += blockDim.x) {  // phi_k^E on the offsets T - S
+            const int c = idx / win;
+            int w = idx - c * win;
+            const TermDesc& t = a.terms[cand[c]];
+            int64_t z[3];
+            bool in = true;
+            for (int d = D - 1; d >= 0; --d) {
+                const int wd = 2 * bs[d] - 1;
+                z[d] = s_t[d] - s_s[d] + (w % wd) - (bs[d] - 1) - t.k_lo[d];
+                w /= wd;
+                in = in && z[d] >= 0 && z[d] < t.k_ext[d];
+            }
+            double ph = 0.0;
+            if (in) {
+                int64_t zl = 0;
+                for (int d = 0; d < D; ++d) zl = zl * t.k_ext[d] + z[d];
+                ph = a.phi_pool[t.phi_off + zl];
+            }
+            PH[c * win + (idx - c * win)] = ph;
+        }
+        __syncthreads();
+        for (int e = tid; e < npx * npx; e += blockDim.x) {
+            int i = e / npx, j = e - (e / npx) * npx;
+            const int j0 = j;
+            int widx = 0, mul = 1;
+            for (int d = D - 1; d >= 0; --d) {
+                widx += (i % bs[d] - j % bs[d] + bs[d] - 1) * mul;
+                mul *= 2 * bs[d] - 1;
+                i /= bs[d];
+                j /= bs[d];
+            }
+            double sum = 0.0;
+            for (int c = 0; c < nc; ++c) {
+                const double wv = W[c * npx + j0];
+                if (wv != 0.0) sum = __dadd_rn(sum, __dmul_rn(wv, PH[c * win + widx]));
+            }
+            ob[e] = sum;
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, const int64_t* x, double* out,
@@ -200,8 +380,29 @@ cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, co
 }
 
 cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
-                          const int32_t* bshape, double* out, int32_t* bad, cudaStream_t st) {
+                          const int32_t* bshape, const int32_t* bshape_host, double* out, int32_t* bad, cudaStream_t st) {
     if (nblk <= 0) return cudaSuccess;
+    int64_t npx = 1, win = 1;
+    for (int i = 0; i < a.D; ++i) {
+        npx *= bshape_host[i];
+        win *= 2 * (int64_t)bshape_host[i] - 1;
+    }
+    static const int cap = [] {  // staged terms per block (PCB_BLOCK_CAP, <= BT_CAP)
+        const char* e = getenv("PCB_BLOCK_CAP");
+        return e ? std::max(1, std::min(BT_CAP, atoi(e))) : 16;
+    }();
+    const size_t smem = sizeof(double) * (size_t)cap * (size_t)(npx + win);
+    if (smem <= 160 * 1024) {  // tiled: staged weights and kernel windows per block
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(k_blocks_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+        }
+        const int per_sm = std::max<int>(1, (int)((220 * 1024) / (smem + 2048)));
+        const int grid = (int)std::min<int64_t>(nblk, 148LL * std::min(per_sm, 8));
+        k_blocks_tiled<<<grid, 256, smem, st>>>(a, nblk, t_origin, s_origin, bshape_host[0],
+                                                a.D > 1 ? bshape_host[1] : 1, a.D > 2 ? bshape_host[2] : 1, cap, out, bad);
+        return cudaGetLastError();
+    }
     k_blocks<<<148 * 16, 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape, out, bad);
     return cudaGetLastError();
 }

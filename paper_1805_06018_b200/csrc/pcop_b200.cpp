@@ -1895,7 +1895,7 @@ static void blocks_common(pcb_op* op, int32_t nblk, const int64_t* d_t, const in
     PCB_CK(cudaMemcpyAsync(op->st_shape.p, bs, sizeof(bs), cudaMemcpyHostToDevice, st));
     PCB_CK(cudaMemsetAsync(op->st_flag.p, 0, 4, st));
     launch(op, st, "blocks", [&] {
-        return launch_blocks(entry_args(op), nblk, d_t, d_s, op->st_shape.p, d_out, op->st_flag.p, st);
+        return launch_blocks(entry_args(op), nblk, d_t, d_s, op->st_shape.p, bs, d_out, op->st_flag.p, st);
     });
     if (host_check) {
         int32_t bad = 0;

@@ -48,11 +48,7 @@ def run(sizes, copies=True, compute=True):
 
 
 res = {}
-for name, sizes in {"4+8x7+4": [4] + [8] * 7 + [4], "4+8x7+2+1+1": [4] + [8] * 7 + [2, 1, 1],
-                    "2+2+8x7+2+1+1": [2, 2] + [8] * 7 + [2, 1, 1], "4+8x6+6+4+2": [4] + [8] * 6 + [6, 4, 2],
-                    "4+8+12x3+8+4+2+1+1": [4, 8, 12, 12, 12, 8, 4, 2, 1, 1],
-                    "2+4+8x6+4+2+2+1+1": [2, 4] + [8] * 6 + [4, 2, 2, 1, 1], "6x10+4": [6] * 10 + [4],
-                    "4x16": [4] * 16}.items():
+for name, sizes in {"3+6x9+4+3": [3] + [6] * 9 + [4, 3], "4+8x7+4": [4] + [8] * 7 + [4], "64": [64]}.items():
     for mode, kw in {"copies": dict(compute=False), "kernels": dict(copies=False), "both": {}}.items():
         run(sizes, **kw)
         t = min(run(sizes, **kw) for _ in range(3))
