@@ -55,6 +55,12 @@
 #ifndef PCB_CHAIN_STAGE
 #define PCB_CHAIN_STAGE 1  // column chains: stage each member's spectrum tile in shared memory
 #endif
+#ifndef PCB_LOCAL_STAGE
+// LOCAL cols with columns up to this length stage the spectrum tile in shared memory (cp.async,
+// overlapping the S loads and the forward FFT).  Measured: c4 (P0 = 64) cols -2%; c3 / c2
+// (P0 = 192 / 256) +8% slower, so longer columns load it directly.
+#define PCB_LOCAL_STAGE 64
+#endif
 #ifndef PCB_COLS_THREADS
 #define PCB_COLS_THREADS 64
 #endif
@@ -411,6 +417,15 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
         const TermDesc& td = a.terms[a.slots[slot]];
         const int vec = item % nvec;
         const double2* S_item = MODE == CM_SPEC ? a.S + (int64_t)item * a.S_stride : a.S + td.s_pool + vec * td.s_vst;
+        // LOCAL: the term's spectrum tile streams into shared memory while the S rows load and the
+        // forward FFT runs (no registers held for it until the multiply)
+        constexpr bool LSTAGE = MODE != CM_SPEC && P0 <= PCB_LOCAL_STAGE;
+        double2* sspec = buf + smem_words<P0, NL>();
+        if (LSTAGE) {
+            const double2* tile = a.spec_pool + td.spec_off + (c0 / NL) * (int64_t)P0 * NL;
+            for (int i = threadIdx.x; i < P0 * NL; i += NL * FftCfg<P0>::TPL) cp_async16(&sspec[i], tile + i);
+            asm volatile("cp.async.commit_group;\n" ::);
+        }
         if (MODE == CM_SPEC) load_in(S_item, 0, P0, v);
         else if (MODE == CM_APPLY_LOCAL) {
             // family term: the shared rows scaled by its lead factor (all loads before the multiply)
@@ -442,9 +457,13 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
             }
             return;
         }
+        if (LSTAGE) {
+            asm volatile("cp.async.wait_group 0;\n" ::);
+            __syncthreads();
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const double2 ph = cvalid ? __ldg(&spec[(int64_t)fpos(r) * NL]) : czero();
+            const double2 ph = LSTAGE ? sspec[fpos(r) * NL + l] : cvalid ? __ldg(&spec[(int64_t)fpos(r) * NL]) : czero();
             v[r] = MODE == CM_APPLY_LOCAL ? cmul(v[r], ph) : cmulc(v[r], ph);
         }
         fft_rev_order<P0, +1, NL, PSH<NL>>(v, buf, l, tl, tw0);
