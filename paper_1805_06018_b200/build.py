@@ -27,9 +27,12 @@ E_ROWS = os.environ.get("PCB_E_ROWS", "8")
 E_COLS = os.environ.get("PCB_E_COLS", "16")
 E_MID = os.environ.get("PCB_E_MID", "8")
 E3_MID = os.environ.get("PCB_E3_MID", "12")  # 3-smooth engines: 12 elements per thread in mid, 24 elsewhere
+E3_COLS = os.environ.get("PCB_E3_COLS", "24")  # 3-smooth engines of the cols pass
+E3_COLS_SMALL = os.environ.get("PCB_E3_COLS_SMALL", "96")  # cols: 3-smooth lengths <= this use 12 per thread
 E_COLS_SMALL = os.environ.get("PCB_E_COLS_SMALL", "64")  # cols: pow2 lengths <= this use 8 elements per thread
 PER_SOURCE = {"kernels_rows.cu": [f"-DPCB_E2={E_ROWS}"],
-              "kernels_cols.cu": [f"-DPCB_E2={E_COLS}", f"-DPCB_E2_SMALL_MAX={E_COLS_SMALL}"],
+              "kernels_cols.cu": [f"-DPCB_E2={E_COLS}", f"-DPCB_E2_SMALL_MAX={E_COLS_SMALL}", f"-DPCB_E3={E3_COLS}",
+                                  f"-DPCB_E3_SMALL_MAX={E3_COLS_SMALL}"],
               "kernels_mid.cu": [f"-DPCB_E2={E_MID}", f"-DPCB_E3={E3_MID}"]}
 SOURCES = ["kernels_rows.cu", "kernels_cols.cu", "kernels_mid.cu", "kernels_misc.cu", "blur.cu", "hmatrix.cpp", "pcop_b200.cpp"]
 HEADERS = ["fft.cuh", "kernels.cuh", "kernels_impl.cuh"]

@@ -32,12 +32,16 @@
 #ifndef PCB_E2_SMALL_MAX
 #define PCB_E2_SMALL_MAX 0  // power-of-two lengths <= this use 8 elements per thread (0: none)
 #endif
+#ifndef PCB_E3_SMALL_MAX
+#define PCB_E3_SMALL_MAX 0  // 3-smooth lengths <= this use 12 elements per thread (0: none)
+#endif
 #define PCB_NS_CAT2(a, b) a##b
 #define PCB_NS_CAT(a, b) PCB_NS_CAT2(a, b)
 
 namespace pcb {
 // the engine is instantiated per element count: distinct names per translation unit setting
-inline namespace PCB_NS_CAT(PCB_NS_CAT(PCB_NS_CAT(e, PCB_E2), PCB_NS_CAT(_, PCB_E3)), PCB_NS_CAT(_s, PCB_E2_SMALL_MAX)) {
+inline namespace PCB_NS_CAT(PCB_NS_CAT(PCB_NS_CAT(e, PCB_E2), PCB_NS_CAT(_, PCB_E3)),
+                            PCB_NS_CAT(PCB_NS_CAT(_s, PCB_E2_SMALL_MAX), PCB_NS_CAT(_t, PCB_E3_SMALL_MAX))) {
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -173,7 +177,8 @@ struct FftCfg {
     static_assert(fft_len_ok(L) && L <= 4096, "unsupported FFT line length");
     static constexpr bool P2 = is_pow2c(L);
     static constexpr int E2L = (L <= PCB_E2_SMALL_MAX && PCB_E2 > 8) ? 8 : PCB_E2;  // per-length E (pow2)
-    static constexpr int R = P2 ? (L >= E2L ? E2L : L) : (L % PCB_E3 == 0 ? PCB_E3 : 24);  // elements per thread (= last radix)
+    static constexpr int E3L = (L <= PCB_E3_SMALL_MAX && L % 12 == 0) ? 12 : PCB_E3;  // per-length E (3-smooth)
+    static constexpr int R = P2 ? (L >= E2L ? E2L : L) : (L % E3L == 0 ? E3L : 24);  // elements per thread (= last radix)
     static constexpr int TPL = L / R;                        // threads per line
     // forward stage radices: the prefix factors L/R, then R
     static constexpr int pref_radix(int rest) {
