@@ -75,7 +75,7 @@ struct PassArgs {
     int64_t dom_lo[3];
     int32_t n[3];          // domain extents
     int32_t P[3];          // FFT sizes (P[D-1] is the real axis)
-    int32_t W;             // padded half-spectrum row: roundup(P_last/2+1, 8)
+    int32_t W;             // padded half-spectrum row: roundup(P_last/2+1, w_align)
     int64_t L;             // lines of the axis-0 pass: W (2D) or P1*W (3D)
     int32_t lines_max;     // rows_fwd: max lines of one item over the launch's terms
     int32_t nl_cols;       // spectrum tile width

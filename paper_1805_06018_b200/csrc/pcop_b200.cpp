@@ -120,6 +120,11 @@ struct PlanSwitches {
     bool chains = false;
     bool plane_families = true;  // PCB_PLANE_FAMILIES=0: per-term mid forward pass in 3-D
     bool graphs = true;          // PCB_GRAPHS=0: device-pointer applies launch kernel by kernel
+    // PCB_W_ALIGN: half-spectrum rows padded to a multiple of this many complex values.  Every
+    // padding column is transformed by the cols / mid passes for nothing; 32-byte sectors only
+    // need even rows.  Measured (c4 / c3 / c2): 8 -> 914 / 8,008 / 28.5k vec/s, 4 -> 966 / 8,109 /
+    // 28.9k, 2 -> 996 / 8,045 / 28.7k.  Set at create: 2 in 3-D, 4 in 2-D.
+    int w_align = 0;
     double chain_beta = 24.0;  // PCB_CHAIN_BETA: modelled cost of one T row element, in column-FFT units
     bool chain_grow = false;   // PCB_CHAIN_GROW=1: a chain may use a larger FFT than its members' own
 };
@@ -1127,7 +1132,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     int64_t spec_total = 0;
     for (Group& g : op->groups) {
         const int last = g.P[D - 1];
-        g.W = ((last / 2 + 1) + 7) / 8 * 8;
+        g.W = ((last / 2 + 1) + op->sw.w_align - 1) / op->sw.w_align * op->sw.w_align;
         g.L = D == 2 ? g.W : (int64_t)g.P[1] * g.W;
         g.nl = cols_tile_width(g.P[0]);
         if (g.nl <= 0) fail(PCB_EINTERNAL, "unsupported FFT size");
@@ -1630,6 +1635,8 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
         if (const char* e = getenv("PCB_CHAINS")) op->sw.chains = atoi(e) != 0;
         if (const char* e = getenv("PCB_PLANE_FAMILIES")) op->sw.plane_families = atoi(e) != 0;
         if (const char* e = getenv("PCB_GRAPHS")) op->sw.graphs = atoi(e) != 0;
+        op->sw.w_align = dim == 3 ? 2 : 4;
+        if (const char* e = getenv("PCB_W_ALIGN")) op->sw.w_align = std::max(1, atoi(e));
         if (const char* e = getenv("PCB_CHAIN_BETA")) op->sw.chain_beta = atof(e);
         if (const char* e = getenv("PCB_CHAIN_GROW")) op->sw.chain_grow = atoi(e) != 0;
 
