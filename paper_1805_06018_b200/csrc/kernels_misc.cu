@@ -199,6 +199,7 @@ __global__ void k_zero(double* p, int64_t n) {
 // the domain or have too many candidate terms take the per-entry path.
 constexpr int BT_CAP = 32;  // max staged candidate terms per block (shared cand[] array)
 constexpr int BT_IDS = 64;  // gathered bucket entries (with duplicates) per block
+constexpr int BT_NZ = 8;    // listed nonzero-weight terms per source point
 
 __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk, const int64_t* __restrict__ t_origin,
                                                       const int64_t* __restrict__ s_origin, int bs0, int bs1, int bs2,
@@ -218,7 +219,28 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk,
     }
     double* W = sm;               // [cap][npx]
     double* PH = sm + cap * npx;  // [cap][win]
+    int* offs = reinterpret_cast<int*>(PH + cap * win);              // [npx] window offset of a point
+    unsigned char* nzn = reinterpret_cast<unsigned char*>(offs + npx);  // [npx] nonzero-term count
+    unsigned char* nzc = nzn + npx;                                   // [npx][BT_NZ] their indices
     const int tid = threadIdx.x;
+    int centre = 0;
+    {
+        int mul = 1;
+        for (int d = D - 1; d >= 0; --d) {
+            centre += (bs[d] - 1) * mul;
+            mul *= 2 * bs[d] - 1;
+        }
+    }
+    for (int p = tid; p < npx; p += blockDim.x) {
+        int r = p, o = 0, mul = 1;
+        for (int d = D - 1; d >= 0; --d) {
+            o += (r % bs[d]) * mul;
+            mul *= 2 * bs[d] - 1;
+            r /= bs[d];
+        }
+        offs[p] = o;
+    }
+    __syncthreads();
     for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
         if (tid == 0) {
             int fb = 0;
@@ -348,20 +370,32 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk,
             PH[c * win + (idx - c * win)] = ph;
         }
         __syncthreads();
+        for (int j = tid; j < npx; j += blockDim.x) {  // per source point: its terms with w != 0
+            int q = 0;
+            for (int c = 0; c < nc; ++c)
+                if (W[c * npx + j] != 0.0) {
+                    if (q < BT_NZ) nzc[j * BT_NZ + q] = (unsigned char)c;
+                    ++q;
+                }
+            nzn[j] = (unsigned char)(q <= BT_NZ ? q : 255);
+        }
+        __syncthreads();
+        // entry (i, j): window index T_off[i] - S_off[j] + centre (the per-axis offset is linear)
         for (int e = tid; e < npx * npx; e += blockDim.x) {
-            int i = e / npx, j = e - (e / npx) * npx;
-            const int j0 = j;
-            int widx = 0, mul = 1;
-            for (int d = D - 1; d >= 0; --d) {
-                widx += (i % bs[d] - j % bs[d] + bs[d] - 1) * mul;
-                mul *= 2 * bs[d] - 1;
-                i /= bs[d];
-                j /= bs[d];
-            }
+            const int i = e / npx, j = e - i * npx;
+            const int widx = offs[i] - offs[j] + centre;
             double sum = 0.0;
-            for (int c = 0; c < nc; ++c) {
-                const double wv = W[c * npx + j0];
-                if (wv != 0.0) sum = __dadd_rn(sum, __dmul_rn(wv, PH[c * win + widx]));
+            const int q = nzn[j];
+            if (q != 255) {
+                for (int r = 0; r < q; ++r) {
+                    const int c = nzc[j * BT_NZ + r];
+                    sum = __dadd_rn(sum, __dmul_rn(W[c * npx + j], PH[c * win + widx]));
+                }
+            } else {
+                for (int c = 0; c < nc; ++c) {
+                    const double wv = W[c * npx + j];
+                    if (wv != 0.0) sum = __dadd_rn(sum, __dmul_rn(wv, PH[c * win + widx]));
+                }
             }
             ob[e] = sum;
         }
@@ -391,7 +425,8 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
         const char* e = getenv("PCB_BLOCK_CAP");
         return e ? std::max(1, std::min(BT_CAP, atoi(e))) : 16;
     }();
-    const size_t smem = sizeof(double) * (size_t)cap * (size_t)(npx + win);
+    const size_t smem = sizeof(double) * (size_t)cap * (size_t)(npx + win) + sizeof(int) * (size_t)npx +
+                        (size_t)npx * (1 + BT_NZ) + 16;
     if (smem <= 160 * 1024) {  // tiled: staged weights and kernel windows per block
         if (smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(k_blocks_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
