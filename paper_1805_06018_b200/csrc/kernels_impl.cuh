@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
                 for (int r = 0; r < R; ++r) v[r] = cscale(v[r], sc[r]);
             }
         }
-        else load_in(S_item, td.o_lo[0], td.o_cnt[0], v);
+        else load_in(td.af_off >= 0 ? a.S + td.af_off + vec * td.af_vst : S_item, td.o_lo[0], td.o_cnt[0], v);
         fft_fwd_order<P0, -1, NL, PSH<NL>>(v, buf, l, tl, tw0);
         double2* spec = a.spec_pool + td.spec_off + tile_off;
         if (MODE == CM_SPEC) {

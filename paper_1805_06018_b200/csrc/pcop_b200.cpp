@@ -195,6 +195,11 @@ struct Class {
         DevBuf<int32_t> slots;
     };
     std::vector<PfSet> pfsets;
+    // 2-D adjoint row families: terms with the same axis-1 output window share the forward rows
+    // of g over the union of their axis-0 output rows (no weight on the adjoint input)
+    std::vector<int> afams;  // indices into pcb_op::afams
+    DevBuf<int32_t> afam_slots;
+    int afam_lines = 1;
 };
 
 std::atomic<long long> g_launches{0};
@@ -222,6 +227,8 @@ struct pcb_op {
     pcb::DevBuf<pcb::TermDesc> d_terms, d_gdesc, d_fams;
     std::vector<pcb::TermDesc> fams;  // row-family descriptors (rows_fwd items of family classes)
     std::vector<pcb::TermDesc> pfams; // 3-D plane-family descriptors (mid forward items)
+    std::vector<pcb::TermDesc> afams; // 2-D adjoint row-family descriptors (rows_fwd adjoint items)
+    pcb::DevBuf<pcb::TermDesc> d_afams;
     pcb::DevBuf<pcb::TermDesc> d_pfams;
     // column chains: output descriptor (s, o_lo/o_cnt, T region; m[ax] = axis-1 support) + members
     std::vector<pcb::TermDesc> chains;
@@ -891,6 +898,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             gd.m[a] = gd.o_cnt[a];
         }
         gd.f_off = gd.f_vst = gd.a_off = -1;
+        gd.af_off = gd.af_vst = -1;
     }
     // groups (full FFT shape) and classes (last-axis length)
     std::map<std::vector<int>, int> gid;
@@ -929,6 +937,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     // A class uses families only when every term factors and the shared rows are >= 1.2x fewer.
     for (TermDesc& t : op->terms) {
         t.f_off = t.f_vst = t.a_off = -1;
+        t.af_off = t.af_vst = -1;
         t.f_ps = 0;
         t.wrow0 = 0;
         t.cols_f = 0;
@@ -1128,6 +1137,59 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             }
         }
 
+    // Adjoint row families (2-D LOCAL).  The adjoint's forward rows are R2C of g on a term's
+    // output window, with no weight: terms of one class with the same axis-1 window (s_1, o_lo_1,
+    // o_cnt_1) have identical rows wherever their axis-0 windows overlap, so they share the rows
+    // over the union of their axis-0 windows.  Used when the shared rows are >= 1.2x fewer.
+    std::vector<int> term_af(r, -1);
+    if (mode == PCB_MODE_LOCAL && D == 2 && op->sw.families)
+        for (Class& c : op->classes) {
+            std::map<std::tuple<int64_t, int32_t, int32_t>, int> fid;
+            std::vector<std::vector<int>> members;
+            for (int k : c.terms) {
+                const TermDesc& t = op->terms[k];
+                auto key = std::make_tuple(t.s[1], t.o_lo[1], t.o_cnt[1]);
+                auto it = fid.find(key);
+                if (it == fid.end()) {
+                    it = fid.emplace(key, (int)members.size()).first;
+                    members.emplace_back();
+                }
+                members[it->second].push_back(k);
+            }
+            int64_t rows_terms = 0, rows_fams = 0;
+            std::vector<TermDesc> fd(members.size());
+            for (size_t f = 0; f < members.size(); ++f) {
+                int64_t lo = INT64_MAX, hi = INT64_MIN;
+                for (int k : members[f]) {
+                    const TermDesc& t = op->terms[k];
+                    lo = std::min<int64_t>(lo, t.s[0] + t.o_lo[0]);
+                    hi = std::max<int64_t>(hi, t.s[0] + t.o_lo[0] + t.o_cnt[0]);
+                    rows_terms += t.o_cnt[0];
+                }
+                const TermDesc& t0 = op->terms[members[f][0]];
+                TermDesc& d = fd[f];
+                d = TermDesc{};
+                d.s[0] = lo;  // rows y0 = lo + line
+                d.o_lo[0] = 0;
+                d.o_cnt[0] = (int32_t)(hi - lo);
+                d.s[1] = t0.s[1];
+                d.o_lo[1] = t0.o_lo[1];
+                d.o_cnt[1] = t0.o_cnt[1];
+                d.o_cnt[2] = 1;
+                d.P1 = 1;
+                d.f_off = d.f_vst = d.a_off = d.af_off = d.af_vst = -1;
+                rows_fams += hi - lo;
+            }
+            if (members.size() == c.terms.size() || (double)rows_terms < 1.2 * (double)rows_fams) continue;
+            for (size_t f = 0; f < members.size(); ++f) {
+                const int id = (int)op->afams.size();
+                for (int k : members[f]) term_af[k] = id;
+                c.afams.push_back(id);
+                c.afam_lines = std::max<int>(c.afam_lines, fd[f].o_cnt[0]);
+                op->afams.push_back(fd[f]);
+            }
+        }
+
     // layout: spectra per group; scratch regions per term (pools reused class by class)
     int64_t spec_total = 0;
     for (Group& g : op->groups) {
@@ -1172,6 +1234,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             s_sum += (D == 2 ? (int64_t)f.m[0] : (int64_t)f.m[0] * f.m[1]) * c.W;
         }
         for (int ci : c.chains) t_sum += (int64_t)op->chains[ci].o_cnt[0] * c.W;
+        for (int id : c.afams) s_sum += (int64_t)op->afams[id].o_cnt[0] * c.W;
         for (const Class::PfSet& ps : c.pfsets)
             for (int id : ps.ids) s_sum += (int64_t)op->pfams[id].m[0] * op->pfams[id].P1 * c.W;
         for (int gi : c.groups) c.P0max = std::max(c.P0max, op->groups[gi].P[0]);
@@ -1240,6 +1303,19 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
                 d.s_vst = (int64_t)d.m[0] * d.P1 * c.W;
                 so += d.s_vst * vb;
             }
+        for (int id : c.afams) {  // adjoint row families
+            TermDesc& d = op->afams[id];
+            d.s_pool = so;
+            d.s_vst = (int64_t)d.o_cnt[0] * c.W;
+            so += d.s_vst * vb;
+        }
+        for (int k : c.terms) {
+            if (term_af[k] < 0) continue;
+            TermDesc& t = op->terms[k];
+            const TermDesc& d = op->afams[term_af[k]];
+            t.af_off = d.s_pool + (t.s[0] + t.o_lo[0] - d.s[0]) * c.W;
+            t.af_vst = d.s_vst;
+        }
         for (int k : c.terms) {
             if (term_pf[k] < 0) continue;
             TermDesc& t = op->terms[k];
@@ -1273,6 +1349,9 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     op->phi_pool.upload(ppool);
     op->d_fams.upload(op->fams.empty() ? std::vector<TermDesc>(1) : op->fams);
     op->d_pfams.upload(op->pfams.empty() ? std::vector<TermDesc>(1) : op->pfams);
+    op->d_afams.upload(op->afams.empty() ? std::vector<TermDesc>(1) : op->afams);
+    for (Class& c : op->classes)
+        if (!c.afams.empty()) c.afam_slots.upload(std::vector<int32_t>(c.afams.begin(), c.afams.end()));
     for (Class& c : op->classes)
         for (Class::PfSet& ps : c.pfsets) ps.slots.upload(std::vector<int32_t>(ps.ids.begin(), ps.ids.end()));
     {
@@ -1488,6 +1567,13 @@ void run_batch(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG
                 af.n_slots = (int)c.fams.size();
                 af.lines_max = c.fam_lines;
                 launch(op, st, "rows_fwd(apply)", [&] { return launch_rows_fwd(af, RF_APPLY, st); });
+            } else if (adjoint && !c.afams.empty()) {  // shared rows of g (2-D adjoint families)
+                PassArgs af = a;
+                af.terms = op->d_afams.p;
+                af.slots = c.afam_slots.p;
+                af.n_slots = (int)c.afams.size();
+                af.lines_max = c.afam_lines;
+                launch(op, st, "rows_fwd(adjoint)", [&] { return launch_rows_fwd(af, RF_ADJ, st); });
             } else {
                 launch(op, st, adjoint ? "rows_fwd(adjoint)" : "rows_fwd(apply)",
                        [&] { return launch_rows_fwd(a, adjoint ? RF_ADJ : RF_APPLY, st); });
