@@ -117,7 +117,7 @@ enum RowsFwdMode { RF_APPLY = 0, RF_ADJ = 1, RF_SPEC = 2 };
 enum ColsMode { CM_SPEC = 0, CM_APPLY_LOCAL = 1, CM_APPLY_GLOBAL = 2, CM_ADJ_LOCAL = 3, CM_ADJ_GLOBAL = 4,
                 CM_APPLY_CHAIN = 5 };
 enum MidMode { MM_FWD_APPLY = 0, MM_FWD_ADJ = 1, MM_FWD_SPEC = 2, MM_INV_APPLY = 3, MM_INV_ADJ = 4 };
-enum RowsInvMode { RI_APPLY = 0, RI_ADJ = 1, RI_APPLY_B = 2 };
+enum RowsInvMode { RI_APPLY = 0, RI_ADJ = 1, RI_APPLY_B = 2, RI_ADJ_B = 3 };
 
 // launchers (kernels.cu); return cudaGetLastError()
 cudaError_t launch_rows_fwd(const PassArgs& a, int mode, cudaStream_t st);

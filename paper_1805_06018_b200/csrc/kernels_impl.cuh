@@ -714,7 +714,10 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
 // flight per CTA), summed into the lane's half spectrum in registers -- scale * T[k] *
 // exp(-2 pi i k delta / P) -- then one C2R per bundle and one add of its range into the output
 // line.  Members are summed in CSR order, bundles in CSR order: deterministic.
-template <int N, int NL>
+// ADJ: the 2-D adjoint's family bundles -- members of one row family covering the output line,
+// scaled by A_k(line) / prod P (no phase: one placement), summed, transformed once, and the
+// result multiplied by the family's last-axis weight row c (header w_off) as it accumulates.
+template <int N, int NL, int ADJ>
 __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_MINB_B : PCB_ROWS_MINB_MIXED)
     k_rows_inv_b(PassArgs a) {
     constexpr int R = FftCfg<N>::R;
@@ -857,7 +860,12 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
             const int lo = meta[ll].lo, hi = meta[ll].hi;
             const double* x = xs + ll * XS - meta[ll].sh;
             int p = lo + (int)((threadIdx.x + NT - (unsigned)(lo % NT)) % NT);
-            for (; p < hi; p += NT) acc[p - ulo] += x[p];
+            if (ADJ) {
+                const double* w = a.w_pool + meta[ll].w_off;
+                for (; p < hi; p += NT) acc[p - ulo] += w[p] * x[p];
+            } else {
+                for (; p < hi; p += NT) acc[p - ulo] += x[p];
+            }
         }
         __syncthreads();  // xs (the FFT buffer) and meta are free
         GatherEntry* t = meta;
@@ -945,7 +953,12 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
             const int lo = meta[ll].lo, hi = meta[ll].hi;
             const double* x = xs + ll * XS - meta[ll].sh;
             int p = lo + (int)((threadIdx.x + NT - (unsigned)(lo % NT)) % NT);
-            for (; p < hi; p += NT) acc[p - ulo] += x[p];
+            if (ADJ) {
+                const double* w = a.w_pool + meta[ll].w_off;
+                for (; p < hi; p += NT) acc[p - ulo] += w[p] * x[p];
+            } else {
+                for (; p < hi; p += NT) acc[p - ulo] += x[p];
+            }
         }
     }
 #endif

@@ -41,7 +41,7 @@ cudaError_t rows_inv_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
     return launch_dyn(k_rows_inv<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
 }
 
-template <int N>
+template <int N, int ADJ>
 cudaError_t rows_inv_b_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
     constexpr int NL = rows_nl<N>();
     constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
@@ -54,15 +54,15 @@ cudaError_t rows_inv_b_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
 #endif
     const size_t smem = sizeof(double2) * stage_words + sizeof(double) * ((size_t)a.n[a.D - 1] + 1) +
                         (1 + PCB_BUNDLE_XPF) * NL * sizeof(GatherEntry) + 16;
-    return launch_dyn(k_rows_inv_b<N, NL>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
+    return launch_dyn(k_rows_inv_b<N, NL, ADJ>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
 }
 
 template <int MODE>
 cudaError_t rows_inv_mode(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
-    if constexpr (MODE == RI_APPLY_B) {
+    if constexpr (MODE == RI_APPLY_B || MODE == RI_ADJ_B) {
         switch (a.P[a.D - 1] / 2) {
 #define PCB_CASE(n) \
-    case n: return rows_inv_b_n<n>(a, n_lines, st);
+    case n: return rows_inv_b_n<n, MODE == RI_ADJ_B ? 1 : 0>(a, n_lines, st);
             PCB_ROW_SIZES(PCB_CASE)
 #undef PCB_CASE
             default: return cudaErrorInvalidValue;
@@ -104,6 +104,7 @@ cudaError_t launch_rows_inv(const PassArgs& a, int mode, int64_t n_lines, cudaSt
         case RI_APPLY: return rows_inv_mode<RI_APPLY>(a, n_lines, st);
         case RI_ADJ: return rows_inv_mode<RI_ADJ>(a, n_lines, st);
         case RI_APPLY_B: return rows_inv_mode<RI_APPLY_B>(a, n_lines, st);
+        case RI_ADJ_B: return rows_inv_mode<RI_ADJ_B>(a, n_lines, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -228,6 +228,8 @@ struct pcb_op {
     std::vector<pcb::TermDesc> fams;  // row-family descriptors (rows_fwd items of family classes)
     std::vector<pcb::TermDesc> pfams; // 3-D plane-family descriptors (mid forward items)
     std::vector<pcb::TermDesc> afams; // 2-D adjoint row-family descriptors (rows_fwd adjoint items)
+    std::vector<int> term_fam;        // row family of each term (-1: none)
+    std::vector<double> apool_host;   // host copy of the lead-axis weight factors (a_pool)
     pcb::DevBuf<pcb::TermDesc> d_afams;
     pcb::DevBuf<pcb::TermDesc> d_pfams;
     // column chains: output descriptor (s, o_lo/o_cnt, T region; m[ax] = axis-1 support) + members
@@ -568,7 +570,71 @@ void build_csr(pcb_op* op, Class& c, bool global, const std::vector<double>& ter
     };
     if (!global && op->sw.bundle) flatten_b(c.apply);
     else flatten(ap, c.apply);
-    flatten(ad, c.adj);
+    // 2-D adjoint with row families: per output line, the rows of one family's members (same
+    // placement, same last-axis weight row c) are summed with the scales A_k(line) / prod P,
+    // transformed once and multiplied by c -- one C2R per (line, family) instead of per term
+    if (!global && D == 2 && op->sw.bundle && !c.fams.empty()) {
+        std::vector<std::vector<std::pair<int, int>>> lines(n_lines);  // (term, u0) per output line
+        for (int k : c.terms) {
+            const TermDesc& t = op->terms[k];
+            for (int u0 = 0; u0 < t.m[0]; ++u0) lines[line_of(t.x_lo[0] + u0, 0)].push_back({k, u0});
+        }
+        std::vector<int64_t> hp, ids;
+        std::vector<int32_t> rg;
+        std::vector<GatherEntry> he;
+        std::vector<BundleMember> hm;
+        for (int64_t ln = 0; ln < n_lines; ++ln) {
+            auto& L = lines[ln];
+            if (L.empty()) continue;
+            std::stable_sort(L.begin(), L.end(), [&](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+                return op->term_fam[x.first] < op->term_fam[y.first];
+            });
+            int ulo = INT32_MAX, uhi = INT32_MIN;
+            hp.push_back((int64_t)he.size());
+            ids.push_back(ln);
+            size_t i = 0;
+            while (i < L.size()) {
+                const int f = op->term_fam[L[i].first];
+                const TermDesc& t0 = op->terms[L[i].first];
+                GatherEntry h{};
+                h.sh = (int)(t0.x_lo[ax] - op->dom_lo[ax]);
+                h.lo = std::max(h.sh, 0);
+                h.hi = std::min(h.sh + t0.m[ax], op->n[ax]);
+                h.w_off = op->fams[f].w_off - h.sh;
+                h.t_off = (int64_t)hm.size();
+                for (; i < L.size() && op->term_fam[L[i].first] == f; ++i) {
+                    const int k = L[i].first, u0 = L[i].second;
+                    const TermDesc& t = op->terms[k];
+                    hm.push_back(BundleMember{t.t_pool + (int64_t)u0 * c.W, t.t_vst,
+                                              term_scale[k] * op->apool_host[t.a_off + u0], 0, 0});
+                    ++h.pad_;
+                }
+                ulo = std::min(ulo, h.lo);
+                uhi = std::max(uhi, h.hi);
+                he.push_back(h);
+            }
+            rg.push_back(ulo);
+            rg.push_back(std::max(ulo, uhi));
+        }
+        Csr& out = c.adj;
+        hp.push_back((int64_t)he.size());
+        out.n_lines = (int64_t)ids.size();
+        out.ptr.upload(hp);
+        if (ids.empty()) {
+            ids.push_back(0);
+            rg.push_back(0);
+            rg.push_back(0);
+        }
+        if (he.empty()) he.push_back(GatherEntry{});
+        if (hm.empty()) hm.push_back(BundleMember{});
+        out.ids.upload(ids);
+        out.rng.upload(rg);
+        out.en.upload(he);
+        out.mem.upload(hm);
+        out.bundled = true;
+    } else {
+        flatten(ad, c.adj);
+    }
 }
 
 void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t r, const int64_t* w_lo,
@@ -1137,6 +1203,8 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             }
         }
 
+    op->term_fam = term_fam;
+    op->apool_host = apool;
     // Adjoint row families (2-D LOCAL).  The adjoint's forward rows are R2C of g on a term's
     // output window, with no weight: terms of one class with the same axis-1 window (s_1, o_lo_1,
     // o_cnt_1) have identical rows wherever their axis-0 windows overlap, so they share the rows
@@ -1624,7 +1692,7 @@ void run_batch(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG
             a.line_rng = csr.rng.p;
             a.entries = csr.en.p;
             a.members = csr.mem.p;
-            const int ri = adjoint ? RI_ADJ : (csr.bundled ? RI_APPLY_B : RI_APPLY);
+            const int ri = adjoint ? (csr.bundled ? RI_ADJ_B : RI_ADJ) : (csr.bundled ? RI_APPLY_B : RI_APPLY);
             if (csr.n_lines > 0)
                 launch(op, st, adjoint ? "rows_inv(adjoint)" : "rows_inv(apply)",
                        [&] { return launch_rows_inv(a, ri, csr.n_lines, st); });
