@@ -34,9 +34,12 @@ struct TermDesc {
     // forward row transforms are the family's shared rows (double2 offset f_off for vector 0,
     // + f_vst per vector, f_ps lines per family plane in 3-D) times A_k (a_pool + a_off); -1: none
     int64_t f_off, f_vst, a_off;
-    // adjoint row family (2-D LOCAL): the forward rows of g on this term's output window are the
-    // family's rows from af_off (+ af_vst per vector); -1: the term's own S region
+    // adjoint row family (LOCAL): the forward rows of g on this term's output window are the
+    // family's rows from af_off (+ af_vst per vector; 3-D: af_ps lines per family plane, read by
+    // the mid pass); -1: the term's own S region
     int64_t af_off, af_vst;
+    int32_t af_ps;
+    int32_t pad2_;
     int32_t f_ps;
     int32_t P1;        // axis-1 FFT size of the term (3-D plane stride); 1 in 2-D.  A family
                        // descriptor (rows_fwd item) holds its lead-axis-1 line count here

@@ -299,7 +299,12 @@ __global__ void __launch_bounds__(NL * FftCfg<P1>::TPL) k_mid(PassArgs a) {
     if (fwd) {
         // family term: the input lines are the family's shared rows scaled by A_k(plane, line)
         const bool fam = MODE == MM_FWD_APPLY && td.a_off >= 0;
-        const double2* src = fam ? a.S + td.f_off + vec * td.f_vst + plane * (int64_t)td.f_ps * a.W + c : base;
+        // adjoint family term: its input lines [in_lo, in_lo + in_cnt) are the family's rows of g
+        const bool afam = MODE == MM_FWD_ADJ && td.af_off >= 0;
+        const double2* src = fam ? a.S + td.f_off + vec * td.f_vst + plane * (int64_t)td.f_ps * a.W + c
+                           : afam ? a.S + td.af_off + vec * td.af_vst + plane * (int64_t)td.af_ps * a.W + c -
+                                        (int64_t)in_lo * a.W
+                                  : base;
         double sc[R];
         if (fam) {
             const double* av = a.a_pool + td.a_off + plane * (int64_t)td.m[1];
@@ -447,7 +452,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
                 for (int r = 0; r < R; ++r) v[r] = cscale(v[r], sc[r]);
             }
         }
-        else load_in(td.af_off >= 0 ? a.S + td.af_off + vec * td.af_vst : S_item, td.o_lo[0], td.o_cnt[0], v);
+        else load_in(a.D == 2 && td.af_off >= 0 ? a.S + td.af_off + vec * td.af_vst : S_item, td.o_lo[0], td.o_cnt[0], v);
         fft_fwd_order<P0, -1, NL, PSH<NL>>(v, buf, l, tl, tw0);
         double2* spec = a.spec_pool + td.spec_off + tile_off;
         if (MODE == CM_SPEC) {

@@ -1004,6 +1004,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     for (TermDesc& t : op->terms) {
         t.f_off = t.f_vst = t.a_off = -1;
         t.af_off = t.af_vst = -1;
+        t.af_ps = 0;
         t.f_ps = 0;
         t.wrow0 = 0;
         t.cols_f = 0;
@@ -1210,13 +1211,14 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     // o_cnt_1) have identical rows wherever their axis-0 windows overlap, so they share the rows
     // over the union of their axis-0 windows.  Used when the shared rows are >= 1.2x fewer.
     std::vector<int> term_af(r, -1);
-    if (mode == PCB_MODE_LOCAL && D == 2 && op->sw.families)
+    if (mode == PCB_MODE_LOCAL && op->sw.families)
         for (Class& c : op->classes) {
+            const int ax = D - 1;
             std::map<std::tuple<int64_t, int32_t, int32_t>, int> fid;
             std::vector<std::vector<int>> members;
             for (int k : c.terms) {
                 const TermDesc& t = op->terms[k];
-                auto key = std::make_tuple(t.s[1], t.o_lo[1], t.o_cnt[1]);
+                auto key = std::make_tuple(t.s[ax], t.o_lo[ax], t.o_cnt[ax]);
                 auto it = fid.find(key);
                 if (it == fid.end()) {
                     it = fid.emplace(key, (int)members.size()).first;
@@ -1227,33 +1229,40 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             int64_t rows_terms = 0, rows_fams = 0;
             std::vector<TermDesc> fd(members.size());
             for (size_t f = 0; f < members.size(); ++f) {
-                int64_t lo = INT64_MAX, hi = INT64_MIN;
-                for (int k : members[f]) {
-                    const TermDesc& t = op->terms[k];
-                    lo = std::min<int64_t>(lo, t.s[0] + t.o_lo[0]);
-                    hi = std::max<int64_t>(hi, t.s[0] + t.o_lo[0] + t.o_cnt[0]);
-                    rows_terms += t.o_cnt[0];
-                }
                 const TermDesc& t0 = op->terms[members[f][0]];
                 TermDesc& d = fd[f];
                 d = TermDesc{};
-                d.s[0] = lo;  // rows y0 = lo + line
-                d.o_lo[0] = 0;
-                d.o_cnt[0] = (int32_t)(hi - lo);
-                d.s[1] = t0.s[1];
-                d.o_lo[1] = t0.o_lo[1];
-                d.o_cnt[1] = t0.o_cnt[1];
-                d.o_cnt[2] = 1;
-                d.P1 = 1;
+                int64_t lines = 1;
+                for (int a = 0; a < ax; ++a) {  // union of the lead-axis output windows
+                    int64_t lo = INT64_MAX, hi = INT64_MIN;
+                    for (int k : members[f]) {
+                        const TermDesc& t = op->terms[k];
+                        lo = std::min<int64_t>(lo, t.s[a] + t.o_lo[a]);
+                        hi = std::max<int64_t>(hi, t.s[a] + t.o_lo[a] + t.o_cnt[a]);
+                    }
+                    d.s[a] = lo;  // line coordinate y_a = lo + v_a
+                    d.o_lo[a] = 0;
+                    d.o_cnt[a] = (int32_t)(hi - lo);
+                    lines *= hi - lo;
+                }
+                for (int k : members[f]) {
+                    const TermDesc& t = op->terms[k];
+                    rows_terms += D == 2 ? t.o_cnt[0] : (int64_t)t.o_cnt[0] * t.o_cnt[1];
+                }
+                d.s[ax] = t0.s[ax];
+                d.o_lo[ax] = t0.o_lo[ax];
+                d.o_cnt[ax] = t0.o_cnt[ax];
+                for (int a = D; a < 3; ++a) d.o_cnt[a] = 1;
+                d.P1 = D == 3 ? d.o_cnt[1] : 1;  // family rows [U0][U1][W]
                 d.f_off = d.f_vst = d.a_off = d.af_off = d.af_vst = -1;
-                rows_fams += hi - lo;
+                rows_fams += lines;
             }
             if (members.size() == c.terms.size() || (double)rows_terms < 1.2 * (double)rows_fams) continue;
             for (size_t f = 0; f < members.size(); ++f) {
                 const int id = (int)op->afams.size();
                 for (int k : members[f]) term_af[k] = id;
                 c.afams.push_back(id);
-                c.afam_lines = std::max<int>(c.afam_lines, fd[f].o_cnt[0]);
+                c.afam_lines = std::max<int>(c.afam_lines, D == 2 ? fd[f].o_cnt[0] : fd[f].o_cnt[0] * fd[f].o_cnt[1]);
                 op->afams.push_back(fd[f]);
             }
         }
@@ -1302,7 +1311,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             s_sum += (D == 2 ? (int64_t)f.m[0] : (int64_t)f.m[0] * f.m[1]) * c.W;
         }
         for (int ci : c.chains) t_sum += (int64_t)op->chains[ci].o_cnt[0] * c.W;
-        for (int id : c.afams) s_sum += (int64_t)op->afams[id].o_cnt[0] * c.W;
+        for (int id : c.afams) s_sum += (int64_t)op->afams[id].o_cnt[0] * op->afams[id].P1 * c.W;
         for (const Class::PfSet& ps : c.pfsets)
             for (int id : ps.ids) s_sum += (int64_t)op->pfams[id].m[0] * op->pfams[id].P1 * c.W;
         for (int gi : c.groups) c.P0max = std::max(c.P0max, op->groups[gi].P[0]);
@@ -1374,15 +1383,18 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
         for (int id : c.afams) {  // adjoint row families
             TermDesc& d = op->afams[id];
             d.s_pool = so;
-            d.s_vst = (int64_t)d.o_cnt[0] * c.W;
+            d.s_vst = (int64_t)d.o_cnt[0] * d.P1 * c.W;
             so += d.s_vst * vb;
         }
         for (int k : c.terms) {
             if (term_af[k] < 0) continue;
             TermDesc& t = op->terms[k];
             const TermDesc& d = op->afams[term_af[k]];
-            t.af_off = d.s_pool + (t.s[0] + t.o_lo[0] - d.s[0]) * c.W;
+            const int64_t line0 = D == 2 ? t.s[0] + t.o_lo[0] - d.s[0]
+                                         : (t.s[0] + t.o_lo[0] - d.s[0]) * d.P1 + (t.s[1] + t.o_lo[1] - d.s[1]);
+            t.af_off = d.s_pool + line0 * c.W;
             t.af_vst = d.s_vst;
+            t.af_ps = D == 3 ? d.P1 : 0;
         }
         for (int k : c.terms) {
             if (term_pf[k] < 0) continue;
