@@ -154,7 +154,9 @@ cudaError_t launch_block_direct(const EntryArgs& a, int32_t nblk, int64_t max_t,
                                 const int64_t* g_off, const double* f, double* g, int adjoint, int32_t* bad,
                                 cudaStream_t st);
 
-// estimator reductions (K5): per (box, probe) sums of (Yt - Y)^2 and Y^2
+// estimator reductions (K5): per (box, probe) sums of (Yt - Y)^2, and whole-domain (Yt - Y)^2 and
+// Y^2 per probe (y2 needs q + probe_sums_scratch() doubles: the chunk partials follow it)
+int64_t probe_sums_scratch(int D, const int32_t* n, int32_t q);
 cudaError_t launch_probe_sums(int D, const int32_t* n, int32_t nbox, const int64_t* box_lo, const int64_t* box_hi,
                               int32_t q, const double* Yt, const double* Y, double* d2, double* y2, cudaStream_t st);
 

@@ -137,38 +137,50 @@ __global__ void k_block_direct(EntryArgs a, int32_t nblk, const int64_t* __restr
 
 // ---------------------------------------------------------------------------
 // K5 reductions: d2[box, probe] = sum_{p in box cap Omega} (Yt - Y)^2, y2[probe] = sum Y^2
-__global__ void k_probe_sums(int D, int32_t n0, int32_t n1, int32_t n2, int32_t nbox, const int64_t* __restrict__ blo,
-                             const int64_t* __restrict__ bhi, const double* __restrict__ Yt,
-                             const double* __restrict__ Y, double* d2, double* y2) {
-    const int box = blockIdx.x;  // box == nbox -> whole domain (also sums Y^2)
+// Estimator sums (K5).  CTA (x < nbox, probe): sum over leaf box x of (Yt - Y)^2.  CTA
+// (x = nbox + c, probe): chunk c of PS_CHUNK consecutive points of the whole domain, (Yt - Y)^2
+// and Y^2, into partials reduced by k_probe_total in chunk order (deterministic).
+constexpr int PS_CHUNK = 16384;
+
+__global__ void __launch_bounds__(256) k_probe_sums(int D, int32_t n0, int32_t n1, int32_t n2, int32_t nbox,
+                                                    const int64_t* __restrict__ blo, const int64_t* __restrict__ bhi,
+                                                    const double* __restrict__ Yt, const double* __restrict__ Y,
+                                                    double* d2, double* part) {
+    const int box = blockIdx.x;
     const int probe = blockIdx.y;
+    const int q = gridDim.y;
     const int32_t n[3] = {n0, n1, D == 3 ? n2 : 1};
-    int64_t lo[3] = {0, 0, 0}, hi[3] = {n0 - 1, n1 - 1, n[2] - 1};
-    if (box < nbox) {
-        for (int i = 0; i < D; ++i) {
-            lo[i] = blo[box * D + i] > 0 ? blo[box * D + i] : 0;
-            hi[i] = bhi[box * D + i] < n[i] - 1 ? bhi[box * D + i] : n[i] - 1;
-        }
-    }
-    int64_t ext[3];
-    int64_t cnt = 1;
-    for (int i = 0; i < 3; ++i) {
-        ext[i] = hi[i] >= lo[i] ? hi[i] - lo[i] + 1 : 0;
-        cnt *= ext[i];
-    }
     const int64_t N = (int64_t)n[0] * n[1] * n[2];
     const double* yt = Yt + probe * N;
     const double* yy = Y + probe * N;
     double s = 0.0, sy = 0.0;
-    for (int64_t q = threadIdx.x; q < cnt; q += blockDim.x) {
-        const int64_t i2 = q % ext[2];
-        const int64_t r = q / ext[2];
-        const int64_t i1 = r % ext[1];
-        const int64_t i0 = r / ext[1];
-        const int64_t off = ((lo[0] + i0) * n[1] + lo[1] + i1) * n[2] + lo[2] + i2;
-        const double dv = yt[off] - yy[off];
-        s += dv * dv;
-        sy += yy[off] * yy[off];
+    if (box < nbox) {
+        int64_t lo[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
+        for (int i = 0; i < D; ++i) {
+            const int64_t l = blo[box * D + i] > 0 ? blo[box * D + i] : 0;
+            const int64_t h = bhi[box * D + i] < n[i] - 1 ? bhi[box * D + i] : n[i] - 1;
+            lo[i] = l;
+            ext[i] = h >= l ? h - l + 1 : 0;
+        }
+        const int ax = D - 1;  // rows of the box along the last axis: one division per row
+        const int64_t rows = D == 3 ? ext[0] * ext[1] : ext[0];
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int64_t r = warp; r < rows; r += blockDim.x >> 5) {
+            const int64_t r0 = D == 3 ? r / ext[1] : r, r1 = D == 3 ? r - (r / ext[1]) * ext[1] : 0;
+            const int64_t base = D == 3 ? ((lo[0] + r0) * n[1] + lo[1] + r1) * n[2] + lo[2] : (lo[0] + r0) * n[1] + lo[1];
+            for (int64_t c = lane; c < ext[ax]; c += 32) {
+                const double dv = yt[base + c] - yy[base + c];
+                s += dv * dv;
+            }
+        }
+    } else {
+        const int64_t c0 = (int64_t)(box - nbox) * PS_CHUNK;
+        const int64_t c1 = c0 + PS_CHUNK < N ? c0 + PS_CHUNK : N;
+        for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+            const double dv = yt[i] - yy[i];
+            s += dv * dv;
+            sy += yy[i] * yy[i];
+        }
     }
     __shared__ double red[2][256];
     red[0][threadIdx.x] = s;
@@ -182,9 +194,28 @@ __global__ void k_probe_sums(int D, int32_t n0, int32_t n1, int32_t n2, int32_t 
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        d2[(int64_t)box * gridDim.y + probe] = red[0][0];
-        if (box == nbox) y2[probe] = red[1][0];
+        if (box < nbox) {
+            d2[(int64_t)box * q + probe] = red[0][0];
+        } else {
+            const int64_t c = box - nbox;
+            part[(c * q + probe) * 2] = red[0][0];
+            part[(c * q + probe) * 2 + 1] = red[1][0];
+        }
     }
+}
+
+// whole-domain sums per probe from the chunk partials, in chunk order
+__global__ void k_probe_total(int32_t nbox, int32_t q, int64_t nchunk, const double* __restrict__ part, double* d2,
+                              double* y2) {
+    const int probe = blockIdx.x * blockDim.x + threadIdx.x;
+    if (probe >= q) return;
+    double s = 0.0, sy = 0.0;
+    for (int64_t c = 0; c < nchunk; ++c) {
+        s += part[(c * q + probe) * 2];
+        sy += part[(c * q + probe) * 2 + 1];
+    }
+    d2[(int64_t)nbox * q + probe] = s;
+    y2[probe] = sy;
 }
 
 __global__ void k_zero(double* p, int64_t n) {
@@ -444,8 +475,14 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
 
 cudaError_t launch_probe_sums(int D, const int32_t* n, int32_t nbox, const int64_t* box_lo, const int64_t* box_hi,
                               int32_t q, const double* Yt, const double* Y, double* d2, double* y2, cudaStream_t st) {
-    dim3 grid((unsigned)(nbox + 1), (unsigned)q);
-    k_probe_sums<<<grid, 256, 0, st>>>(D, n[0], n[1], D == 3 ? n[2] : 1, nbox, box_lo, box_hi, Yt, Y, d2, y2);
+    // chunk partials live behind the q whole-domain y2 slots of the caller's buffer (see
+    // probe_sums_scratch)
+    const int64_t N = (int64_t)n[0] * n[1] * (D == 3 ? n[2] : 1);
+    const int64_t nchunk = (N + PS_CHUNK - 1) / PS_CHUNK;
+    double* part = y2 + q;
+    dim3 grid((unsigned)(nbox + nchunk), (unsigned)q);
+    k_probe_sums<<<grid, 256, 0, st>>>(D, n[0], n[1], D == 3 ? n[2] : 1, nbox, box_lo, box_hi, Yt, Y, d2, part);
+    k_probe_total<<<(q + 127) / 128, 128, 0, st>>>(nbox, q, nchunk, part, d2, y2);
     return cudaGetLastError();
 }
 
@@ -457,6 +494,11 @@ cudaError_t launch_block_direct(const EntryArgs& a, int32_t nblk, int64_t max_t,
     dim3 grid((unsigned)((max_t + 255) / 256), (unsigned)nblk);
     k_block_direct<<<grid, 256, 0, st>>>(a, nblk, t_lo, t_hi, s_lo, s_hi, f_off, g_off, f, g, adjoint, bad);
     return cudaGetLastError();
+}
+
+int64_t probe_sums_scratch(int D, const int32_t* n, int32_t q) {
+    const int64_t N = (int64_t)n[0] * n[1] * (D == 3 ? n[2] : 1);
+    return 2 * ((N + PS_CHUNK - 1) / PS_CHUNK) * (int64_t)q;
 }
 
 cudaError_t launch_zero(double* p, int64_t n, cudaStream_t st) {

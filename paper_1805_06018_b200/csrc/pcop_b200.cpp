@@ -2236,7 +2236,7 @@ static void estimate_common(pcb_op* op, int32_t q, const double* dZ, const doubl
     op->st_i64a.ensure(std::max<size_t>(1, blo.size()));
     op->st_i64b.ensure(std::max<size_t>(1, bhi.size()));
     const size_t nd2 = (size_t)(nleaf + 1) * q;
-    op->st_aux.ensure(nd2 + q);
+    op->st_aux.ensure(nd2 + q + probe_sums_scratch(op->D, op->n, q));
     if (!blo.empty()) {
         PCB_CK(cudaMemcpyAsync(op->st_i64a.p, blo.data(), blo.size() * 8, cudaMemcpyHostToDevice, st));
         PCB_CK(cudaMemcpyAsync(op->st_i64b.p, bhi.data(), bhi.size() * 8, cudaMemcpyHostToDevice, st));
@@ -2355,7 +2355,7 @@ void est_sums(pcb_estimator* e, int32_t nleaf, const int64_t* leaf_lo, const int
     e->blo.ensure(std::max<size_t>(1, lo.size()));
     e->bhi.ensure(std::max<size_t>(1, hi.size()));
     const size_t nd2 = (size_t)(nleaf + 1) * e->q;
-    e->aux.ensure(nd2 + e->q);
+    e->aux.ensure(nd2 + e->q + probe_sums_scratch(e->D, e->n, e->q));
     if (!lo.empty()) {
         PCB_CK(cudaMemcpyAsync(e->blo.p, lo.data(), lo.size() * 8, cudaMemcpyHostToDevice, e->stream));
         PCB_CK(cudaMemcpyAsync(e->bhi.p, hi.data(), hi.size() * 8, cudaMemcpyHostToDevice, e->stream));
