@@ -40,6 +40,9 @@
 #ifndef PCB_BUNDLE_XPF
 #define PCB_BUNDLE_XPF 1  // 1: next batch's headers and first members issued before this batch's C2R
 #endif
+#ifndef PCB_SLS_CF
+#define PCB_SLS_CF 1  // conflict-free staged-line stride in the gathers
+#endif
 #ifndef PCB_RINV_ALIAS
 #define PCB_RINV_ALIAS 1  // per-entry gather: split straight into registers, stage doubles as FFT buffer
 #endif
@@ -86,7 +89,11 @@ __host__ __device__ constexpr int stage_stride_b() {
     constexpr int words = SmemLine<N, NL, PSH<NL>>::WORDS;
     constexpr int xsw = (NL * (2 * N + 1) + 1) / 2;
     constexpr int need = words > xsw ? words : xsw;
-    return (N + 1) * NL >= need ? N + 1 : (need + NL - 1) / NL;
+    constexpr int base = (N + 1) * NL >= need ? N + 1 : (need + NL - 1) / NL;
+    // lanes l of a 128-bit quarter-warp read x[l * stride + k] for 8 / NL consecutive k: with
+    // stride = 8 / NL (mod 8) they fall in distinct bank groups (also for x[N - k])
+    constexpr int q = NL >= 8 ? 1 : 8 / NL;
+    return PCB_SLS_CF ? base + ((q - base % 8) % 8 + 8) % 8 : base;
 }
 
 template <int LEN>
