@@ -258,16 +258,25 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
     // phase 3: even/odd split X[k] = A[k] + W^k B[k], k = 0..N
     const double2* twP = twtab<2 * N>(a.tw);
     double2* S_item = MODE == RF_SPEC ? a.S + (int64_t)item * a.S_stride : a.S + td.s_pool + vec * td.s_vst;
-    for (int idx = threadIdx.x; idx < NL * (N + 1); idx += NT) {
-        const int ll = idx / (N + 1);
-        const int k = idx - ll * (N + 1);
+    // k and N - k from the same two loads: A(N-k) = conj A(k), B(N-k) = conj B(k) exactly (IEEE
+    // sums commute, negation is exact), so X[N-k] = conj A + W^(N-k) conj B; k = 0 also gives X[N]
+    constexpr int NH = N / 2 + 1;
+    for (int idx = threadIdx.x; idx < NL * NH; idx += NT) {
+        const int ll = idx / NH;
+        const int k = idx - ll * NH;
         const int64_t row = m_row[ll];
         if (row < 0) continue;
-        const double2 zk = buf[sidx<NL, PS>(k == N ? 0 : k, ll)];
+        const double2 zk = buf[sidx<NL, PS>(k, ll)];
         const double2 zn = buf[sidx<NL, PS>(k == 0 ? 0 : N - k, ll)];
         const double2 A = make_double2(0.5 * (zk.x + zn.x), 0.5 * (zk.y - zn.y));
         const double2 Bm = make_double2(0.5 * (zk.y + zn.y), -0.5 * (zk.x - zn.x));  // (zk - conj zn)/(2i)
         S_item[row + k] = cadd(A, cmul(__ldg(&twP[k]), Bm));
+        if (k == 0) {
+            S_item[row + N] = cadd(A, cmul(__ldg(&twP[N]), Bm));
+        } else if (2 * k != N) {
+            const double2 Ac = make_double2(A.x, -A.y), Bc = make_double2(Bm.x, -Bm.y);
+            S_item[row + N - k] = cadd(Ac, cmul(__ldg(&twP[N - k]), Bc));
+        }
     }
 }
 
