@@ -15,7 +15,7 @@ cudaError_t cols_p(const PassArgs& a, cudaStream_t st) {
     const size_t stage = (P0 <= PCB_LOCAL_STAGE && (MODE == CM_APPLY_LOCAL || MODE == CM_ADJ_LOCAL)) ? (size_t)P0 * NL
                          : (MODE == CM_APPLY_GLOBAL || (MODE == CM_APPLY_CHAIN && PCB_CHAIN_STAGE)) ? (P0 <= 512 ? (size_t)P0 * NL : 0)
                          : MODE == CM_ADJ_GLOBAL ? 2 * (size_t)P0 * NL : 0;
-    const size_t smem = sizeof(double2) * (smem_words<P0, NL>() + stage);
+    const size_t smem = sizeof(double2) * (smem_words_c<P0, NL>() + stage);
     return launch_dyn(k_cols<P0, NL, MODE>, grid, dim3(NL * FftCfg<P0>::TPL), smem, st, a);
 }
 

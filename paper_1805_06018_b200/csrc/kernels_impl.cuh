@@ -40,6 +40,9 @@
 #ifndef PCB_BUNDLE_XPF
 #define PCB_BUNDLE_XPF 1  // 1: next batch's headers and first members issued before this batch's C2R
 #endif
+#ifndef PCB_COLS_PS4
+#define PCB_COLS_PS4 1  // column pass with 4-line tiles: one pad word per 16 (conflict-free stores)
+#endif
 #ifndef PCB_SLS_CF
 #define PCB_SLS_CF 1  // conflict-free staged-line stride in the gathers
 #endif
@@ -105,6 +108,15 @@ __device__ __forceinline__ const double2* twtab(const double2* tw) {
 template <int LEN, int NL>
 constexpr int smem_words() {
     return SmemLine<LEN, NL, PSH<NL>>::WORDS;
+}
+
+// pad shift of the column pass: with 4 lines per tile its first forward and first inverse stages
+// store stride-16 runs (64 words apart), which one pad per 8 words maps onto the same banks
+template <int NL>
+constexpr int PSC = (PCB_COLS_PS4 && NL == 4) ? 4 : PSH<NL>;
+template <int LEN, int NL>
+constexpr int smem_words_c() {
+    return SmemLine<LEN, NL, PSC<NL>>::WORDS;
 }
 
 // number of lines of one item for the rows_fwd pass
@@ -441,7 +453,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
         // LOCAL: the term's spectrum tile streams into shared memory while the S rows load and the
         // forward FFT runs (no registers held for it until the multiply)
         constexpr bool LSTAGE = MODE != CM_SPEC && P0 <= PCB_LOCAL_STAGE;
-        double2* sspec = buf + smem_words<P0, NL>();
+        double2* sspec = buf + smem_words_c<P0, NL>();
         if (LSTAGE) {
             const double2* tile = a.spec_pool + td.spec_off + (c0 / NL) * (int64_t)P0 * NL;
             for (int i = threadIdx.x; i < P0 * NL; i += NL * FftCfg<P0>::TPL) cp_async16(&sspec[i], tile + i);
@@ -469,7 +481,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
             }
         }
         else load_in(a.D == 2 && td.af_off >= 0 ? a.S + td.af_off + vec * td.af_vst : S_item, td.o_lo[0], td.o_cnt[0], v);
-        fft_fwd_order<P0, -1, NL, PSH<NL>>(v, buf, l, tl, tw0);
+        fft_fwd_order<P0, -1, NL, PSC<NL>>(v, buf, l, tl, tw0);
         double2* spec = a.spec_pool + td.spec_off + tile_off;
         if (MODE == CM_SPEC) {
             if (cvalid) {
@@ -487,7 +499,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
             const double2 ph = LSTAGE ? sspec[fpos(r) * NL + l] : cvalid ? __ldg(&spec[(int64_t)fpos(r) * NL]) : czero();
             v[r] = MODE == CM_APPLY_LOCAL ? cmul(v[r], ph) : cmulc(v[r], ph);
         }
-        fft_rev_order<P0, +1, NL, PSH<NL>>(v, buf, l, tl, tw0);
+        fft_rev_order<P0, +1, NL, PSC<NL>>(v, buf, l, tl, tw0);
         double2* T_item = a.T + td.t_pool + vec * td.t_vst;
         if (MODE == CM_APPLY_LOCAL) store_out(T_item, td.o_lo[0], td.o_cnt[0], v);
         else store_out(T_item, 0, td.m[0], v);
@@ -497,7 +509,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
     if (MODE == CM_APPLY_CHAIN) {
         // column chain: the members' products FFT(w_k f) . Phi_k (each Phi_k placed at the chain
         // origin) summed in registers, one inverse per (chain, vector, column tile)
-        double2* sspec = buf + smem_words<P0, NL>();
+        double2* sspec = buf + smem_words_c<P0, NL>();
         const int slot = item / nvec;
         const int vec = item % nvec;
         const int cid = a.slots[slot];
@@ -516,7 +528,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
                 asm volatile("cp.async.commit_group;\n" ::);
             }
             load_apply(td, vec, v);
-            fft_fwd_order<P0, -1, NL, PSH<NL>>(v, buf, l, tl, tw0);
+            fft_fwd_order<P0, -1, NL, PSC<NL>>(v, buf, l, tl, tw0);
             if (STAGE) {
                 asm volatile("cp.async.wait_group 0;\n" ::);
                 __syncthreads();
@@ -530,7 +542,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
                 }
             }
         }
-        fft_rev_order<P0, +1, NL, PSH<NL>>(acc, buf, l, tl, tw0);
+        fft_rev_order<P0, +1, NL, PSC<NL>>(acc, buf, l, tl, tw0);
         store_out(a.T + ch.t_pool + vec * ch.t_vst, ch.o_lo[0], ch.o_cnt[0], acc);
         return;
     }
@@ -538,7 +550,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
     if (MODE == CM_APPLY_GLOBAL) {
         // Phi_k tile (P0 x NL contiguous, tile-major) streamed into shared memory with async copies
         // issued before the term's forward FFT, so the HBM stream overlaps the transform
-        double2* sspec = buf + smem_words<P0, NL>();
+        double2* sspec = buf + smem_words_c<P0, NL>();
         const int vec = item;
         double2 acc[R];
 #pragma unroll
@@ -554,7 +566,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
             }
             const double2* S_item = a.S + td.s_pool + vec * td.s_vst;
             load_in(S_item, 0, td.m[0], v);
-            fft_fwd_order<P0, -1, NL, PSH<NL>, true>(v, buf, l, tl, tw0, td.m[0]);
+            fft_fwd_order<P0, -1, NL, PSC<NL>, true>(v, buf, l, tl, tw0, td.m[0]);
             if (STAGE) {
                 asm volatile("cp.async.wait_group 0;\n" ::);
                 __syncthreads();
@@ -568,7 +580,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
                 }
             }
         }
-        fft_rev_order<P0, +1, NL, PSH<NL>>(acc, buf, l, tl, tw0);
+        fft_rev_order<P0, +1, NL, PSC<NL>>(acc, buf, l, tl, tw0);
         const TermDesc& g = *a.gdesc;
         store_out(a.T + g.t_pool + vec * g.t_vst, g.o_lo[0], g.o_cnt[0], acc);
         return;
@@ -577,7 +589,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
     // CM_ADJ_GLOBAL: one forward transform of g, one pruned inverse per term; Phi_{k+1}'s tile
     // streams into the other shared buffer while term k's inverse runs
     {
-        double2* sspec = buf + smem_words<P0, NL>();
+        double2* sspec = buf + smem_words_c<P0, NL>();
         const int vec = item;
         const TermDesc& g = *a.gdesc;
         double2 x[R];
@@ -590,7 +602,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
             asm volatile("cp.async.commit_group;\n" ::);
         };
         if (a.n_slots > 0) issue(0);
-        fft_fwd_order<P0, -1, NL, PSH<NL>>(x, buf, l, tl, tw0);
+        fft_fwd_order<P0, -1, NL, PSC<NL>>(x, buf, l, tl, tw0);
         for (int slot = 0; slot < a.n_slots; ++slot) {
             const TermDesc& td = a.terms[a.slots[slot]];
             asm volatile("cp.async.wait_group 0;\n" ::);
@@ -599,7 +611,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(Pa
             const double2* sp = sspec + (slot & 1) * P0 * NL;
 #pragma unroll
             for (int r = 0; r < R; ++r) v[r] = cmulc(x[r], sp[fpos(r) * NL + l]);
-            fft_rev_order<P0, +1, NL, PSH<NL>>(v, buf, l, tl, tw0);
+            fft_rev_order<P0, +1, NL, PSC<NL>>(v, buf, l, tl, tw0);
             store_out(a.T + td.t_pool + vec * td.t_vst, 0, td.m[0], v);
         }
     }
