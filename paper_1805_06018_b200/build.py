@@ -30,7 +30,8 @@ E3_MID = os.environ.get("PCB_E3_MID", "12")  # 3-smooth engines: 12 elements per
 E3_COLS = os.environ.get("PCB_E3_COLS", "24")  # 3-smooth engines of the cols pass
 E3_COLS_SMALL = os.environ.get("PCB_E3_COLS_SMALL", "96")  # cols: 3-smooth lengths <= this use 12 per thread
 E_COLS_SMALL = os.environ.get("PCB_E_COLS_SMALL", "64")  # cols: pow2 lengths <= this use 8 elements per thread
-PER_SOURCE = {"kernels_rows.cu": [f"-DPCB_E2={E_ROWS}"],
+RADIX_DESC_ROWS = os.environ.get("PCB_RADIX_DESC_ROWS", "1")  # rows: prefix radices largest first
+PER_SOURCE = {"kernels_rows.cu": [f"-DPCB_E2={E_ROWS}", f"-DPCB_RADIX_DESC={RADIX_DESC_ROWS}"],
               "kernels_cols.cu": [f"-DPCB_E2={E_COLS}", f"-DPCB_E2_SMALL_MAX={E_COLS_SMALL}", f"-DPCB_E3={E3_COLS}",
                                   f"-DPCB_E3_SMALL_MAX={E3_COLS_SMALL}"],
               "kernels_mid.cu": [f"-DPCB_E2={E_MID}", f"-DPCB_E3={E3_MID}"]}

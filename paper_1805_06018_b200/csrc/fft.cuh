@@ -32,6 +32,9 @@
 #ifndef PCB_E2_SMALL_MAX
 #define PCB_E2_SMALL_MAX 0  // power-of-two lengths <= this use 8 elements per thread (0: none)
 #endif
+#ifndef PCB_RADIX_DESC
+#define PCB_RADIX_DESC 0  // 1: prefix stage radices in descending order
+#endif
 #ifndef PCB_E3_SMALL_MAX
 #define PCB_E3_SMALL_MAX 0  // 3-smooth lengths <= this use 12 elements per thread (0: none)
 #endif
@@ -41,7 +44,8 @@
 namespace pcb {
 // the engine is instantiated per element count: distinct names per translation unit setting
 inline namespace PCB_NS_CAT(PCB_NS_CAT(PCB_NS_CAT(e, PCB_E2), PCB_NS_CAT(_, PCB_E3)),
-                            PCB_NS_CAT(PCB_NS_CAT(_s, PCB_E2_SMALL_MAX), PCB_NS_CAT(_t, PCB_E3_SMALL_MAX))) {
+                            PCB_NS_CAT(PCB_NS_CAT(PCB_NS_CAT(_s, PCB_E2_SMALL_MAX), PCB_NS_CAT(_t, PCB_E3_SMALL_MAX)),
+                                       PCB_NS_CAT(_d, PCB_RADIX_DESC))) {
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -206,10 +210,11 @@ struct FftCfg {
             f[n++] = p;
             rest /= p;
         }
-        // ascending prefix order keeps the first stage the smallest radix
+        // ascending prefix order keeps the first stage the smallest radix (PCB_RADIX_DESC: the
+        // largest first -- its stride-RS shared-memory stores are RS * NL words apart)
         for (int i = 0; i < n; ++i)
             for (int j = i + 1; j < n; ++j)
-                if (f[j] < f[i]) {
+                if (PCB_RADIX_DESC ? f[j] > f[i] : f[j] < f[i]) {
                     const int t = f[i];
                     f[i] = f[j];
                     f[j] = t;
