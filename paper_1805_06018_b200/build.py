@@ -47,13 +47,17 @@ def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(OBJDIR, os.path.splitext(src)[0] + ".o")
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS] + \
         [os.path.join(ROOT, "include", "pcb", "pcb.h")]
-    if os.path.exists(obj) and os.path.getmtime(obj) >= _newest(deps):
-        return obj
     lang = [] if src.endswith(".cu") else ["-x", "cu"]
     cmd = [NVCC] + ARCH + COMMON + EXTRA + PER_SOURCE.get(src, []) + lang + ["-c", os.path.join(CSRC, src), "-o", obj]
+    stamp = obj + ".cmd"  # the object is stale when its sources are newer or its command changed
+    if (os.path.exists(obj) and os.path.getmtime(obj) >= _newest(deps) and os.path.exists(stamp)
+            and open(stamp).read() == " ".join(cmd)):
+        return obj
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
+    with open(stamp, "w") as f:
+        f.write(" ".join(cmd))
     return obj
 
 
