@@ -40,6 +40,9 @@
 #ifndef PCB_BUNDLE_XPF
 #define PCB_BUNDLE_XPF 1  // 1: next batch's headers and first members issued before this batch's C2R
 #endif
+#ifndef PCB_COLS_MINB_SMALL
+#define PCB_COLS_MINB_SMALL 10  // min CTAs/SM of the column pass for lengths <= 64 (96 registers; c4 cols -5%)
+#endif
 #ifndef PCB_COLS_PS4
 #define PCB_COLS_PS4 1  // column pass with 4-line tiles: one pad word per 16 (conflict-free stores)
 #endif
@@ -385,7 +388,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P1>::TPL) k_mid(PassArgs a) {
 // ---------------------------------------------------------------------------
 // cols: axis-0 pass with the frequency-domain product (K3).
 template <int P0, int NL, int MODE>
-__global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, PCB_COLS_MINB) k_cols(PassArgs a) {
+__global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, P0 <= 64 ? PCB_COLS_MINB_SMALL : PCB_COLS_MINB) k_cols(PassArgs a) {
     constexpr int R = FftCfg<P0>::R;
     constexpr int RF = FirstPos<P0>::RF;
     constexpr int RL = LastPos<P0>::RL;
