@@ -61,6 +61,9 @@
 #ifndef PCB_ROWS_MINB_MIXED
 #define PCB_ROWS_MINB_MIXED 1
 #endif
+#ifndef PCB_ROWS_MINB_SHORT3
+#define PCB_ROWS_MINB_SHORT3 16  // short 3-smooth rows (N <= 48, one thread per line): c4 rows_inv -13%
+#endif
 #ifndef PCB_CHAIN_STAGE
 #define PCB_CHAIN_STAGE 1  // column chains: stage each member's spectrum tile in shared memory
 #endif
@@ -156,7 +159,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // w_k . f on the footprint window, ADJ gathers g on the output window (both
 // staged through shared memory with cp.async), SPEC places the trimmed kernel.
 template <int N, int NL, int MODE>
-__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_MINB : PCB_ROWS_MINB_MIXED) k_rows_fwd(PassArgs a) {
+__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_MINB : (N <= 48 ? PCB_ROWS_MINB_SHORT3 : PCB_ROWS_MINB_MIXED)) k_rows_fwd(PassArgs a) {
     constexpr int R = FftCfg<N>::R;
     constexpr int RF = FirstPos<N>::RF;
     constexpr int NT = NL * FftCfg<N>::TPL;
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, P0 <= 64 ? PCB_COLS_MINB
 // output positions p = t mod blockDim, so contributions to one position are
 // added by one thread in ascending entry order (deterministic, no atomics).
 template <int N, int NL, int MODE>
-__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_MINB : PCB_ROWS_MINB_MIXED) k_rows_inv(PassArgs a) {
+__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_MINB : (N <= 48 ? PCB_ROWS_MINB_SHORT3 : PCB_ROWS_MINB_MIXED)) k_rows_inv(PassArgs a) {
     constexpr int R = FftCfg<N>::R;
     constexpr int RL = LastPos<N>::RL;
     constexpr int NT = NL * FftCfg<N>::TPL;
@@ -754,7 +757,7 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
 // scaled by A_k(line) / prod P (no phase: one placement), summed, transformed once, and the
 // result multiplied by the family's last-axis weight row c (header w_off) as it accumulates.
 template <int N, int NL, int ADJ>
-__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_MINB_B : PCB_ROWS_MINB_MIXED)
+__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_MINB_B : (N <= 48 ? PCB_ROWS_MINB_SHORT3 : PCB_ROWS_MINB_MIXED))
     k_rows_inv_b(PassArgs a) {
     constexpr int R = FftCfg<N>::R;
     constexpr int RL = LastPos<N>::RL;
