@@ -1974,7 +1974,7 @@ static pcb_status apply_host_common(pcb_op* op, bool adjoint, int32_t B, const d
         // unoverlapped fill (first H2D) and drain (last D2H) stay short.
         static const double sub_mb = [] {
             const char* e = std::getenv("PCB_SUB_MB");
-            return e ? std::max(1.0, std::atof(e)) : 32.0;  // c3 sweep 16-64 MiB (scripts/e2e_sweep.sh): 24-32 best
+            return e ? std::max(1.0, std::atof(e)) : 16.0;  // c3 sweep 8-64 MiB (scripts/e2e_sweep.sh): 16 best
         }();
         const double vec_mb = (double)op->N * 8.0 / (1 << 20);
         const int per = (int)std::max(1.0, std::floor(sub_mb / vec_mb));
