@@ -1977,7 +1977,7 @@ static pcb_status apply_host_common(pcb_op* op, bool adjoint, int32_t B, const d
             return e ? std::max(1.0, std::atof(e)) : 16.0;  // c3 sweep 8-64 MiB (scripts/e2e_sweep.sh): 16 best
         }();
         const double vec_mb = (double)op->N * 8.0 / (1 << 20);
-        const int per = (int)std::max(1.0, std::floor(sub_mb / vec_mb));
+        const int per = (int)std::max(2.0, std::floor(sub_mb / vec_mb));  // >= 2 vectors per kernel batch
         std::vector<int> sizes;
         if (B <= per) {
             sizes.push_back(B);
