@@ -53,14 +53,36 @@ typedef enum pcb_mode {
 
 typedef struct pcb_op pcb_op;
 
+/* Shard-by-k combine: how the ranks' partial outputs are summed when the handle
+ * has a communicator (pcb_options.nccl_id). */
+typedef enum pcb_reduce {
+    PCB_REDUCE_NONE = 0, /* no combine: apply returns this shard's partial sum */
+    PCB_REDUCE_ALL = 1,  /* ncclAllReduce: every rank gets the full apply */
+    PCB_REDUCE_ROOT = 2  /* ncclReduce: shard 0 gets the full apply (others keep their partial) */
+} pcb_reduce;
+
+/* How the active terms are split into contiguous shards. */
+typedef enum pcb_partition {
+    PCB_PARTITION_COST = 0, /* balanced by the planner's modelled per-term cost (default) */
+    PCB_PARTITION_COUNT = 1 /* balanced by term count */
+} pcb_partition;
+
 typedef struct pcb_options {
     int32_t device;        /* CUDA device ordinal; -1 = current device */
     int32_t mode;          /* pcb_mode */
     int32_t max_batch;     /* vectors per internal pass; 0 = default (16) */
     int32_t shard_rank;    /* shard-by-k: this process owns terms of shard_rank ... */
-    int32_t shard_count;   /* ... out of shard_count (1 = unsharded); apply returns the partial sum */
-    int32_t reserved;
+    int32_t shard_count;   /* ... out of shard_count (1 = unsharded) */
+    int32_t reduce;        /* pcb_reduce: the combine done inside every apply when nccl_id is set */
     int64_t scratch_bytes; /* scratch budget for pipelined passes; 0 = default */
+    /* 128-byte ncclUniqueId (pcb_comm_unique_id on one rank, sent to the others by the caller).
+     * With it, pcb_create joins an NCCL communicator of shard_count ranks (collective: every shard
+     * calls pcb_create with the same id) and every apply / adjoint / estimator call becomes
+     * collective, combining the shards' partials as `reduce` says over NVLink, pipelined with the
+     * kernels of the next vector chunk.  NULL: no communicator; apply returns the partial. */
+    const void* nccl_id;
+    int32_t partition;     /* pcb_partition */
+    int32_t host_sub_mb;   /* host-buffer calls: MiB per pipelined H2D / kernels / D2H sub-batch; 0 = 16 */
 } pcb_options;
 
 typedef struct pcb_info {
@@ -84,9 +106,30 @@ typedef struct pcb_info {
     double kernel_flops[4];
     int32_t n_column_chains; /* 2-D LOCAL apply: column chains (terms sharing one axis-0 inverse) */
     int32_t n_chained_terms; /* terms in chains of two or more */
+    int32_t shard_rank, shard_count;
+    int32_t comm_nranks;     /* ranks of the handle's NCCL communicator (0: none) */
+    int32_t comm_version;    /* NCCL version code of the loaded library (0: none) */
+    int32_t term_lo, term_hi; /* this shard owns the active terms with index in [term_lo, term_hi) (reference k) */
+    double shard_cost;       /* modelled cost of this shard's terms (s, at the planner's roofs) */
+    double total_cost;       /* modelled cost of all active terms */
+    double model_ms_local;   /* planner's modelled time per vector of this shard, LOCAL plan */
+    double model_ms_global;  /* ... GLOBAL plan */
 } pcb_info;
 
 PCB_API void pcb_default_options(pcb_options* opt);
+
+/* A fresh 128-byte ncclUniqueId for pcb_options.nccl_id (call on one rank; NCCL is dlopen'ed at
+ * run time, PCB_ENCCL when it is absent). */
+PCB_API pcb_status pcb_comm_unique_id(void* id128);
+
+/* The planner's shard partition, host only (no device needed; the same inputs as pcb_create):
+ * owner[k] = the shard that owns term k (-1: inactive -- no footprint in the domain or an all-zero
+ * kernel window), cost[k] = its modelled cost (s per vector); either may be NULL.  pcb_create with
+ * shard_rank = s keeps exactly the terms with owner[k] == s. */
+PCB_API pcb_status pcb_plan_shards(int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t r,
+                                   const int64_t* w_lo, const int64_t* w_hi, const double* const* w_vals,
+                                   const int64_t* phi_lo, const int64_t* phi_hi, const double* const* phi_vals,
+                                   int32_t shard_count, int32_t partition, int32_t* owner, double* cost);
 PCB_API const char* pcb_last_error(void);
 
 /* Replaces ProductConvolutionOperator(domain, grid, weights, impulses)

@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -275,6 +276,17 @@ int ref_estimate(void* h, int q, const double* Z, const double* Y, int nleaf,
             for (const auto& df : st.diff) s += squared_norm_on_box(df, leaf);
             eta_cells[c] = std::sqrt(s / st.q);
         }
+    });
+}
+
+// The reference's vector / probe stream (adaptivity.cpp:19-23, test_pc_operator.cpp:13-18):
+// std::mt19937_64(seed) + std::normal_distribution<double>(0, 1), count draws.  Lets the
+// reference arm of bench.py draw its inputs without loading the product library.
+int ref_normal_fill(std::uint64_t seed, std::int64_t count, double* out) {
+    return guarded([&] {
+        std::mt19937_64 gen(seed);
+        std::normal_distribution<double> nd(0.0, 1.0);
+        for (std::int64_t i = 0; i < count; ++i) out[i] = nd(gen);
     });
 }
 

@@ -40,6 +40,7 @@ def lib():
         L.ref_apply_batch_threads.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _dp, _dp, ctypes.c_int]
         L.ref_entries.argtypes = [ctypes.c_void_p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _dp]
         L.ref_apply_block.argtypes = [ctypes.c_void_p] + [ctypes.POINTER(_i64)] * 4 + [_dp, ctypes.c_int, _dp]
+        L.ref_normal_fill.argtypes = [ctypes.c_uint64, _i64, _dp]
         L.ref_estimate.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _dp, ctypes.c_int, ctypes.POINTER(_i64),
                                    ctypes.POINTER(_i64), _dp, _dp, _dp, _dp]
         _lib = L
@@ -140,6 +141,50 @@ class RefOperator:
                                   hi.ctypes.data_as(ctypes.POINTER(_i64)), _dptr(yt), _dptr(cells),
                                   ctypes.byref(ea), ctypes.byref(er)))
         return yt, cells, ea.value, er.value
+
+
+def normal_vectors(seed: int, count: int, n: int) -> np.ndarray:
+    """count x n draws of std::mt19937_64(seed) + std::normal_distribution<double>
+    (adaptivity.cpp:19-23), drawn inside the reference build (no product library loaded)."""
+    out = np.empty(count * n)
+    _check(lib().ref_normal_fill(ctypes.c_uint64(seed), count * n, _dptr(out)))
+    return out.reshape(count, n)
+
+
+def apply_split(inp, F: np.ndarray, adjoint: bool = False, threads: int = 0) -> np.ndarray:
+    """The reference apply / apply_adjoint (pc_operator.cpp:45-69) of the FULL operator, with its
+    serial k-loop split across host threads: thread t owns the terms k = t, t+T, t+2T, ... as its
+    own reference ProductConvolutionOperator and the partial outputs are summed (linearity of the
+    k-sum).  Each thread runs the unmodified reference routine; only the order of the final sum
+    over threads differs from the reference's single ascending-k accumulation (rounding ~1e-16).
+    ctypes releases the GIL during the calls, so the threads run concurrently."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    F = np.atleast_2d(np.ascontiguousarray(F, dtype=np.float64))
+    T = max(1, min(threads or (os.cpu_count() or 1), inp.rank))
+    parts = [list(range(t, inp.rank, T)) for t in range(T)]
+    ops = [RefOperator(inp, ks=p) for p in parts]
+    out = np.zeros_like(F)
+    for b in range(F.shape[0]):
+        with ThreadPoolExecutor(T) as ex:
+            res = list(ex.map(lambda o: o.apply(F[b], adjoint=adjoint), ops))
+        for r in res:  # fixed thread order: deterministic
+            out[b] += r
+    return out
+
+
+def entries_split(op: "RefOperator", y: np.ndarray, x: np.ndarray, threads: int = 0) -> np.ndarray:
+    """Reference entry (pc_operator.cpp:84-96) for many (y, x) pairs, chunked across host threads
+    (entry is pure and thread-safe, pc_operator.hpp:15-16).  Every value is the reference's own."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    y = np.ascontiguousarray(y, dtype=np.int64).reshape(-1, op.dim)
+    x = np.ascontiguousarray(x, dtype=np.int64).reshape(-1, op.dim)
+    T = max(1, threads or (os.cpu_count() or 1))
+    cuts = np.linspace(0, y.shape[0], T + 1).astype(np.int64)
+    with ThreadPoolExecutor(T) as ex:
+        res = list(ex.map(lambda i: op.entries(y[cuts[i]:cuts[i + 1]], x[cuts[i]:cuts[i + 1]]), range(T)))
+    return np.concatenate(res) if res else np.zeros(0)
 
 
 def fft_convolve(psi_lo, psi, f_lo, f):

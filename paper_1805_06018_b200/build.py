@@ -35,8 +35,8 @@ PER_SOURCE = {"kernels_rows.cu": [f"-DPCB_E2={E_ROWS}", f"-DPCB_RADIX_DESC={RADI
               "kernels_cols.cu": [f"-DPCB_E2={E_COLS}", f"-DPCB_E2_SMALL_MAX={E_COLS_SMALL}", f"-DPCB_E3={E3_COLS}",
                                   f"-DPCB_E3_SMALL_MAX={E3_COLS_SMALL}"],
               "kernels_mid.cu": [f"-DPCB_E2={E_MID}", f"-DPCB_E3={E3_MID}"]}
-SOURCES = ["kernels_rows.cu", "kernels_cols.cu", "kernels_mid.cu", "kernels_misc.cu", "blur.cu", "hmatrix.cpp", "pcop_b200.cpp"]
-HEADERS = ["fft.cuh", "kernels.cuh", "kernels_impl.cuh"]
+SOURCES = ["kernels_rows.cu", "kernels_cols.cu", "kernels_mid.cu", "kernels_misc.cu", "blur.cu", "hmatrix.cpp", "comm.cpp", "pcop_b200.cpp"]
+HEADERS = ["fft.cuh", "kernels.cuh", "kernels_impl.cuh", "comm.h"]
 
 
 def _newest(paths):
@@ -75,5 +75,43 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
+# FFT engine unit test (tests/cuda/fft_unit.cu vs a long-double DFT, every compiled length, both
+# directions, both register orders), once per element-count setting the product compiles:
+# (PCB_E2, PCB_E3, PCB_E2_SMALL_MAX, PCB_E3_SMALL_MAX, PCB_RADIX_DESC) of cols (16/24, 8 for <= 64,
+# 12 for <= 96), rows (8/24, radices largest first) and mid (8/12).  Run by tests/test_gpu_tools.py.
+FFT_UNIT_CONFIGS = [(E_COLS, E3_COLS, E_COLS_SMALL, E3_COLS_SMALL, "0"), (E_COLS, E3_COLS, "0", "0", "0"),
+                    (E_ROWS, "24", "0", "0", RADIX_DESC_ROWS), (E_ROWS, "24", "0", "0", "0"), (E_MID, E3_MID, "0", "0", "0")]
+TOOLDIR = os.path.join(ROOT, "build", "tools")
+
+
+def fft_unit_path(cfg) -> str:
+    return os.path.join(TOOLDIR, "fft_unit_" + "_".join(cfg))
+
+
+def build_tools(verbose: bool = False) -> list:
+    os.makedirs(TOOLDIR, exist_ok=True)
+    src = os.path.join(ROOT, "tests", "cuda", "fft_unit.cu")
+    deps = [src, os.path.join(CSRC, "fft.cuh")]
+
+    def one(cfg):
+        out = fft_unit_path(cfg)
+        if os.path.exists(out) and os.path.getmtime(out) >= _newest(deps):
+            return out
+        e2, e3, s2, s3, desc = cfg
+        cmd = [NVCC] + ARCH + ["-O2", "-std=c++17", "--expt-relaxed-constexpr", f"-DPCB_E2={e2}", f"-DPCB_E3={e3}",
+                               f"-DPCB_E2_SMALL_MAX={s2}", f"-DPCB_E3_SMALL_MAX={s3}", f"-DPCB_RADIX_DESC={desc}",
+                               f"-I{CSRC}", f"-I{os.path.join(ROOT, 'include')}", src, "-o", out]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        return out
+
+    cfgs = list(dict.fromkeys(FFT_UNIT_CONFIGS))
+    with ThreadPoolExecutor(max_workers=len(cfgs)) as ex:
+        return list(ex.map(one, cfgs))
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv))
+    if "--tools" in sys.argv:
+        print(build_tools(verbose="-v" in sys.argv))

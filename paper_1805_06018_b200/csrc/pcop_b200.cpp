@@ -35,6 +35,9 @@
 #include <string>
 #include <vector>
 
+#include <thread>
+
+#include "comm.h"
 #include "fft.cuh"
 #include "kernels.cuh"
 #include "pcb/pcb.h"
@@ -223,6 +226,8 @@ struct pcb_op {
     pcb::PlanSwitches sw;
     std::vector<pcb::TermDesc> terms;
     std::vector<char> has_x, has_k, owned;
+    std::vector<int> shard_of;        // shard owning each term (-1: inactive), see pcb_plan_shards
+    std::vector<double> term_cost;    // modelled LOCAL cost per term (s per vector)
     pcb::TermDesc gdesc{};
     pcb::DevBuf<pcb::TermDesc> d_terms, d_gdesc, d_fams;
     std::vector<pcb::TermDesc> fams;  // row-family descriptors (rows_fwd items of family classes)
@@ -252,10 +257,21 @@ struct pcb_op {
         double* G;
         cudaGraphExec_t exec;
         long long launches;
+        unsigned long long used;
     };
     std::vector<GraphRec> graphs;
-    cudaEvent_t ev_g[2] = {nullptr, nullptr};
-    cudaEvent_t ev_io[8] = {};
+    unsigned long long graph_clock = 0;
+    long long graph_captures = 0;   // graphs instantiated over the handle's life (pcb_get_stats)
+    cudaEvent_t ev_x[8] = {};       // bridging / completion events (op_event)
+    cudaEvent_t ev_io[8] = {};      // host pipeline
+    double host_sub_mb = 16.0;
+    double* bounce = nullptr;       // pinned bounce slots for pageable host buffers (2 in, 2 out)
+    size_t bounce_n = 0;
+    // shard-by-k communicator (comm.cpp): the partial outputs are summed inside every apply
+    void* comm = nullptr;
+    int reduce = PCB_REDUCE_NONE;
+    int comm_chunks = 4;
+    cudaStream_t s_comm = nullptr;
     // entry gather
     int32_t bucket[3] = {1, 1, 1}, nb[3] = {1, 1, 1};
     pcb::DevBuf<int64_t> bucket_ptr;
@@ -637,9 +653,58 @@ void build_csr(pcb_op* op, Class& c, bool global, const std::vector<double>& ter
     }
 }
 
+// Modelled seconds per vector of one term in the LOCAL plan at the planner's effective roofs (the
+// same model the plan choice uses below): row R2C + column FFTs both ways + the product, or the
+// spectrum and S/T round trips at HBM speed, whichever is larger.
+constexpr double kModelFlops = 8e12;  // effective fp64 FFT rate of the row/column passes
+constexpr double kModelBytes = 6e12;  // effective HBM rate
+
+double local_term_cost(const pcb_op* op, const TermDesc& t) {
+    const int D = op->D;
+    int64_t P[3] = {1, 1, 1};
+    for (int a = 0; a < D; ++a) {
+        P[a] = fft_size_at_least((int64_t)t.m[a] + t.k_ext[a] - 1, a == D - 1, op->sw.mixed_last, op->sw.pow2_only);
+        if (P[a] > 4096) P[a] = 4096;
+    }
+    const double last = (double)P[D - 1];
+    const double W = last / 2 + 1;
+    const double lead = D == 2 ? (double)P[0] : (double)P[0] * P[1];
+    const double mlead = D == 2 ? t.m[0] : (double)t.m[0] * t.m[1];
+    const double fl = (mlead * 3.0) * 2.5 * last * std::log2(last) +
+                      2 * W * (D == 3 ? P[1] : 1) * 5.0 * P[0] * std::log2((double)P[0]) +
+                      (D == 3 ? 2 * W * t.m[0] * 5.0 * P[1] * std::log2((double)P[1]) : 0) + 6.0 * lead * W;
+    const double by = lead * W * 16.0 * 4.0;
+    return std::max(fl / kModelFlops, by / kModelBytes);
+}
+
+// Contiguous split of a cost sequence into `parts` blocks of near-equal cost: block s is
+// [cut[s], cut[s+1]).  Cut s is the first index whose cost prefix reaches s/parts of the total
+// (every block non-empty while there are at least `parts` items).
+std::vector<int> balanced_cuts(const std::vector<double>& cost, int parts) {
+    const int n = (int)cost.size();
+    std::vector<int> cut(parts + 1, n);
+    cut[0] = 0;
+    double total = 0.0;
+    for (double c : cost) total += std::max(0.0, c);
+    std::vector<double> pre(n + 1, 0.0);
+    for (int i = 0; i < n; ++i) pre[i + 1] = pre[i] + std::max(0.0, cost[i]);
+    int i = 0;
+    for (int s = 1; s < parts; ++s) {
+        const double target = total * s / parts;
+        if (total <= 0.0) i = (int)((int64_t)n * s / parts);
+        else
+            while (i < n && pre[i] + 0.5 * std::max(0.0, cost[i]) < target) ++i;  // the boundary nearest target
+        const int lo = std::min(cut[s - 1] + 1, n);
+        const int hi = std::max(n - (parts - s), lo);
+        cut[s] = std::min(std::max(i, lo), hi);
+        i = cut[s];
+    }
+    return cut;
+}
+
 void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t r, const int64_t* w_lo,
           const int64_t* w_hi, const double* const* w_vals, const int64_t* phi_lo, const int64_t* phi_hi,
-          const double* const* phi_vals, const pcb_options& opt) {
+          const double* const* phi_vals, const pcb_options& opt, bool geometry_only = false) {
     if (dim < 1 || dim > 3) fail(PCB_EINVAL, "pcb_create: dim must be 1, 2 or 3");
     if (r < 0) fail(PCB_EINVAL, "PCOp: one weight per impulse required");
     if (!dom_lo || !dom_hi || (r > 0 && (!w_lo || !w_hi || !w_vals || !phi_lo || !phi_hi || !phi_vals)))
@@ -765,16 +830,38 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     if (wpool.empty()) wpool.push_back(0.0);
     if (ppool.empty()) ppool.push_back(0.0);
 
-    // shard-by-k over the active terms (contiguous, balanced by count)
+    // shard-by-k over the active terms: contiguous blocks in ascending k (a contiguous block of the
+    // reference's lattice order is a spatially compact band of sample points), balanced by the
+    // modelled per-term cost of the LOCAL plan (its FFT sizes vary per term: c3's graded lattice has
+    // 11 shapes) or by count
     std::vector<int> active;
     for (int k = 0; k < r; ++k)
         if (op->has_x[k] && op->has_k[k]) active.push_back(k);
     const int sc = std::max(1, opt.shard_count);
     const int sr = opt.shard_rank;
     if (sr < 0 || sr >= sc) fail(PCB_EINVAL, "pcb_create: shard_rank out of range");
-    const size_t a0 = active.size() * (size_t)sr / sc, a1 = active.size() * (size_t)(sr + 1) / sc;
-    std::vector<int> mine(active.begin() + a0, active.begin() + a1);
+    op->term_cost.assign(r, 0.0);
+    for (int k : active) op->term_cost[k] = local_term_cost(op, op->terms[k]);
+    op->shard_of.assign(r, -1);
+    {
+        std::vector<double> c(active.size(), 1.0);
+        if (opt.partition == PCB_PARTITION_COST)
+            for (size_t i = 0; i < active.size(); ++i) c[i] = op->term_cost[active[i]];
+        const std::vector<int> cut = balanced_cuts(c, sc);
+        for (int s2 = 0; s2 < sc; ++s2)
+            for (int i = cut[s2]; i < cut[s2 + 1]; ++i) op->shard_of[active[i]] = s2;
+    }
+    std::vector<int> mine;
+    double shard_cost = 0.0, total_cost = 0.0;
+    for (int k : active) {
+        total_cost += op->term_cost[k];
+        if (op->shard_of[k] == sr) {
+            mine.push_back(k);
+            shard_cost += op->term_cost[k];
+        }
+    }
     for (int k : mine) op->owned[k] = 1;
+    if (geometry_only) return;
 
     // candidate plans
     int64_t Pg[3] = {1, 1, 1};
@@ -824,8 +911,8 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
                 (D == 3 ? 2 * W * t.m[0] * fft_flops_c((double)P[1]) : 0) + 6.0 * lead * W;
         l_by += lead * W * 16.0 * 4.0;  // spectra + forward/inverse scratch round trips
     }
-    const double g_t = std::max(g_fl / 8e12, g_by / 6e12);
-    const double l_t = std::max(l_fl / 8e12, l_by / 6e12);
+    const double g_t = std::max(g_fl / kModelFlops, g_by / kModelBytes);
+    const double l_t = std::max(l_fl / kModelFlops, l_by / kModelBytes);
     int mode = opt.mode;
     if (mode == PCB_MODE_AUTO) mode = (local_ok && (!global_ok || l_t < g_t)) ? PCB_MODE_LOCAL : PCB_MODE_GLOBAL;
     if (mode == PCB_MODE_GLOBAL && !global_ok) fail(PCB_EINVAL, "pcb_create: global FFT grid exceeds 4096 per axis");
@@ -1510,6 +1597,14 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     in.dim = dim;
     in.rank = r;
     in.rank_active = (int32_t)mine.size();
+    in.shard_rank = sr;
+    in.shard_count = sc;
+    in.term_lo = mine.empty() ? 0 : mine.front();
+    in.term_hi = mine.empty() ? 0 : mine.back() + 1;
+    in.shard_cost = shard_cost;
+    in.total_cost = total_cost;
+    in.model_ms_local = l_t * 1e3;
+    in.model_ms_global = g_t * 1e3;
     in.mode = mode;
     in.n_groups = (int32_t)op->groups.size();
     in.n_points = op->N;
@@ -1759,6 +1854,43 @@ PCB_API void pcb_default_options(pcb_options* opt) {
 
 PCB_API const char* pcb_last_error(void) { return g_err.c_str(); }
 
+PCB_API pcb_status pcb_comm_unique_id(void* id128) {
+    if (!id128) {
+        set_err("pcb_comm_unique_id: null output");
+        return PCB_EINVAL;
+    }
+    const std::string err = comm_unique_id(id128);
+    if (!err.empty()) {
+        set_err(err);
+        return PCB_ENCCL;
+    }
+    return PCB_OK;
+}
+
+PCB_API pcb_status pcb_plan_shards(int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t r,
+                                   const int64_t* w_lo, const int64_t* w_hi, const double* const* w_vals,
+                                   const int64_t* phi_lo, const int64_t* phi_hi, const double* const* phi_vals,
+                                   int32_t shard_count, int32_t partition, int32_t* owner, double* cost) {
+    return guarded([&] {
+        if (shard_count < 1) fail(PCB_EINVAL, "pcb_plan_shards: shard_count >= 1 required");
+        pcb_options opt;
+        pcb_default_options(&opt);
+        opt.shard_count = shard_count;
+        opt.partition = partition;
+        if (partition != PCB_PARTITION_COST && partition != PCB_PARTITION_COUNT)
+            fail(PCB_EINVAL, "pcb_plan_shards: bad partition");
+        std::unique_ptr<pcb_op> op(new pcb_op);
+        op->sw.mixed_last = dim == 3;  // as pcb_create
+        if (const char* e = getenv("PCB_POW2")) op->sw.pow2_only = atoi(e) != 0;
+        if (const char* e = getenv("PCB_MIXED_LAST")) op->sw.mixed_last = atoi(e) != 0;
+        plan(op.get(), dim, dom_lo, dom_hi, r, w_lo, w_hi, w_vals, phi_lo, phi_hi, phi_vals, opt, true);
+        for (int k = 0; k < r; ++k) {
+            if (owner) owner[k] = op->shard_of[k];
+            if (cost) cost[k] = op->term_cost[k];
+        }
+    });
+}
+
 PCB_API long long pcb_launch_count(void) { return g_launches.load(); }
 
 PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t r,
@@ -1806,7 +1938,21 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
         if (const char* e = getenv("PCB_CHAIN_BETA")) op->sw.chain_beta = atof(e);
         if (const char* e = getenv("PCB_CHAIN_GROW")) op->sw.chain_grow = atoi(e) != 0;
 
+        op->host_sub_mb = opt.host_sub_mb > 0 ? (double)opt.host_sub_mb : 16.0;
+        if (const char* e = getenv("PCB_SUB_MB")) op->host_sub_mb = std::max(1.0, atof(e));
+        if (const char* e = getenv("PCB_COMM_CHUNKS")) op->comm_chunks = std::max(1, atoi(e));
+        if (opt.reduce < PCB_REDUCE_NONE || opt.reduce > PCB_REDUCE_ROOT) fail(PCB_EINVAL, "pcb_create: bad reduce");
+        if (opt.partition != PCB_PARTITION_COST && opt.partition != PCB_PARTITION_COUNT)
+            fail(PCB_EINVAL, "pcb_create: bad partition");
+
         PCB_CK(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
+        if (opt.nccl_id) {  // collective: every shard joins with the same id
+            const int sc = std::max(1, opt.shard_count);
+            if (opt.shard_rank < 0 || opt.shard_rank >= sc) fail(PCB_EINVAL, "pcb_create: shard_rank out of range");
+            const std::string err = comm_init(opt.nccl_id, sc, opt.shard_rank, &op->comm);
+            if (!err.empty()) fail(PCB_ENCCL, err);
+            op->reduce = opt.reduce;
+        }
 
         make_twiddles(op);
         plan(op, dim, dom_lo, dom_hi, r, w_lo, w_hi, w_vals, phi_lo, phi_hi, phi_vals, opt);
@@ -1815,6 +1961,8 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
                      op->S.bytes() + op->T.bytes() + op->d_terms.bytes() + op->bucket_ptr.bytes() +
                      op->bucket_terms.bytes();
         op->info.device_bytes = (int64_t)dev;
+        op->info.comm_nranks = op->comm ? std::max(1, opt.shard_count) : 0;
+        op->info.comm_version = op->comm ? comm_version() : 0;
     });
     if (st != PCB_OK) {
         pcb_destroy(op);
@@ -1837,8 +1985,14 @@ PCB_API pcb_status pcb_destroy(pcb_op* op) {
     }
     for (auto e : op->ev_pool) cudaEventDestroy(e);
     for (auto& g : op->graphs) cudaGraphExecDestroy(g.exec);
-    for (cudaEvent_t e : op->ev_g)
+    for (cudaEvent_t e : op->ev_x)
         if (e) cudaEventDestroy(e);
+    if (op->s_comm) {
+        cudaStreamSynchronize(op->s_comm);
+        cudaStreamDestroy(op->s_comm);
+    }
+    if (op->comm) comm_destroy(op->comm);
+    if (op->bounce) cudaFreeHost(op->bounce);
     for (cudaEvent_t e : op->ev_io)
         if (e) cudaEventDestroy(e);
     for (cudaStream_t s : {op->s_h2d, op->s_d2h})
@@ -1874,18 +2028,16 @@ PCB_API pcb_status pcb_get_info(const pcb_op* op, pcb_info* info) {
 
 // Device-pointer apply: the launch sequence of run_batch (one per class and group: 17 kernels at
 // c3) is captured once per (adjoint, B, F, G) into a CUDA graph and replayed on the handle's
-// stream, ordered after / before the caller's stream by events.  Graphs are skipped while the
-// per-kernel profile is on and when the caller's stream is itself being captured; a capture
-// failure turns them off for the handle.
-static void run_dev(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG, cudaStream_t st) {
+// stream.  The cache is LRU; the host path reuses two fixed staging slots, so its sub-batches hit
+// the same few keys on every call.  Graphs are skipped while the per-kernel profile is on and when
+// the handle's stream is itself being captured; a capture failure turns them off for the handle.
+static void enqueue_batch(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (st) PCB_CK(cudaStreamIsCapturing(st, &cs));
+    PCB_CK(cudaStreamIsCapturing(op->stream, &cs));
     if (!op->sw.graphs || op->prof || cs != cudaStreamCaptureStatusNone) {
-        run_batch(op, adjoint, B, dF, dG, st);
+        run_batch(op, adjoint, B, dF, dG, op->stream);
         return;
     }
-    if (!op->ev_g[0])
-        for (auto& e : op->ev_g) PCB_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     pcb_op::GraphRec* rec = nullptr;
     for (auto& g : op->graphs)
         if (g.adjoint == adjoint && g.B == B && g.F == dF && g.G == dG) rec = &g;
@@ -1910,27 +2062,73 @@ static void run_dev(pcb_op* op, bool adjoint, int32_t B, const double* dF, doubl
             cudaGetLastError();
             if (exec) cudaGraphExecDestroy(exec);
             op->sw.graphs = false;
-            run_batch(op, adjoint, B, dF, dG, st);
+            run_batch(op, adjoint, B, dF, dG, op->stream);
             return;
         }
-        if (op->graphs.size() >= 32) {
-            cudaGraphExecDestroy(op->graphs.front().exec);
-            op->graphs.erase(op->graphs.begin());
+        if (op->graphs.size() >= 64) {  // evict the least recently used
+            auto lru = std::min_element(op->graphs.begin(), op->graphs.end(),
+                                        [](const pcb_op::GraphRec& x, const pcb_op::GraphRec& y) { return x.used < y.used; });
+            cudaGraphExecDestroy(lru->exec);
+            op->graphs.erase(lru);
         }
-        op->graphs.push_back({adjoint, B, dF, dG, exec, captured});
+        op->graphs.push_back({adjoint, B, dF, dG, exec, captured, 0});
         rec = &op->graphs.back();
+        ++op->graph_captures;
     }
-    if (st == op->stream) {  // the host path's sub-batches
-        PCB_CK(cudaGraphLaunch(rec->exec, op->stream));
-        g_launches.fetch_add(rec->launches);
-        return;
-    }
-    PCB_CK(cudaEventRecord(op->ev_g[0], st));
-    PCB_CK(cudaStreamWaitEvent(op->stream, op->ev_g[0], 0));
+    rec->used = ++op->graph_clock;
     PCB_CK(cudaGraphLaunch(rec->exec, op->stream));
     g_launches.fetch_add(rec->launches);
-    PCB_CK(cudaEventRecord(op->ev_g[1], op->stream));
-    PCB_CK(cudaStreamWaitEvent(st, op->ev_g[1], 0));
+}
+
+static cudaEvent_t op_event(pcb_op* op, int i) {
+    if (!op->ev_x[i]) PCB_CK(cudaEventCreateWithFlags(&op->ev_x[i], cudaEventDisableTiming));
+    return op->ev_x[i];
+}
+
+// Caller stream <-> handle stream.  All of a handle's device work runs on op->stream (its scratch
+// pools, staging buffers and graphs are shared by every entry point); a call on another stream is
+// ordered after that stream's prior work and makes it wait for the result.
+static void bridge_in(pcb_op* op, cudaStream_t st) {
+    if (st == op->stream) return;
+    PCB_CK(cudaEventRecord(op_event(op, 0), st));
+    PCB_CK(cudaStreamWaitEvent(op->stream, op_event(op, 0), 0));
+}
+static void bridge_out(pcb_op* op, cudaStream_t st) {
+    if (st == op->stream) return;
+    PCB_CK(cudaEventRecord(op_event(op, 1), op->stream));
+    PCB_CK(cudaStreamWaitEvent(st, op_event(op, 1), 0));
+}
+
+static bool has_reduce(const pcb_op* op) { return op->comm && op->reduce != PCB_REDUCE_NONE; }
+
+// Apply (or adjoint) of B vectors on op->stream, then -- for a sharded handle with a communicator
+// -- the fp64 sum of the shards' partials.  The batch is cut into chunks; chunk c's
+// reduce runs on the comm stream while the kernels of chunk c+1 run, so the NVLink transfer hides
+// behind the next chunk's FFTs.  Returns the event after which dG holds the result (recorded on
+// op->stream, or on the comm stream when reducing); op->stream itself does NOT wait for the last
+// reduce (callers that reuse dG on op->stream must wait on the returned event).
+static cudaEvent_t full_apply(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG, bool force_all = false) {
+    if (!has_reduce(op)) {
+        enqueue_batch(op, adjoint, B, dF, dG);
+        PCB_CK(cudaEventRecord(op_event(op, 2), op->stream));
+        return op_event(op, 2);
+    }
+    if (!op->s_comm) PCB_CK(cudaStreamCreateWithFlags(&op->s_comm, cudaStreamNonBlocking));
+    const int root = (op->reduce == PCB_REDUCE_ALL || force_all) ? -1 : 0;
+    // chunks of >= 2 vectors, at most op->comm_chunks of them (same on every rank: depends on B only)
+    const int nch = std::max(1, std::min(op->comm_chunks, B / 2));
+    for (int c = 0; c < nch; ++c) {
+        const int b0 = (int)((int64_t)B * c / nch), b1 = (int)((int64_t)B * (c + 1) / nch);
+        if (b1 <= b0) continue;
+        enqueue_batch(op, adjoint, b1 - b0, dF + (int64_t)b0 * op->N, dG + (int64_t)b0 * op->N);
+        cudaEvent_t e = op_event(op, 4 + (c & 1));
+        PCB_CK(cudaEventRecord(e, op->stream));
+        PCB_CK(cudaStreamWaitEvent(op->s_comm, e, 0));
+        const std::string err = comm_sum(op->comm, dG + (int64_t)b0 * op->N, (size_t)(b1 - b0) * op->N, root, op->s_comm);
+        if (!err.empty()) fail(PCB_ENCCL, err);
+    }
+    PCB_CK(cudaEventRecord(op_event(op, 3), op->s_comm));
+    return op_event(op, 3);
 }
 
 static pcb_status apply_dev_common(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG, void* stream) {
@@ -1944,7 +2142,11 @@ static pcb_status apply_dev_common(pcb_op* op, bool adjoint, int32_t B, const do
         if (B == 0) return;
         if (!dF || !dG) fail(PCB_EINVAL, "null vector pointer");
         set_device(op);
-        run_dev(op, adjoint, B, dF, dG, (cudaStream_t)stream);
+        const cudaStream_t st = (cudaStream_t)stream;
+        bridge_in(op, st);
+        cudaEvent_t done = full_apply(op, adjoint, B, dF, dG);
+        PCB_CK(cudaStreamWaitEvent(op->stream, done, 0));  // later work on the handle sees the result
+        bridge_out(op, st);
     });
 }
 
@@ -1955,6 +2157,36 @@ PCB_API pcb_status pcb_apply_adjoint_batch_dev(pcb_op* op, int32_t B, const doub
     return apply_dev_common(op, true, B, dF, dG, stream);
 }
 
+// Host memcpy split over a few threads (pageable caller buffers <-> the pinned bounce slots).
+static void par_memcpy(void* dst, const void* src, size_t bytes) {
+    const size_t grain = (size_t)4 << 20;
+    const int nt = (int)std::min<size_t>(8, std::max<size_t>(1, bytes / grain));
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> th;
+    const size_t part = (bytes / nt + 63) & ~(size_t)63;
+    for (int t = 0; t < nt; ++t) {
+        const size_t o = std::min(bytes, part * t), e = std::min(bytes, part * (t + 1));
+        if (e > o) th.emplace_back([=] { std::memcpy((char*)dst + o, (const char*)src + o, e - o); });
+    }
+    for (auto& x : th) x.join();
+}
+
+static bool host_pinned(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// Host-buffer apply: sub-batches of ~host_sub_mb MiB pipelined over three streams -- H2D(j+1),
+// kernels(j) (+ the shard reduce), D2H(j-1) -- through two fixed device staging slots (so the graph
+// keys repeat across calls).  Pageable caller buffers go through two pinned bounce slots per
+// direction: the host copies of sub-batch j+1 in and j-1 out run while the GPU works on j.
 static pcb_status apply_host_common(pcb_op* op, bool adjoint, int32_t B, const double* F, double* G) {
     if (!op) {
         set_err("null handle");
@@ -1966,18 +2198,11 @@ static pcb_status apply_host_common(pcb_op* op, bool adjoint, int32_t B, const d
         if (B == 0) return;
         if (!F || !G) fail(PCB_EINVAL, "null vector pointer");
         set_device(op);
-        const size_t cnt = (size_t)B * (size_t)op->N;
-        op->st_in.ensure(cnt);
-        op->st_out.ensure(cnt);
-        // Sub-batches overlap H2D(j+1) and D2H(j-1) with the kernels of sub-batch j (PCIe is full duplex,
-        // ~55 GB/s per direction).  ~sub_mb MiB each (geometric ramps at the ends measured no better); the first and the last are half size so the
-        // unoverlapped fill (first H2D) and drain (last D2H) stay short.
-        static const double sub_mb = [] {
-            const char* e = std::getenv("PCB_SUB_MB");
-            return e ? std::max(1.0, std::atof(e)) : 16.0;  // c3 sweep 8-64 MiB (scripts/e2e_sweep.sh): 16 best
-        }();
+        // ~sub_mb MiB per sub-batch (c3 sweep 8-64 MiB, scripts/e2e_sweep.sh: 16 best), >= 2 vectors per
+        // kernel batch; the first and the last are half size so the unoverlapped fill (first H2D) and
+        // drain (last D2H) stay short
         const double vec_mb = (double)op->N * 8.0 / (1 << 20);
-        const int per = (int)std::max(2.0, std::floor(sub_mb / vec_mb));  // >= 2 vectors per kernel batch
+        const int per = (int)std::max(2.0, std::floor(op->host_sub_mb / vec_mb));
         std::vector<int> sizes;
         if (B <= per) {
             sizes.push_back(B);
@@ -1992,26 +2217,66 @@ static pcb_status apply_host_common(pcb_op* op, bool adjoint, int32_t B, const d
             }
             sizes.push_back(edge);
         }
+        const int mx = *std::max_element(sizes.begin(), sizes.end());
+        const size_t slot = (size_t)mx * (size_t)op->N;
+        op->st_in.ensure(2 * slot);
+        op->st_out.ensure(2 * slot);
+        const bool pin_f = host_pinned(F), pin_g = host_pinned(G);
+        if ((!pin_f || !pin_g) && op->bounce_n < 4 * slot) {
+            if (op->bounce) cudaFreeHost(op->bounce);
+            op->bounce = nullptr;
+            op->bounce_n = 0;
+            PCB_CK(cudaHostAlloc((void**)&op->bounce, 4 * slot * sizeof(double), cudaHostAllocDefault));
+            op->bounce_n = 4 * slot;
+        }
         if (!op->s_h2d) {
             PCB_CK(cudaStreamCreateWithFlags(&op->s_h2d, cudaStreamNonBlocking));
             PCB_CK(cudaStreamCreateWithFlags(&op->s_d2h, cudaStreamNonBlocking));
             for (int j = 0; j < 8; ++j) PCB_CK(cudaEventCreateWithFlags(&op->ev_io[j], cudaEventDisableTiming));
         }
-        int b0 = 0;
+        cudaEvent_t* ev_h2d = op->ev_io;      // [2] H2D of slot done (device slot in, bounce in free)
+        cudaEvent_t* ev_k = op->ev_io + 2;    // [2] kernels done reading the device in-slot
+        cudaEvent_t* ev_d2h = op->ev_io + 4;  // [2] D2H of slot done (device out-slot free)
+        std::vector<size_t> offs(sizes.size());
+        size_t off = 0;
         for (size_t j = 0; j < sizes.size(); ++j) {
-            const int b1 = b0 + sizes[j];
-            const size_t off = (size_t)b0 * op->N, n = (size_t)(b1 - b0) * op->N;
-            PCB_CK(cudaMemcpyAsync(op->st_in.p + off, F + off, n * sizeof(double), cudaMemcpyHostToDevice, op->s_h2d));
-            PCB_CK(cudaEventRecord(op->ev_io[2 * (j & 1)], op->s_h2d));
-            PCB_CK(cudaStreamWaitEvent(op->stream, op->ev_io[2 * (j & 1)], 0));
-            run_dev(op, adjoint, b1 - b0, op->st_in.p + off, op->st_out.p + off, op->stream);
-            PCB_CK(cudaEventRecord(op->ev_io[2 * (j & 1) + 1], op->stream));
-            PCB_CK(cudaStreamWaitEvent(op->s_d2h, op->ev_io[2 * (j & 1) + 1], 0));
-            PCB_CK(cudaMemcpyAsync(G + off, op->st_out.p + off, n * sizeof(double), cudaMemcpyDeviceToHost, op->s_d2h));
-            b0 = b1;
+            offs[j] = off;
+            off += (size_t)sizes[j] * op->N;
         }
+        auto drain = [&](size_t j) {  // pageable G: the bounce copy of sub-batch j out to the caller
+            PCB_CK(cudaEventSynchronize(ev_d2h[j & 1]));
+            par_memcpy(G + offs[j], op->bounce + 2 * slot + (j & 1) * slot, (size_t)sizes[j] * op->N * sizeof(double));
+        };
+        for (size_t j = 0; j < sizes.size(); ++j) {
+            const int s = (int)(j & 1);
+            const size_t n = (size_t)sizes[j] * op->N;
+            double* din = op->st_in.p + s * slot;
+            double* dout = op->st_out.p + s * slot;
+            const double* src = F + offs[j];
+            if (j >= 2) PCB_CK(cudaStreamWaitEvent(op->s_h2d, ev_k[s], 0));  // kernels j-2 done with din
+            if (!pin_f) {
+                double* bin = op->bounce + s * slot;
+                if (j >= 2) PCB_CK(cudaEventSynchronize(ev_h2d[s]));  // H2D j-2 done with the bounce slot
+                par_memcpy(bin, src, n * sizeof(double));
+                src = bin;
+            }
+            PCB_CK(cudaMemcpyAsync(din, src, n * sizeof(double), cudaMemcpyHostToDevice, op->s_h2d));
+            PCB_CK(cudaEventRecord(ev_h2d[s], op->s_h2d));
+            PCB_CK(cudaStreamWaitEvent(op->stream, ev_h2d[s], 0));
+            if (j >= 2) PCB_CK(cudaStreamWaitEvent(op->stream, ev_d2h[s], 0));  // D2H j-2 done with dout
+            cudaEvent_t ready = full_apply(op, adjoint, sizes[j], din, dout);
+            PCB_CK(cudaEventRecord(ev_k[s], op->stream));
+            PCB_CK(cudaStreamWaitEvent(op->s_d2h, ready, 0));
+            double* dst = pin_g ? G + offs[j] : op->bounce + 2 * slot + s * slot;
+            if (!pin_g && j >= 2) PCB_CK(cudaStreamWaitEvent(op->s_d2h, ev_d2h[s], 0));  // (drained below)
+            PCB_CK(cudaMemcpyAsync(dst, dout, n * sizeof(double), cudaMemcpyDeviceToHost, op->s_d2h));
+            PCB_CK(cudaEventRecord(ev_d2h[s], op->s_d2h));
+            if (!pin_g && j >= 1) drain(j - 1);
+        }
+        if (!pin_g) drain(sizes.size() - 1);
         PCB_CK(cudaStreamSynchronize(op->s_d2h));
         PCB_CK(cudaStreamSynchronize(op->stream));
+        if (op->s_comm) PCB_CK(cudaStreamSynchronize(op->s_comm));
     });
 }
 
@@ -2087,10 +2352,16 @@ PCB_API pcb_status pcb_blocks(pcb_op* op, int32_t nblk, const int64_t* t_origin,
     std::lock_guard<std::mutex> lk(op->mu);
     return guarded([&] {
         if (nblk == 0) return;
-        if (!t_origin || !s_origin || !out) fail(PCB_EINVAL, "null pointer");
+        if (nblk < 0) fail(PCB_EINVAL, "pcb_blocks: negative block count");
+        if (!t_origin || !s_origin || !out || !block_shape) fail(PCB_EINVAL, "null pointer");
         set_device(op);
         int64_t bsz = 1;
-        for (int a = 0; a < op->dim_user; ++a) bsz *= block_shape[a];
+        for (int a = 0; a < op->dim_user; ++a) {
+            if (block_shape[a] < 1 || block_shape[a] > (1 << 20)) fail(PCB_EINVAL, "pcb_blocks: bad block shape");
+            bsz *= block_shape[a];
+            if (bsz > (int64_t)1 << 24) fail(PCB_EINVAL, "pcb_blocks: block too large");
+        }
+        if ((double)nblk * (double)bsz * (double)bsz > 4e9) fail(PCB_EINVAL, "pcb_blocks: output too large");
         std::vector<int64_t> ti = to_internal_points(op, t_origin, nblk), si = to_internal_points(op, s_origin, nblk);
         op->st_i64a.ensure(ti.size());
         op->st_i64b.ensure(si.size());
@@ -2115,7 +2386,9 @@ PCB_API pcb_status pcb_blocks_dev(pcb_op* op, int32_t nblk, const int64_t* d_t_o
         if (nblk == 0) return;
         if (op->dim_user != op->D) fail(PCB_EINVAL, "pcb_blocks_dev: dim-1 operators use pcb_blocks");
         set_device(op);
-        blocks_common(op, nblk, d_t_origin, d_s_origin, block_shape, d_out, (cudaStream_t)stream, false);
+        bridge_in(op, (cudaStream_t)stream);  // st_shape / st_flag are the handle's
+        blocks_common(op, nblk, d_t_origin, d_s_origin, block_shape, d_out, op->stream, false);
+        bridge_out(op, (cudaStream_t)stream);
     });
 }
 
@@ -2197,8 +2470,10 @@ PCB_API pcb_status pcb_apply_block(pcb_op* op, int32_t nblk, const int64_t* t_lo
                                                          (i2 - op->dom_lo[2]);
                         full[lin] = f[foff[b] + q++];
                     }
+            if (op->info.rank_active != op->info.rank && !has_reduce(op))
+                fail(PCB_EINVAL, "pcb_apply_block: large blocks of a sharded operator need a communicator");
             PCB_CK(cudaMemcpyAsync(dfull.p, full.data(), (size_t)op->N * 8, cudaMemcpyHostToDevice, op->stream));
-            run_batch(op, adjoint != 0, 1, dfull.p, dout.p, op->stream);
+            PCB_CK(cudaStreamWaitEvent(op->stream, full_apply(op, adjoint != 0, 1, dfull.p, dout.p, true), 0));
             PCB_CK(cudaMemcpyAsync(out.data(), dout.p, (size_t)op->N * 8, cudaMemcpyDeviceToHost, op->stream));
             PCB_CK(cudaStreamSynchronize(op->stream));
             q = 0;
@@ -2221,7 +2496,13 @@ static void estimate_common(pcb_op* op, int32_t q, const double* dZ, const doubl
                             double* eta_rel, cudaStream_t st) {
     if (q < 1) fail(PCB_EINVAL, "make_probes: q >= 1 required");
     if (nleaf < 0 || (nleaf > 0 && (!leaf_lo || !leaf_hi || !eta_cells))) fail(PCB_EINVAL, "bad leaf arguments");
-    run_batch(op, true, q, dZ, dYt, st);
+    if (op->info.rank_active != op->info.rank && !has_reduce(op))
+        fail(PCB_EINVAL, "update_samples: a sharded operator needs a communicator (pcb_options.nccl_id)");
+    bridge_in(op, st);  // everything below runs on op->stream (shared scratch / staging)
+    cudaEvent_t done = full_apply(op, true, q, dZ, dYt, true);  // shards: all-reduce Ytilde
+    PCB_CK(cudaStreamWaitEvent(op->stream, done, 0));
+    const cudaStream_t caller = st;
+    st = op->stream;
     std::vector<int64_t> blo, bhi;
     if (nleaf > 0) {
         blo = to_internal_points(op, leaf_lo, nleaf);
@@ -2248,6 +2529,7 @@ static void estimate_common(pcb_op* op, int32_t q, const double* dZ, const doubl
     std::vector<double> h(nd2 + q);
     PCB_CK(cudaMemcpyAsync(h.data(), op->st_aux.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
     PCB_CK(cudaStreamSynchronize(st));
+    bridge_out(op, caller);
     for (int32_t c = 0; c < nleaf; ++c) {
         double s = 0;
         for (int i = 0; i < q; ++i) s += h[(size_t)c * q + i];
@@ -2495,8 +2777,8 @@ PCB_API pcb_status pcb_estimator_update(pcb_estimator* e, pcb_op* op, int32_t nc
         for (int a = 0; a < e->D; ++a)
             if (op->dom_lo[a] != e->dom_lo[a] || op->n[a] != e->n[a])
                 fail(PCB_EINVAL, "update_samples: operator domain differs from the probes'");
-        if (op->info.rank_active != op->info.rank)
-            fail(PCB_EINVAL, "update_samples: the estimator needs the unsharded operator");
+        if (op->info.rank_active != op->info.rank && !has_reduce(op))
+            fail(PCB_EINVAL, "update_samples: a sharded operator needs a communicator (pcb_options.nccl_id)");
         if (nchanged < 0 || (nchanged > 0 && !changed_ks)) fail(PCB_EINVAL, "bad changed list");
         const int32_t r = op->info.rank;
         std::set<int32_t> changed(changed_ks, changed_ks + nchanged);
@@ -2506,7 +2788,11 @@ PCB_API pcb_status pcb_estimator_update(pcb_estimator* e, pcb_op* op, int32_t nc
         for (int32_t k = e->cached; k < r; ++k)
             if (!changed.count(k)) fail(PCB_EINVAL, "update_samples: uncached sample point not marked changed");
         e->cached = r;
-        run_batch(op, true, e->q, e->Z.p, e->Yt.p, e->stream);
+        set_device(op);
+        bridge_in(op, e->stream);  // the adjoint runs on the operator's stream (its scratch pools)
+        cudaEvent_t done = full_apply(op, true, e->q, e->Z.p, e->Yt.p, true);  // shards: all-reduce Ytilde
+        PCB_CK(cudaStreamWaitEvent(op->stream, done, 0));
+        bridge_out(op, e->stream);
         e->have_yt = true;
         std::vector<double> h;
         est_sums(e, 0, nullptr, nullptr, h);

@@ -33,12 +33,15 @@ EXPORTS = ["pcb_default_options", "pcb_last_error", "pcb_create", "pcb_destroy",
            "pcb_estimator_set_y_blur", "pcb_estimator_update", "pcb_estimator_cells", "pcb_estimator_read",
            "pcb_get_domain", "pcb_cluster_tree", "pcb_hmatrix_assemble", "pcb_hmatrix_compress",
            "pcb_hmatrix_destroy", "pcb_hmatrix_get_info", "pcb_hmatrix_tree", "pcb_hmatrix_block",
-           "pcb_hmatrix_admissible", "pcb_hmatrix_matvec", "pcb_hmatrix_save", "pcb_hmatrix_load"]
+           "pcb_hmatrix_admissible", "pcb_hmatrix_matvec", "pcb_hmatrix_save", "pcb_hmatrix_load",
+           "pcb_comm_unique_id", "pcb_plan_shards"]
+REDUCE = {"none": 0, "all": 1, "root": 2}
+PARTITION = {"cost": 0, "count": 1}
 
 
 class Options(ctypes.Structure):
     _fields_ = [("device", i32), ("mode", i32), ("max_batch", i32), ("shard_rank", i32), ("shard_count", i32),
-                ("reserved", i32), ("scratch_bytes", i64)]
+                ("reduce", i32), ("scratch_bytes", i64), ("nccl_id", vp), ("partition", i32), ("host_sub_mb", i32)]
 
 
 class Info(ctypes.Structure):
@@ -46,7 +49,9 @@ class Info(ctypes.Structure):
                 ("fft_size", i32 * 3), ("n_points", i64), ("spectra_bytes", i64), ("device_bytes", i64),
                 ("bytes_per_vector", dbl), ("flops_per_vector", dbl), ("launches_per_batch", i32),
                 ("n_row_families", i32), ("kernel_bytes", dbl * 4), ("kernel_flops", dbl * 4),
-                ("n_column_chains", i32), ("n_chained_terms", i32)]
+                ("n_column_chains", i32), ("n_chained_terms", i32), ("shard_rank", i32), ("shard_count", i32),
+                ("comm_nranks", i32), ("comm_version", i32), ("term_lo", i32), ("term_hi", i32),
+                ("shard_cost", dbl), ("total_cost", dbl), ("model_ms_local", dbl), ("model_ms_global", dbl)]
 
     def as_dict(self) -> dict:
         return {"dim": self.dim, "rank": self.rank, "rank_active": self.rank_active,
@@ -57,7 +62,11 @@ class Info(ctypes.Structure):
                 "launches_per_batch": self.launches_per_batch, "n_row_families": self.n_row_families,
                 "n_column_chains": self.n_column_chains, "n_chained_terms": self.n_chained_terms,
                 "kernel_bytes": dict(zip(KERNEL_FAMILIES, list(self.kernel_bytes))),
-                "kernel_flops": dict(zip(KERNEL_FAMILIES, list(self.kernel_flops)))}
+                "kernel_flops": dict(zip(KERNEL_FAMILIES, list(self.kernel_flops))),
+                "shard_rank": self.shard_rank, "shard_count": self.shard_count, "comm_nranks": self.comm_nranks,
+                "comm_version": self.comm_version, "term_lo": self.term_lo, "term_hi": self.term_hi,
+                "shard_cost": self.shard_cost, "total_cost": self.total_cost,
+                "model_ms_local": self.model_ms_local, "model_ms_global": self.model_ms_global}
 
 
 class HMatrixInfo(ctypes.Structure):
@@ -134,6 +143,9 @@ def load():
     L.pcb_hmatrix_matvec.argtypes = [vp, vp, vp]
     L.pcb_hmatrix_save.argtypes = [vp, ctypes.c_char_p]
     L.pcb_hmatrix_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
+    L.pcb_comm_unique_id.argtypes = [vp]
+    L.pcb_plan_shards.argtypes = [i32, P_i64, P_i64, i32, P_i64, P_i64, ctypes.POINTER(vp), P_i64, P_i64,
+                                  ctypes.POINTER(vp), i32, i32, vp, vp]
     for n in EXPORTS:
         if n not in ("pcb_default_options", "pcb_last_error", "pcb_launch_count", "pcb_blur_last_error"):
             getattr(L, n).restype = ctypes.c_int
@@ -159,3 +171,10 @@ def default_options() -> Options:
 
 def launch_count() -> int:
     return int(load().pcb_launch_count())
+
+
+def comm_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (pcb_comm_unique_id) for pcb_options.nccl_id."""
+    buf = ctypes.create_string_buffer(128)
+    check(load().pcb_comm_unique_id(buf))
+    return buf.raw

@@ -38,9 +38,17 @@ class ProductConvolutionOperator:
 
     def __init__(self, domain: Tuple[Sequence[int], Sequence[int]], weights: Sequence, impulses: Sequence,
                  points: Optional[Sequence[Sequence[int]]] = None, mode: str = "auto", max_batch: int = 16,
-                 shard: Tuple[int, int] = (0, 1), device: int = -1, scratch_bytes: int = 0):
+                 shard: Tuple[int, int] = (0, 1), device: int = -1, scratch_bytes: int = 0,
+                 nccl_id: Optional[bytes] = None, reduce: str = "all", partition: str = "cost",
+                 host_sub_mb: int = 0):
         """domain = (lo, hi) inclusive; weights / impulses: objects with ``.lo`` and ``.values``
-        (``inputs.Field``) or (lo, values) pairs."""
+        (``inputs.Field``) or (lo, values) pairs.
+
+        Shard-by-k: ``shard = (rank, count)`` keeps this rank's cost-balanced block
+        of terms (``partition``); with ``nccl_id`` (``lib.comm_unique_id()`` on one rank, sent to the
+        others) construction joins an NCCL communicator and every apply sums the shards' partials
+        inside the library (``reduce``: "all" = every rank gets the full result, "root" = rank 0,
+        "none" = partial).  Without it, apply returns this shard's partial sum."""
         if len(weights) != len(impulses):
             raise ValueError("PCOp: one weight per impulse required")
         L = _L.load()
@@ -80,6 +88,15 @@ class ProductConvolutionOperator:
         opt.shard_rank, opt.shard_count = int(shard[0]), int(shard[1])
         opt.device = int(device)
         opt.scratch_bytes = int(scratch_bytes)
+        opt.partition = _L.PARTITION[partition]
+        opt.host_sub_mb = int(host_sub_mb)
+        id_buf = None
+        if nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise ValueError("nccl_id must be 128 bytes (pcb_comm_unique_id)")
+            id_buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            opt.nccl_id = ctypes.cast(id_buf, _L.vp)
+            opt.reduce = _L.REDUCE[reduce]
         PP = _L.vp * max(1, r)
         h = _L.vp()
         rc = L.pcb_create(self.dim, _i64arr(lo), _i64arr(hi), r, pts, _i64arr(w_lo), _i64arr(w_hi),
@@ -262,3 +279,28 @@ def uniform_ints(seed: int, lo: int, hi: int, count: int) -> np.ndarray:
     out = np.empty(count, dtype=np.int64)
     _L.check(_L.load().pcb_uniform_int_fill(ctypes.c_uint64(seed), lo, hi, count, _ptr(out)))
     return out
+
+
+def plan_shards(inp, shard_count: int, partition: str = "cost"):
+    """The C planner's shard partition (pcb_plan_shards, host only): (owner[k], cost[k]) per term;
+    owner -1 = inactive term.  pcb_create with shard_rank s keeps exactly the terms owned by s."""
+    L = _L.load()
+    r = inp.rank
+    keep, w_lo, w_hi, p_lo, p_hi, w_ptr, p_ptr = [], [], [], [], [], [], []
+    for w, e in zip(inp.weights, inp.impulses):
+        wv = np.ascontiguousarray(w.values, dtype=np.float64)
+        ev = np.ascontiguousarray(e.values, dtype=np.float64)
+        keep += [wv, ev]
+        w_lo += list(w.lo)
+        w_hi += [l + s - 1 for l, s in zip(w.lo, wv.shape)]
+        p_lo += list(e.lo)
+        p_hi += [l + s - 1 for l, s in zip(e.lo, ev.shape)]
+        w_ptr.append(wv.ctypes.data)
+        p_ptr.append(ev.ctypes.data)
+    PP = _L.vp * max(1, r)
+    owner = np.zeros(max(1, r), dtype=np.int32)
+    cost = np.zeros(max(1, r))
+    _L.check(L.pcb_plan_shards(inp.dim, _i64arr(inp.dom_lo), _i64arr(inp.dom_hi), r, _i64arr(w_lo), _i64arr(w_hi),
+                               PP(*w_ptr), _i64arr(p_lo), _i64arr(p_hi), PP(*p_ptr), int(shard_count),
+                               _L.PARTITION[partition], _ptr(owner), _ptr(cost)))
+    return owner[:r], cost[:r]

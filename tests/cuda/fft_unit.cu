@@ -104,7 +104,7 @@ int main() {
     int bad = 0;
 #define T(n) bad |= run<n>(dtw);
     T(8) T(16) T(24) T(32) T(48) T(64) T(72) T(96) T(128) T(144) T(192) T(256) T(288) T(384) T(512) T(576) T(768)
-    T(1024) T(1152) T(1536) T(2048) T(2304) T(3072)
+    T(1024) T(1152) T(1536) T(2048) T(2304) T(3072) T(4096)
     printf(bad ? "FFT UNIT: FAIL\n" : "FFT UNIT: all lengths OK\n");
     return bad;
 }

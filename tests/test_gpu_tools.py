@@ -1,0 +1,133 @@
+"""GPU checks beyond parity: the FFT engine unit test, compute-sanitizer (memcheck / racecheck /
+synccheck) over every entry point, the library's NCCL shard reduce on a 1-rank communicator, and
+the host-buffer pipeline with many sub-batches (pinned and pageable)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from paper_1805_06018_b200 import build, inputs
+from paper_1805_06018_b200.operator import ProductConvolutionOperator, normal_vectors
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("cfg", list(dict.fromkeys(build.FFT_UNIT_CONFIGS)), ids=lambda c: "_".join(c))
+def test_fft_engine_unit(gpu, cfg):
+    """fft.cuh for every compiled line length (8..4096, 2^a * {1,3,9}), forward and inverse, both
+    register orders, vs a long-double DFT: relative l2 < 1e-14 (tests/cuda/fft_unit.cu)."""
+    exe = build.fft_unit_path(cfg)
+    if not os.path.exists(exe):
+        exe = build.build_tools()[list(dict.fromkeys(build.FFT_UNIT_CONFIGS)).index(cfg)]
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "all lengths OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def _sanitizer():
+    for p in (shutil.which("compute-sanitizer"), "/usr/local/cuda/bin/compute-sanitizer"):
+        if p and os.path.exists(p):
+            return p
+    pytest.fail("compute-sanitizer not found")
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer(gpu, tool):
+    env = dict(os.environ)
+    if tool != "memcheck":
+        env["PCB_GRAPHS"] = "0"  # kernel-by-kernel launches (memcheck also covers the graph replays)
+    cmd = [_sanitizer(), f"--tool={tool}", "--error-exitcode=99", "--print-limit=20"]
+    if tool == "memcheck":
+        cmd += ["--leak-check=no"]
+    if tool == "racecheck":
+        cmd += ["--racecheck-report=hazard"]
+    cmd += [sys.executable, os.path.join(ROOT, "tests", "sanitize_target.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1800, env=env)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "SANITIZE TARGET OK" in r.stdout, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-4000:]
+
+
+def test_nccl_reduce_one_rank(gpu):
+    """The shard reduce inside the library (pcb_options.nccl_id) on a 1-rank communicator: the
+    chunked apply + ncclReduce / ncclAllReduce pipeline gives the unsharded result (a sum over one
+    rank is exact), device and host paths, apply, adjoint and the estimator update."""
+    from paper_1805_06018_b200 import lib
+
+    inp = inputs.make_config("c2")
+    F = normal_vectors(1, 6, inp.n_points)
+    ref = ProductConvolutionOperator.from_inputs(inp)
+    G0, GA0 = ref.apply_batch(F), ref.apply_adjoint_batch(F)
+    for red in ("all", "root"):
+        op = ProductConvolutionOperator.from_inputs(inp, shard=(0, 1), nccl_id=lib.comm_unique_id(), reduce=red)
+        assert op.info["comm_nranks"] == 1 and op.info["comm_version"] > 0
+        assert np.array_equal(op.apply_batch(F), G0)
+        assert np.array_equal(op.apply_adjoint_batch(F), GA0)
+        import torch
+
+        dF = torch.from_numpy(F).cuda()
+        dG = torch.empty_like(dF)
+        op.apply_batch_dev(6, dF.data_ptr(), dG.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(dG.cpu().numpy(), G0)
+        yt, cells, ea, er = op.probe_estimate(F[:2], F[:2] * 0.5, [], want_ytilde=True)
+        assert np.array_equal(yt, GA0[:2])
+        op.close()
+
+
+def test_k_shards_partition_and_sum(gpu):
+    """Cost-balanced k-shards (no communicator): each shard keeps exactly the planner's block
+    (pcb_plan_shards) and the partials sum to the full apply."""
+    from paper_1805_06018_b200 import sharding
+
+    inp = inputs.make_config("c3")
+    F = normal_vectors(2, 2, inp.n_points)
+    full = ProductConvolutionOperator.from_inputs(inp).apply_batch(F)
+    acc = np.zeros_like(full)
+    for s in range(3):
+        op = ProductConvolutionOperator.from_inputs(inp, shard=(s, 3))
+        ks = sharding.k_terms(inp, s, 3)
+        assert op.info["rank_active"] == len(ks)
+        assert (op.info["term_lo"], op.info["term_hi"]) == (ks[0], ks[-1] + 1)
+        acc += op.apply_batch(F)
+        op.close()
+    assert rel(acc, full) <= 1e-14
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+@pytest.mark.parametrize("B", [5, 7])
+def test_host_pipeline_many_sub_batches(gpu, cfg, B):
+    """pcb_apply_batch with 1 MiB sub-batches (many of them, ping-pong staging slots, half-size
+    edges), pinned and pageable host buffers, apply and adjoint: bitwise equal to the device path."""
+    import torch
+
+    inp = inputs.make_config(cfg)
+    op = ProductConvolutionOperator.from_inputs(inp, host_sub_mb=1)
+    F = normal_vectors(9, B, inp.n_points)
+    dF = torch.from_numpy(F).cuda()
+    dG = torch.empty_like(dF)
+    for adj in (False, True):
+        op.apply_batch_dev(B, dF.data_ptr(), dG.data_ptr(), torch.cuda.current_stream().cuda_stream, adjoint=adj)
+        torch.cuda.synchronize()
+        want = dG.cpu().numpy()
+        got = op.apply_adjoint_batch(F) if adj else op.apply_batch(F)  # pageable numpy
+        assert np.array_equal(got, want)
+        Fp = torch.from_numpy(F).pin_memory()
+        Gp = torch.empty_like(Fp).pin_memory()
+        from paper_1805_06018_b200 import lib
+
+        fn = lib.load().pcb_apply_adjoint_batch if adj else lib.load().pcb_apply_batch
+        lib.check(fn(op._h, B, Fp.data_ptr(), Gp.data_ptr()))
+        assert np.array_equal(Gp.numpy(), want)
+        # repeated calls replay the cached graphs (same keys every call)
+        again = op.apply_adjoint_batch(F) if adj else op.apply_batch(F)
+        assert np.array_equal(again, want)
+    op.close()

@@ -247,3 +247,21 @@ def test_oracle_apply_block_is_apply_then_restrict():  # test_pc_operator.cpp:15
             g = (op.apply_adjoint if adj else op.apply)(full.reshape(-1)).reshape(14, 14)
             blk = op.apply_block(T, S, f, adj)
             assert np.max(np.abs(blk.values - g[tlo[0]:thi[0] + 1, tlo[1]:thi[1] + 1])) <= 1e-12
+
+
+@pytest.mark.parametrize("cfg,seed", [("c3", 2)])
+def test_oracle_vs_reference_headline_fingerprint(cfg, seed):
+    """The numpy restatement at the FULL c3 size against the reference's own apply
+    (tests/golden/headline_c3.npz, made by tests/golden/make_headline_golden.py)."""
+    import os
+
+    from headline_common import compare
+    from paper_1805_06018_b200.operator import normal_vectors
+
+    inp = inputs.make_config(cfg)
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", f"headline_{cfg}.npz"))
+    assert str(gold["checksum"]) == inp.checksum()
+    f = normal_vectors(seed, 1, inp.n_points)[0]
+    err = compare(O.PCOperator.from_inputs(inp).apply(f), inp.shape,
+                  {k: gold[f"apply0_{k}"] for k in ("samples", "tiles", "norm")})
+    assert max(err.values()) <= 1e-12, err
