@@ -114,6 +114,8 @@ typedef struct pcb_info {
     double total_cost;       /* modelled cost of all active terms */
     double model_ms_local;   /* planner's modelled time per vector of this shard, LOCAL plan */
     double model_ms_global;  /* ... GLOBAL plan */
+    int32_t plan_terms;      /* terms the FFT plan runs: the owned terms, with split terms replaced by their pieces */
+    int32_t split_terms;     /* owned terms whose linear convolution exceeds one 4096-point line, split into pieces */
 } pcb_info;
 
 PCB_API void pcb_default_options(pcb_options* opt);

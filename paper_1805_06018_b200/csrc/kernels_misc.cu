@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk,
                                                       int cap, double* __restrict__ out, int32_t* bad) {
     extern __shared__ double sm[];
     __shared__ int64_t s_t[3], s_s[3];
-    __shared__ int s_n, s_nc, s_fb;
+    __shared__ int s_nc, s_fb;
     __shared__ int ids[BT_IDS];
     __shared__ int first[BT_IDS];
     __shared__ int cand[BT_CAP];
@@ -283,10 +283,14 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk,
                     fb = 1;
             }
             s_fb = fb;
-            s_n = 0;
+            s_nc = 0;
         }
         __syncthreads();
-        if (tid < 32 && !s_fb) {  // warp 0: the candidate terms from the buckets covering S
+        if (tid < 32 && !s_fb) {
+            // warp 0: the candidate terms -- listed in the buckets covering S, deduplicated, kept
+            // only when X_k meets S and the kernel box K_k meets the offsets T - S (every other term
+            // reads phi^E = 0 there: its products are exact zeros, which leave the sum unchanged),
+            // in ascending k (the reference's summation order)
             int blo[3] = {0, 0, 0}, bn[3] = {1, 1, 1}, nbk = 1;
             for (int i = 0; i < D; ++i) {
                 blo[i] = (int)((s_s[i] - a.dom_lo[i]) / a.bucket[i]);
@@ -317,32 +321,55 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk,
                 if (tid == 0) s_fb = 1;
             } else {
                 for (int q = 0; q < cnt; ++q) ids[off + q] = a.bucket_terms[beg + q];
-                if (tid == 0) s_n = total;
+                __syncwarp();
+                // lane l owns positions l and l + 32: keep = first occurrence and the term can contribute
+                int keep[2] = {0, 0}, idv[2] = {0, 0};
+                for (int h = 0; h < 2; ++h) {
+                    const int pos = tid + 32 * h;
+                    if (pos >= total) continue;
+                    const int id = ids[pos];
+                    int f = 1;
+                    for (int j = 0; j < pos; ++j) f &= ids[j] != id;
+                    if (f) {
+                        const TermDesc& t = a.terms[id];
+                        for (int d = 0; d < D && f; ++d) {
+                            const int64_t o = s_t[d] - s_s[d];
+                            f &= (t.x_lo[d] <= s_s[d] + bs[d] - 1) && (t.x_lo[d] + t.m[d] - 1 >= s_s[d]) &&
+                                 (t.k_lo[d] <= o + bs[d] - 1) && (t.k_lo[d] + t.k_ext[d] - 1 >= o - (bs[d] - 1));
+                        }
+                    }
+                    keep[h] = f;
+                    idv[h] = id;
+                    first[pos] = f ? id : -1;
+                }
+                __syncwarp();
+                const int nk = __popc(__ballot_sync(0xffffffffu, keep[0])) + __popc(__ballot_sync(0xffffffffu, keep[1]));
+                for (int h = 0; h < 2; ++h) {
+                    if (!keep[h]) continue;
+                    int rank = 0;
+                    for (int j = 0; j < total; ++j) rank += first[j] >= 0 && first[j] < idv[h];
+                    if (rank < cap) cand[rank] = idv[h];
+                }
+                if (tid == 0) {
+                    s_nc = nk;
+                    if (nk > cap) s_fb = 1;
+                }
             }
         }
         __syncthreads();
-        const int n = s_n;
-        if (!s_fb && tid < n) {  // first occurrences
-            const int id = ids[tid];
-            int f = 1;
-            for (int j = 0; j < tid; ++j) f &= ids[j] != id;
-            first[tid] = f;
-        }
-        __syncthreads();
-        if (!s_fb && tid < n && first[tid]) {  // ascending rank among the distinct ids
-            const int id = ids[tid];
-            int rank = 0;
-            for (int j = 0; j < n; ++j) rank += first[j] && ids[j] < id;
-            if (rank < cap) cand[rank] = id;
-        }
-        if (tid == 0 && !s_fb) {
-            int nc = 0;
-            for (int j = 0; j < n; ++j) nc += first[j];
-            s_nc = nc;
-            if (nc > cap) s_fb = 1;
-        }
-        __syncthreads();
         double* ob = out + (int64_t)blk * npx * npx;
+        if (!s_fb && s_nc == 0) {  // no term can contribute: an all-zero block, 16-byte stores
+            const int n2 = npx * npx;
+            if ((reinterpret_cast<uintptr_t>(ob) & 15) == 0) {
+                double2* o2 = reinterpret_cast<double2*>(ob);
+                for (int e = tid; e < n2 / 2; e += blockDim.x) o2[e] = make_double2(0.0, 0.0);
+                if ((n2 & 1) && tid == 0) ob[n2 - 1] = 0.0;
+            } else {
+                for (int e = tid; e < n2; e += blockDim.x) ob[e] = 0.0;
+            }
+            __syncthreads();
+            continue;
+        }
         if (s_fb) {  // per-entry path (out-of-domain entries flag `bad`)
             for (int e = tid; e < npx * npx; e += blockDim.x) {
                 int i = e / npx, j = e - (e / npx) * npx;

@@ -862,6 +862,97 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     }
     for (int k : mine) op->owned[k] = 1;
     if (geometry_only) return;
+    const int owned_terms = (int)mine.size();
+
+    // Terms too large for one FFT line (the reference pads any size to next_pow2, fft.cpp:58-70;
+    // the engine's lines end at 4096): split the term into pieces -- its input window X_k into
+    // sub-windows and, when the kernel box alone exceeds half a line, K_k into sub-boxes -- so every
+    // piece's full linear convolution fits one line (P >= m' + k' - 1, the reference's own per-term
+    // rule on the piece).  Exact: w_k f is the sum of its restrictions to the sub-windows, phi_k the
+    // sum of its restrictions to the sub-boxes, and every piece is cropped to the domain like a term.
+    // The pieces are appended after the r terms (the entry gather keeps using the originals).
+    int n_split = 0;
+    {
+        int64_t Pmax[3] = {1, 1, 1};
+        for (int a = 0; a < D; ++a) {
+            int64_t p = 4096;
+            while (p > 16 && fft_size_at_least(p, a == D - 1, op->sw.mixed_last, op->sw.pow2_only) != p) p -= 8;
+            Pmax[a] = p;
+        }
+        std::vector<int> mine2;
+        for (int k : mine) {
+            const TermDesc t = op->terms[k];
+            bool big = false;
+            int64_t kp[3] = {1, 1, 1}, mp[3] = {1, 1, 1}, nk[3] = {1, 1, 1}, nm[3] = {1, 1, 1};
+            for (int a = 0; a < D; ++a) {
+                kp[a] = t.k_ext[a];
+                mp[a] = t.m[a];
+                if ((int64_t)t.m[a] + t.k_ext[a] - 1 > Pmax[a]) {
+                    big = true;
+                    kp[a] = std::min<int64_t>(t.k_ext[a], Pmax[a] / 2);
+                    mp[a] = Pmax[a] - kp[a] + 1;
+                }
+                nk[a] = (t.k_ext[a] + kp[a] - 1) / kp[a];
+                nm[a] = (t.m[a] + mp[a] - 1) / mp[a];
+            }
+            if (!big) {
+                mine2.push_back(k);
+                continue;
+            }
+            ++n_split;
+            op->owned[k] = 0;  // served by its pieces
+            for (int64_t c = 0; c < nm[0] * nm[1] * nm[2] * nk[0] * nk[1] * nk[2]; ++c) {
+                int64_t rem = c, u0[3], z0[3];
+                for (int a = 2; a >= 0; --a) {
+                    z0[a] = (rem % nk[a]) * kp[a];
+                    rem /= nk[a];
+                }
+                for (int a = 2; a >= 0; --a) {
+                    u0[a] = (rem % nm[a]) * mp[a];
+                    rem /= nm[a];
+                }
+                TermDesc q{};
+                for (int a = 0; a < 3; ++a) {
+                    q.x_lo[a] = t.x_lo[a] + u0[a];
+                    q.m[a] = (int32_t)std::min<int64_t>(mp[a], t.m[a] - u0[a]);
+                    q.k_lo[a] = t.k_lo[a] + z0[a];
+                    q.k_ext[a] = (int32_t)std::min<int64_t>(kp[a], t.k_ext[a] - z0[a]);
+                }
+                q.w_off = (int64_t)wpool.size();
+                for (int64_t i0 = 0; i0 < q.m[0]; ++i0)
+                    for (int64_t i1 = 0; i1 < q.m[1]; ++i1)
+                        for (int64_t i2 = 0; i2 < q.m[2]; ++i2) {
+                            const double v = wpool[t.w_off + ((u0[0] + i0) * t.m[1] + (u0[1] + i1)) * t.m[2] + (u0[2] + i2)];
+                            wpool.push_back(v);
+                        }
+                q.phi_off = (int64_t)ppool.size();
+                bool any = false;
+                for (int64_t i0 = 0; i0 < q.k_ext[0]; ++i0)
+                    for (int64_t i1 = 0; i1 < q.k_ext[1]; ++i1)
+                        for (int64_t i2 = 0; i2 < q.k_ext[2]; ++i2) {
+                            const double v = ppool[t.phi_off + ((z0[0] + i0) * t.k_ext[1] + (z0[1] + i1)) * t.k_ext[2] +
+                                                   (z0[2] + i2)];
+                            any = any || v != 0.0;
+                            ppool.push_back(v);
+                        }
+                if (!any) {  // an all-zero kernel piece contributes nothing
+                    ppool.resize((size_t)q.phi_off);
+                    wpool.resize((size_t)q.w_off);
+                    continue;
+                }
+                const int id = (int)op->terms.size();
+                op->terms.push_back(q);
+                op->has_x.push_back(1);
+                op->has_k.push_back(1);
+                op->owned.push_back(1);
+                op->shard_of.push_back(sr);
+                op->term_cost.push_back(local_term_cost(op, q));
+                mine2.push_back(id);
+            }
+        }
+        mine.swap(mine2);
+    }
+    const int R = (int)op->terms.size();  // terms + pieces (plan-level term ids)
 
     // candidate plans
     int64_t Pg[3] = {1, 1, 1};
@@ -871,7 +962,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
         // GLOBAL: 3-smooth sizes on every axis (its row passes are not the bottleneck)
         Pg[a] = fft_size_at_least(op->n[a] + mmax - 1, a == D - 1, true, op->sw.pow2_only);
     }
-    std::vector<std::array<int64_t, 3>> chainP(r, std::array<int64_t, 3>{0, 0, 0});
+    std::vector<std::array<int64_t, 3>> chainP(R, std::array<int64_t, 3>{0, 0, 0});
     auto local_P = [&](int k, int a) {
         if (chainP[k][a] > 0) return chainP[k][a];
         return fft_size_at_least((int64_t)op->terms[k].m[a] + op->terms[k].k_ext[a] - 1, a == D - 1,
@@ -921,7 +1012,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     op->mode = mode;
 
     // per-term placement
-    for (int k = 0; k < r; ++k) {
+    for (int k = 0; k < R; ++k) {
         TermDesc& t = op->terms[k];
         if (!op->has_x[k] || !op->has_k[k]) continue;
         for (int a = 0; a < D; ++a) {
@@ -952,7 +1043,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     // gather reads one set of rows per chain.  Consecutive terms (by s_0) are chained by dynamic
     // programming on a modelled cost: column FFTs W * (members + 1) * P0 log2 P0 plus chain_beta
     // per T row element (its write, read and C2R).  Chains of one are the plain LOCAL plan.
-    std::vector<int> term_chain(r, -1);
+    std::vector<int> term_chain(R, -1);
     if (mode == PCB_MODE_LOCAL && D == 2 && op->sw.chains) {
         std::map<std::pair<int64_t, int32_t>, std::vector<int>> clusters;
         for (int k : mine) clusters[{op->terms[k].x_lo[1], op->terms[k].m[1]}].push_back(k);
@@ -1097,7 +1188,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
         t.cols_f = 0;
     }
     std::vector<double> apool;
-    std::vector<int> term_fam(r, -1);
+    std::vector<int> term_fam(R, -1);
     if (mode == PCB_MODE_LOCAL && op->sw.families) {
         const int ax = D - 1;
         auto lead_of = [&](const TermDesc& t) { return D == 2 ? (int64_t)t.m[0] : (int64_t)t.m[0] * t.m[1]; };
@@ -1194,7 +1285,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     // family).  Terms of one row family with the same axis-1 window, factor b (bitwise) and axis-1
     // FFT size share those transforms over the union of their x0 ranges; the cols pass then
     // applies a_k(x0) as it loads each plane.
-    std::vector<int> term_pf(r, -1);
+    std::vector<int> term_pf(R, -1);
     if (D == 3 && op->sw.plane_families)
         for (Class& c : op->classes) {
             if (c.fams.empty()) continue;
@@ -1297,7 +1388,7 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     // output window, with no weight: terms of one class with the same axis-1 window (s_1, o_lo_1,
     // o_cnt_1) have identical rows wherever their axis-0 windows overlap, so they share the rows
     // over the union of their axis-0 windows.  Used when the shared rows are >= 1.2x fewer.
-    std::vector<int> term_af(r, -1);
+    std::vector<int> term_af(R, -1);
     if (mode == PCB_MODE_LOCAL && op->sw.families)
         for (Class& c : op->classes) {
             const int ax = D - 1;
@@ -1596,7 +1687,9 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
     in = pcb_info{};
     in.dim = dim;
     in.rank = r;
-    in.rank_active = (int32_t)mine.size();
+    in.rank_active = (int32_t)owned_terms;
+    in.plan_terms = (int32_t)mine.size();
+    in.split_terms = n_split;
     in.shard_rank = sr;
     in.shard_count = sc;
     in.term_lo = mine.empty() ? 0 : mine.front();

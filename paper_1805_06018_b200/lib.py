@@ -51,7 +51,8 @@ class Info(ctypes.Structure):
                 ("n_row_families", i32), ("kernel_bytes", dbl * 4), ("kernel_flops", dbl * 4),
                 ("n_column_chains", i32), ("n_chained_terms", i32), ("shard_rank", i32), ("shard_count", i32),
                 ("comm_nranks", i32), ("comm_version", i32), ("term_lo", i32), ("term_hi", i32),
-                ("shard_cost", dbl), ("total_cost", dbl), ("model_ms_local", dbl), ("model_ms_global", dbl)]
+                ("shard_cost", dbl), ("total_cost", dbl), ("model_ms_local", dbl), ("model_ms_global", dbl),
+                ("plan_terms", i32), ("split_terms", i32)]
 
     def as_dict(self) -> dict:
         return {"dim": self.dim, "rank": self.rank, "rank_active": self.rank_active,
@@ -66,7 +67,8 @@ class Info(ctypes.Structure):
                 "shard_rank": self.shard_rank, "shard_count": self.shard_count, "comm_nranks": self.comm_nranks,
                 "comm_version": self.comm_version, "term_lo": self.term_lo, "term_hi": self.term_hi,
                 "shard_cost": self.shard_cost, "total_cost": self.total_cost,
-                "model_ms_local": self.model_ms_local, "model_ms_global": self.model_ms_global}
+                "model_ms_local": self.model_ms_local, "model_ms_global": self.model_ms_global,
+                "plan_terms": self.plan_terms, "split_terms": self.split_terms}
 
 
 class HMatrixInfo(ctypes.Structure):
