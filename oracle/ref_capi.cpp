@@ -15,6 +15,9 @@
 //                          from an explicit neighbour list instead of an AdaptiveGrid
 //   ref_estimate        -> make_estimator_state + update_samples (adaptivity.cpp:30-37,75-112),
 //                          per-leaf eta as eta_for_cells (adaptivity.cpp:114-121) over explicit boxes
+//   ref_hmatrix_*       -> assemble_hmatrix / HMatrix::matvec / save_hmatrix / load_hmatrix
+//                          (hmatrix.cpp:338-526), compiled verbatim against the Eigen shim
+//                          (oracle/shim/Eigen/Dense: Householder QR, one-sided Jacobi SVD)
 //   ref_apply_batch_threads -> T concurrent ::apply calls on distinct vectors (apply is pure and
 //                          thread-safe, pc_operator.hpp:15-16)
 #include <cmath>
@@ -29,6 +32,7 @@
 
 #include "pcop/adaptivity.hpp"
 #include "pcop/fft.hpp"
+#include "pcop/hmatrix.hpp"
 #include "pcop/impulse.hpp"
 #include "pcop/pc_operator.hpp"
 
@@ -287,6 +291,84 @@ int ref_normal_fill(std::uint64_t seed, std::int64_t count, double* out) {
         std::mt19937_64 gen(seed);
         std::normal_distribution<double> nd(0.0, 1.0);
         for (std::int64_t i = 0; i < count; ++i) out[i] = nd(gen);
+    });
+}
+
+// --- H-matrix (hmatrix.cpp) -------------------------------------------------------------------
+void* ref_hmatrix_assemble(void* h, double tol, int leaf_cap, int method, int fixed_rank) {
+    HMatrix* out = nullptr;
+    const int rc = guarded([&] {
+        auto* o = static_cast<RefOp*>(h);
+        out = new HMatrix(assemble_hmatrix(o->op, tol, leaf_cap,
+                                           method == 0 ? CompressionMethod::Randomized : CompressionMethod::Cur,
+                                           fixed_rank));
+    });
+    return rc == 0 ? out : nullptr;
+}
+
+void ref_hmatrix_destroy(void* hm) { delete static_cast<HMatrix*>(hm); }
+
+int ref_hmatrix_save(void* hm, const char* path) {
+    return guarded([&] { save_hmatrix(*static_cast<HMatrix*>(hm), path); });
+}
+
+void* ref_hmatrix_load(const char* path) {
+    HMatrix* out = nullptr;
+    const int rc = guarded([&] { out = new HMatrix(load_hmatrix(path)); });
+    return rc == 0 ? out : nullptr;
+}
+
+int ref_hmatrix_matvec(void* hm, const double* f, double* g) {
+    return guarded([&] {
+        auto* H = static_cast<HMatrix*>(hm);
+        const auto n = static_cast<Eigen::Index>(H->tree.domain().num_points());
+        Eigen::VectorXd out = H->matvec(Eigen::VectorXd(f, n));
+        std::memcpy(g, out.data(), static_cast<std::size_t>(out.size()) * sizeof(double));
+    });
+}
+
+// counts[0..4] = {blocks, low-rank blocks, max rank, any_rank_capped, nodes}
+int ref_hmatrix_info(void* hm, std::int64_t* counts) {
+    return guarded([&] {
+        auto* H = static_cast<HMatrix*>(hm);
+        std::int64_t lr = 0, mr = 0;
+        for (const auto& b : H->blocks)
+            if (b.low_rank) {
+                ++lr;
+                mr = std::max<std::int64_t>(mr, b.factors.rank());
+            }
+        counts[0] = static_cast<std::int64_t>(H->blocks.size());
+        counts[1] = lr;
+        counts[2] = mr;
+        counts[3] = H->any_rank_capped ? 1 : 0;
+        counts[4] = static_cast<std::int64_t>(H->tree.nodes().size());
+    });
+}
+
+// block i: {t, s, low_rank, rows, cols, rank}; B (rows x rank), C (rank x cols) or dense, row-major
+int ref_hmatrix_block(void* hm, std::int64_t i, std::int64_t* meta, double* B, double* C, double* dense) {
+    return guarded([&] {
+        auto* H = static_cast<HMatrix*>(hm);
+        const HBlock& b = H->blocks.at(static_cast<std::size_t>(i));
+        const ClusterNode& tn = H->tree.node(b.t_node);
+        const ClusterNode& sn = H->tree.node(b.s_node);
+        meta[0] = b.t_node;
+        meta[1] = b.s_node;
+        meta[2] = b.low_rank ? 1 : 0;
+        meta[3] = tn.size();
+        meta[4] = sn.size();
+        meta[5] = b.low_rank ? b.factors.rank() : 0;
+        auto put = [](const Eigen::MatrixXd& m, double* out) {
+            if (!out) return;
+            for (Eigen::Index r = 0; r < m.rows(); ++r)
+                for (Eigen::Index c = 0; c < m.cols(); ++c) out[r * m.cols() + c] = m(r, c);
+        };
+        if (b.low_rank) {
+            put(b.factors.B, B);
+            put(b.factors.C, C);
+        } else {
+            put(b.dense, dense);
+        }
     });
 }
 

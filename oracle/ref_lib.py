@@ -41,6 +41,15 @@ def lib():
         L.ref_entries.argtypes = [ctypes.c_void_p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _dp]
         L.ref_apply_block.argtypes = [ctypes.c_void_p] + [ctypes.POINTER(_i64)] * 4 + [_dp, ctypes.c_int, _dp]
         L.ref_normal_fill.argtypes = [ctypes.c_uint64, _i64, _dp]
+        L.ref_hmatrix_assemble.restype = ctypes.c_void_p
+        L.ref_hmatrix_assemble.argtypes = [ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.ref_hmatrix_destroy.argtypes = [ctypes.c_void_p]
+        L.ref_hmatrix_save.argtypes = [ctypes.c_void_p, ctypes.c_char_p]
+        L.ref_hmatrix_load.restype = ctypes.c_void_p
+        L.ref_hmatrix_load.argtypes = [ctypes.c_char_p]
+        L.ref_hmatrix_matvec.argtypes = [ctypes.c_void_p, _dp, _dp]
+        L.ref_hmatrix_info.argtypes = [ctypes.c_void_p, ctypes.POINTER(_i64)]
+        L.ref_hmatrix_block.argtypes = [ctypes.c_void_p, _i64, ctypes.POINTER(_i64), _dp, _dp, _dp]
         L.ref_estimate.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _dp, ctypes.c_int, ctypes.POINTER(_i64),
                                    ctypes.POINTER(_i64), _dp, _dp, _dp, _dp]
         _lib = L
@@ -141,6 +150,60 @@ class RefOperator:
                                   hi.ctypes.data_as(ctypes.POINTER(_i64)), _dptr(yt), _dptr(cells),
                                   ctypes.byref(ea), ctypes.byref(er)))
         return yt, cells, ea.value, er.value
+
+
+class RefHMatrix:
+    """The reference's assemble_hmatrix / HMatrix / PCHM container (hmatrix.cpp:338-526), compiled
+    verbatim against oracle/shim/Eigen (Householder QR, one-sided Jacobi SVD)."""
+
+    def __init__(self, handle, N: int):
+        if not handle:
+            raise RuntimeError(f"reference H-matrix failed: {lib().ref_last_error().decode()}")
+        self.h = handle
+        self.N = N
+
+    @classmethod
+    def assemble(cls, op: "RefOperator", tol: float, leaf_cap: int, method: str = "randomized",
+                 fixed_rank: int = 0) -> "RefHMatrix":
+        m = {"randomized": 0, "cur": 1}[method]
+        return cls(lib().ref_hmatrix_assemble(op.h, float(tol), int(leaf_cap), m, int(fixed_rank)), op.N)
+
+    @classmethod
+    def load(cls, path: str, N: int) -> "RefHMatrix":
+        return cls(lib().ref_hmatrix_load(str(path).encode()), N)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_hmatrix_destroy(self.h)
+            self.h = None
+
+    def save(self, path: str) -> None:
+        _check(lib().ref_hmatrix_save(self.h, str(path).encode()))
+
+    def matvec(self, f: np.ndarray) -> np.ndarray:
+        f = np.ascontiguousarray(f, dtype=np.float64).reshape(-1)
+        g = np.zeros(self.N)
+        _check(lib().ref_hmatrix_matvec(self.h, _dptr(f), _dptr(g)))
+        return g
+
+    def info(self) -> dict:
+        c = (_i64 * 5)()
+        _check(lib().ref_hmatrix_info(self.h, c))
+        return {"n_blocks": c[0], "n_low_rank": c[1], "max_rank": c[2], "any_rank_capped": bool(c[3]),
+                "n_nodes": c[4]}
+
+    def block(self, i: int):
+        """(t_node, s_node, low_rank, B, C, dense) of block i."""
+        meta = (_i64 * 6)()
+        _check(lib().ref_hmatrix_block(self.h, int(i), meta, None, None, None))
+        t, s, lr, rows, cols, rank = (int(v) for v in meta)
+        if lr:
+            B, C = np.zeros((rows, rank)), np.zeros((rank, cols))
+            _check(lib().ref_hmatrix_block(self.h, int(i), meta, _dptr(B), _dptr(C), None))
+            return t, s, True, B, C, None
+        D = np.zeros((rows, cols))
+        _check(lib().ref_hmatrix_block(self.h, int(i), meta, None, None, _dptr(D)))
+        return t, s, False, None, None, D
 
 
 def normal_vectors(seed: int, count: int, n: int) -> np.ndarray:

@@ -141,3 +141,25 @@ def test_pchm_errors(tmp_path):
         HMatrix.cluster_tree(((0,), (9,)), 0)
     with pytest.raises(ValueError, match="size mismatch"):
         h.matvec(np.zeros(3))
+
+
+def test_oracle_tree_and_partition_vs_reference_pchm(tmp_path):
+    """The numpy restatement (oracle/hmatrix_oracle.py) against the reference's own PCHM files
+    (tests/golden/hmatrix_ref_*.pchm.gz, assemble_hmatrix + save_hmatrix compiled verbatim)."""
+    import gzip
+    import os
+
+    from oracle import hmatrix_oracle as HO
+    from paper_1805_06018_b200 import inputs
+
+    inp = inputs.small_lattice(n=12, dim=2, m=2, sigma=3.0)
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    for method in ("randomized", "cur"):
+        p = tmp_path / f"{method}.pchm"
+        p.write_bytes(gzip.decompress((open(os.path.join(gold, f"hmatrix_ref_{method}.pchm.gz"), "rb").read())))
+        d = HO.read_pchm(str(p))
+        o = HO.Tree(inp.dom_lo, inp.dom_hi, 16)
+        assert list(d["perm"]) == o.perm
+        assert [(n["begin"], n["end"], n["split_axis"], n["child_lo"], n["child_hi"]) for n in d["nodes"]] == \
+            [(n["begin"], n["end"], n["split_axis"], n["child_lo"], n["child_hi"]) for n in o.nodes]
+        assert [(t, s, lr) for t, s, lr, *_ in d["blocks"]] == HO.partition(o)
