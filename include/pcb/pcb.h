@@ -289,6 +289,12 @@ PCB_API pcb_status pcb_hmatrix_matvec(pcb_hmatrix* h, const double* f, double* g
 PCB_API pcb_status pcb_hmatrix_save(pcb_hmatrix* h, const char* path);
 PCB_API pcb_status pcb_hmatrix_load(const char* path, pcb_hmatrix** out);
 
+/* Debug: with PCB_GUARD=1 in the environment every device allocation of the library carries a
+ * 64 KiB canary band before and after it.  Synchronizes the device and counts the guarded
+ * allocations alive and the canary bytes that were overwritten (out-of-bounds writes); both are 0
+ * without PCB_GUARD. */
+PCB_API pcb_status pcb_debug_guard_check(int64_t* n_regions, int64_t* n_bad_bytes);
+
 /* Number of kernels this library has launched in the process (all handles). */
 PCB_API long long pcb_launch_count(void);
 

@@ -101,9 +101,12 @@ class RefOperator:
             raise RuntimeError(f"ref_create failed: {L.ref_last_error().decode()}")
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().ref_destroy(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().ref_destroy(self.h)
+                self.h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     def apply(self, f: np.ndarray, adjoint: bool = False) -> np.ndarray:
         f = np.ascontiguousarray(f, dtype=np.float64).reshape(-1)
@@ -173,9 +176,12 @@ class RefHMatrix:
         return cls(lib().ref_hmatrix_load(str(path).encode()), N)
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().ref_hmatrix_destroy(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().ref_hmatrix_destroy(self.h)
+                self.h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     def save(self, path: str) -> None:
         _check(lib().ref_hmatrix_save(self.h, str(path).encode()))

@@ -59,6 +59,25 @@ struct Fail {
         if (e_ != cudaSuccess) fail(PCB_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+// Guard bands (PCB_GUARD=1, a debug mode): every device allocation of the library gets kGuard bytes
+// of a 0xA5 canary before and after it; pcb_debug_guard_check() reports canary bytes that changed,
+// i.e. out-of-bounds writes by any kernel into the 64 KiB around any pool.  (compute-sanitizer is
+// disabled on the GPU pool this was built on; this is the library's own bounds check.)
+constexpr size_t kGuard = (size_t)1 << 16;
+bool guard_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("PCB_GUARD");
+        return e && std::atoi(e) != 0;
+    }();
+    return on;
+}
+struct GuardReg {
+    char* base;
+    size_t bytes;  // user bytes between the two guards
+};
+std::mutex g_guard_mu;
+std::vector<GuardReg> g_guards;
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
@@ -82,19 +101,44 @@ struct DevBuf {
     }
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            if (guard_on()) {
+                char* base = reinterpret_cast<char*>(p) - kGuard;
+                std::lock_guard<std::mutex> lk(g_guard_mu);
+                for (size_t i = 0; i < g_guards.size(); ++i)
+                    if (g_guards[i].base == base) {
+                        g_guards.erase(g_guards.begin() + (std::ptrdiff_t)i);
+                        break;
+                    }
+                cudaFree(base);
+            } else {
+                cudaFree(p);
+            }
+        }
         p = nullptr;
         n = 0;
     }
     void alloc(size_t cnt) {
         release();
         if (cnt == 0) return;
-        cudaError_t e = cudaMalloc(&p, cnt * sizeof(T));
+        const bool g = guard_on();
+        void* raw = nullptr;
+        cudaError_t e = cudaMalloc(&raw, cnt * sizeof(T) + (g ? 2 * kGuard : 0));
         if (e != cudaSuccess) {
-            p = nullptr;
             (void)cudaGetLastError();
             fail(PCB_ENOMEM, "cudaMalloc of " + std::to_string(cnt * sizeof(T)) + " bytes failed: " +
                                  cudaGetErrorString(e));
+        }
+        if (g) {
+            char* base = static_cast<char*>(raw);
+            if (cudaMemset(base, 0xA5, kGuard) != cudaSuccess ||
+                cudaMemset(base + kGuard + cnt * sizeof(T), 0xA5, kGuard) != cudaSuccess)
+                fail(PCB_ECUDA, "guard band fill failed");
+            std::lock_guard<std::mutex> lk(g_guard_mu);
+            g_guards.push_back({base, cnt * sizeof(T)});
+            p = reinterpret_cast<T*>(base + kGuard);
+        } else {
+            p = static_cast<T*>(raw);
         }
         n = cnt;
     }
@@ -279,7 +323,7 @@ struct pcb_op {
     // host-call staging
     pcb::DevBuf<double> st_in, st_out, st_aux;
     pcb::DevBuf<int64_t> st_i64a, st_i64b;
-    pcb::DevBuf<int32_t> st_flag, st_shape;
+    pcb::DevBuf<int32_t> st_flag, st_shape, st_blk;
     cudaStream_t stream = nullptr;
     pcb_info info{};
     // per-kernel event profiling (pcb_profile_begin / pcb_profile_end)
@@ -1947,6 +1991,26 @@ PCB_API void pcb_default_options(pcb_options* opt) {
 
 PCB_API const char* pcb_last_error(void) { return g_err.c_str(); }
 
+PCB_API pcb_status pcb_debug_guard_check(int64_t* n_regions, int64_t* n_bad_bytes) {
+    return guarded([&] {
+        if (!n_regions || !n_bad_bytes) fail(PCB_EINVAL, "pcb_debug_guard_check: null argument");
+        *n_regions = 0;
+        *n_bad_bytes = 0;
+        if (!guard_on()) return;
+        PCB_CK(cudaDeviceSynchronize());
+        std::lock_guard<std::mutex> lk(g_guard_mu);
+        std::vector<unsigned char> h(kGuard);
+        for (const GuardReg& r : g_guards) {
+            for (int side = 0; side < 2; ++side) {
+                const char* src = side == 0 ? r.base : r.base + kGuard + r.bytes;
+                PCB_CK(cudaMemcpy(h.data(), src, kGuard, cudaMemcpyDeviceToHost));
+                for (unsigned char c : h) *n_bad_bytes += c != 0xA5;
+            }
+            ++*n_regions;
+        }
+    });
+}
+
 PCB_API pcb_status pcb_comm_unique_id(void* id128) {
     if (!id128) {
         set_err("pcb_comm_unique_id: null output");
@@ -2423,10 +2487,12 @@ static void blocks_common(pcb_op* op, int32_t nblk, const int64_t* d_t, const in
     }
     op->st_shape.ensure(3);
     op->st_flag.ensure(1);
+    op->st_blk.ensure((size_t)blocks_scratch_ints(nblk));
     PCB_CK(cudaMemcpyAsync(op->st_shape.p, bs, sizeof(bs), cudaMemcpyHostToDevice, st));
     PCB_CK(cudaMemsetAsync(op->st_flag.p, 0, 4, st));
     launch(op, st, "blocks", [&] {
-        return launch_blocks(entry_args(op), nblk, d_t, d_s, op->st_shape.p, bs, d_out, op->st_flag.p, st);
+        return launch_blocks(entry_args(op), nblk, d_t, d_s, op->st_shape.p, bs, d_out, op->st_flag.p, op->st_blk.p,
+                             st);
     });
     if (host_check) {
         int32_t bad = 0;

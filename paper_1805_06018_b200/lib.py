@@ -34,7 +34,7 @@ EXPORTS = ["pcb_default_options", "pcb_last_error", "pcb_create", "pcb_destroy",
            "pcb_get_domain", "pcb_cluster_tree", "pcb_hmatrix_assemble", "pcb_hmatrix_compress",
            "pcb_hmatrix_destroy", "pcb_hmatrix_get_info", "pcb_hmatrix_tree", "pcb_hmatrix_block",
            "pcb_hmatrix_admissible", "pcb_hmatrix_matvec", "pcb_hmatrix_save", "pcb_hmatrix_load",
-           "pcb_comm_unique_id", "pcb_plan_shards"]
+           "pcb_comm_unique_id", "pcb_plan_shards", "pcb_debug_guard_check"]
 REDUCE = {"none": 0, "all": 1, "root": 2}
 PARTITION = {"cost": 0, "count": 1}
 
@@ -146,6 +146,7 @@ def load():
     L.pcb_hmatrix_save.argtypes = [vp, ctypes.c_char_p]
     L.pcb_hmatrix_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
     L.pcb_comm_unique_id.argtypes = [vp]
+    L.pcb_debug_guard_check.argtypes = [P_i64, P_i64]
     L.pcb_plan_shards.argtypes = [i32, P_i64, P_i64, i32, P_i64, P_i64, ctypes.POINTER(vp), P_i64, P_i64,
                                   ctypes.POINTER(vp), i32, i32, vp, vp]
     for n in EXPORTS:
@@ -180,3 +181,10 @@ def comm_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     check(load().pcb_comm_unique_id(buf))
     return buf.raw
+
+
+def guard_check():
+    """(guarded allocations, overwritten canary bytes) -- PCB_GUARD=1 debug mode (pcb_debug_guard_check)."""
+    a, b = i64(), i64()
+    check(load().pcb_debug_guard_check(ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value

@@ -1,7 +1,7 @@
 """GPU checks beyond parity: the FFT engine unit test, the library's NCCL shard reduce on a 1-rank
 communicator, cost-balanced k-shards, and the host-buffer pipeline with many sub-batches (pinned
 and pageable).  (compute-sanitizer is disabled on this GPU pool -- its wrapper refuses to run --
-so memory safety is covered by the guard-band canary test in tests/test_gpu_guard.py.)"""
+so out-of-bounds writes are caught by the library's own guard bands, test_guard_bands.)"""
 import os
 import subprocess
 import sys
@@ -29,6 +29,17 @@ def test_fft_engine_unit(gpu, cfg):
         exe = build.build_tools()[list(dict.fromkeys(build.FFT_UNIT_CONFIGS)).index(cfg)]
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "all lengths OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("graphs", ["1", "0"])
+def test_guard_bands(gpu, graphs):
+    """No kernel writes out of bounds: every device allocation carries 64 KiB canary bands
+    (PCB_GUARD=1) and every entry point runs on c1/c3/c4/1-D/3-D/long-line operators
+    (tests/guard_target.py), with CUDA graphs on and off."""
+    env = dict(os.environ, PCB_GUARD="1", PCB_GRAPHS=graphs)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "guard_target.py")], capture_output=True,
+                       text=True, timeout=900, env=env)
+    assert r.returncode == 0 and "GUARD TARGET OK" in r.stdout, (r.stdout + r.stderr)[-4000:]
 
 
 def test_nccl_reduce_one_rank(gpu):
