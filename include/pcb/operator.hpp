@@ -41,6 +41,31 @@ inline void check(pcb_status st) {
     throw std::runtime_error(msg);
 }
 
+// A fresh 128-byte NCCL id for pcb_options.nccl_id (shard-by-k with the reduce inside the
+// library): create it on one rank and send it to the others (MPI_Bcast, a file, a socket ...).
+inline std::vector<unsigned char> comm_unique_id() {
+    std::vector<unsigned char> id(128);
+    check(pcb_comm_unique_id(id.data()));
+    return id;
+}
+
+// Options of one shard of a k-sharded operator: this process owns the cost-balanced
+// block `rank` of `count`; with `nccl_id` every apply sums the shards' partials over NCCL
+// (`reduce`: PCB_REDUCE_ALL -> every rank gets the full result, PCB_REDUCE_ROOT -> rank 0).
+inline pcb_options shard_options(int32_t rank, int32_t count, const std::vector<unsigned char>* nccl_id = nullptr,
+                                 int32_t reduce = PCB_REDUCE_ALL, int32_t device = -1) {
+    pcb_options o;
+    pcb_default_options(&o);
+    o.shard_rank = rank;
+    o.shard_count = count;
+    o.device = device;
+    if (nccl_id) {
+        o.nccl_id = nccl_id->data();
+        o.reduce = reduce;
+    }
+    return o;
+}
+
 class ProductConvolutionOperator {
   public:
     ProductConvolutionOperator(const Box& domain, const std::vector<Field>& weights,

@@ -222,141 +222,33 @@ __global__ void k_zero(double* p, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = 0.0;
 }
 
-// K6 for dense blocks (config 5), two passes:
-//  k_blocks_classify: one warp per block finds its candidate terms -- listed in the buckets
-//    covering S, deduplicated, kept only when X_k meets S and the kernel box K_k meets the offsets
-//    T - S (any other term reads phi^E = 0 there: exact zeros, which leave the sum unchanged) -- in
-//    ascending k, the reference's summation order.  A block with no candidate is all zeros and the
-//    warp writes it with 16-byte stores; the others are appended to a work list with their
-//    candidates.  (Config 5: 65 of the 4096 seed-3 blocks have candidates.)
-//  k_blocks_tiled: one CTA per listed block stages the candidates' weights on S and phi^E windows
-//    over T - S ((2 bs - 1) per axis) in shared memory; every entry sums over the staged terms in
-//    ascending k with the reference's IEEE mul/add -- the same terms in the same order as
-//    entry_value, so the result is bit-identical.  Blocks that leave the domain or have too many
-//    candidates take the per-entry path.
+// K6 for dense blocks (config 5), one CTA per 8 blocks, two phases:
+//  1. classify (one warp per block): the block's candidate terms -- listed in the buckets covering
+//     S, deduplicated, kept only when X_k meets S and the kernel box K_k meets the offsets T - S (any
+//     other term reads phi^E = 0 there: exact zeros, which leave the sum unchanged) -- in ascending
+//     k, the reference's summation order.  A block with no candidate is all zeros and its warp
+//     writes it with 16-byte stores (config 5: 4031 of the 4096 seed-3 blocks).
+//  2. gather (the whole CTA, block by block, for the CTA's blocks that have candidates): stage the
+//     candidates' weights on S and phi^E windows over T - S ((2 bs - 1) per axis) in shared memory;
+//     every entry sums over the staged terms in ascending k with the reference's IEEE mul/add --
+//     the same terms in the same order as entry_value, so the result is bit-identical.  Blocks that
+//     leave the domain or have too many candidates take the per-entry path.
+// Zero blocks cost one warp's stores; the few gathered blocks overlap the other CTAs' stores
+// instead of waiting behind them at a kernel boundary.
 constexpr int BT_CAP = 32;  // max staged candidate terms per block
 constexpr int BT_IDS = 64;  // gathered bucket entries (with duplicates) per block
 constexpr int BT_NZ = 8;    // listed nonzero-weight terms per source point
-constexpr int BC_WARPS = 8; // classify: warps (blocks) per CTA
+constexpr int BC_WARPS = 8; // blocks (classifying warps) per CTA
 
-__global__ void __launch_bounds__(256) k_blocks_classify(EntryArgs a, int32_t nblk, const int64_t* __restrict__ t_origin,
-                                                         const int64_t* __restrict__ s_origin, int bs0, int bs1,
-                                                         int bs2, int cap, double* __restrict__ out,
-                                                         int32_t* __restrict__ work, int32_t* __restrict__ cand_g) {
-    __shared__ int ids_s[BC_WARPS][BT_IDS];
-    __shared__ int first_s[BC_WARPS][BT_IDS];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int blk = blockIdx.x * BC_WARPS + wid;
-    if (blk >= nblk) return;
-    int* ids = ids_s[wid];
-    int* first = first_s[wid];
-    const int D = a.D;
-    const int bs[3] = {bs0, bs1, bs2};
-    int64_t tv[3], sv[3];
-    int fb = 0;
-    for (int i = 0; i < 3; ++i) {
-        tv[i] = i < D ? t_origin[(int64_t)blk * D + i] : 0;
-        sv[i] = i < D ? s_origin[(int64_t)blk * D + i] : 0;
-        if (i < D && (tv[i] < a.dom_lo[i] || tv[i] + bs[i] > a.dom_lo[i] + a.n[i] || sv[i] < a.dom_lo[i] ||
-                      sv[i] + bs[i] > a.dom_lo[i] + a.n[i]))
-            fb = 1;
-    }
-    int nk = 0;
-    if (!fb) {
-        int blo[3] = {0, 0, 0}, bn[3] = {1, 1, 1}, nbk = 1;
-        for (int i = 0; i < D; ++i) {
-            blo[i] = (int)((sv[i] - a.dom_lo[i]) / a.bucket[i]);
-            bn[i] = (int)((sv[i] + bs[i] - 1 - a.dom_lo[i]) / a.bucket[i]) - blo[i] + 1;
-            nbk *= bn[i];
-        }
-        int64_t beg = 0;
-        int cnt = 0;
-        if (nbk <= 32 && lane < nbk) {
-            int r = lane, c[3] = {0, 0, 0};
-            for (int i = D - 1; i >= 0; --i) {
-                c[i] = blo[i] + r % bn[i];
-                r /= bn[i];
-            }
-            int64_t bl = 0;
-            for (int i = 0; i < D; ++i) bl = bl * a.nb[i] + c[i];
-            beg = a.bucket_ptr[bl];
-            cnt = (int)(a.bucket_ptr[bl + 1] - beg);
-        }
-        int off = cnt;  // inclusive warp prefix sum
-        for (int d = 1; d < 32; d <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, off, d);
-            if (lane >= d) off += v;
-        }
-        const int total = __shfl_sync(0xffffffffu, off, 31);
-        off -= cnt;
-        if (nbk > 32 || total > BT_IDS) {
-            fb = 1;
-        } else {
-            for (int q = 0; q < cnt; ++q) ids[off + q] = a.bucket_terms[beg + q];
-            __syncwarp();
-            int keep[2] = {0, 0}, idv[2] = {0, 0};
-            for (int h = 0; h < 2; ++h) {
-                const int pos = lane + 32 * h;
-                if (pos >= total) continue;
-                const int id = ids[pos];
-                int f = 1;
-                for (int j = 0; j < pos; ++j) f &= ids[j] != id;
-                if (f) {
-                    const TermDesc& t = a.terms[id];
-                    for (int d = 0; d < D && f; ++d) {
-                        const int64_t o = tv[d] - sv[d];
-                        f &= (t.x_lo[d] <= sv[d] + bs[d] - 1) && (t.x_lo[d] + t.m[d] - 1 >= sv[d]) &&
-                             (t.k_lo[d] <= o + bs[d] - 1) && (t.k_lo[d] + t.k_ext[d] - 1 >= o - (bs[d] - 1));
-                    }
-                }
-                keep[h] = f;
-                idv[h] = id;
-                first[pos] = f ? id : -1;
-            }
-            __syncwarp();
-            nk = __popc(__ballot_sync(0xffffffffu, keep[0])) + __popc(__ballot_sync(0xffffffffu, keep[1]));
-            if (nk > cap) {
-                fb = 1;
-            } else {
-                for (int h = 0; h < 2; ++h) {
-                    if (!keep[h]) continue;
-                    int rank = 0;
-                    for (int j = 0; j < total; ++j) rank += first[j] >= 0 && first[j] < idv[h];
-                    cand_g[(int64_t)blk * (cap + 1) + 1 + rank] = idv[h];
-                }
-            }
-        }
-    }
-    if (!fb && nk == 0) {  // no term can contribute: an all-zero block
-        int npx = 1;
-        for (int i = 0; i < D; ++i) npx *= bs[i];
-        const int64_t n2 = (int64_t)npx * npx;
-        double* ob = out + (int64_t)blk * n2;
-        if ((reinterpret_cast<uintptr_t>(ob) & 15) == 0) {
-            double2* o2 = reinterpret_cast<double2*>(ob);
-            for (int64_t e = lane; e < n2 / 2; e += 32) o2[e] = make_double2(0.0, 0.0);
-            if ((n2 & 1) && lane == 0) ob[n2 - 1] = 0.0;
-        } else {
-            for (int64_t e = lane; e < n2; e += 32) ob[e] = 0.0;
-        }
-        return;
-    }
-    if (lane == 0) {
-        cand_g[(int64_t)blk * (cap + 1)] = fb ? -1 : nk;
-        const int slot = atomicAdd(work, 1);
-        work[1 + slot] = blk;
-    }
-}
-
-__global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, const int32_t* __restrict__ work,
-                                                      const int32_t* __restrict__ cand_g,
-                                                      const int64_t* __restrict__ t_origin,
+__global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk, const int64_t* __restrict__ t_origin,
                                                       const int64_t* __restrict__ s_origin, int bs0, int bs1, int bs2,
                                                       int cap, double* __restrict__ out, int32_t* bad) {
     extern __shared__ double sm[];
-    __shared__ int64_t s_t[3], s_s[3];
-    __shared__ int s_nc, s_blk;
-    __shared__ int cand[BT_CAP];
+    __shared__ int ids_s[BC_WARPS][BT_IDS];
+    __shared__ int first_s[BC_WARPS][BT_IDS];
+    __shared__ int cand_s[BC_WARPS][BT_CAP];
+    __shared__ int nc_s[BC_WARPS];  // candidates; 0: zero block (written), -1: per-entry path
+    __shared__ int64_t org_s[BC_WARPS][6];
     const int D = a.D;
     const int bs[3] = {bs0, bs1, bs2};
     int npx = 1, win = 1;
@@ -364,12 +256,117 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, const int32_t
         npx *= bs[i];
         win *= 2 * bs[i] - 1;
     }
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    // ---- phase 1: classify (warp wid <-> block blk) ----
+    {
+        const int blk = blockIdx.x * BC_WARPS + wid;
+        int* ids = ids_s[wid];
+        int* first = first_s[wid];
+        int64_t tv[3] = {0, 0, 0}, sv[3] = {0, 0, 0};
+        int fb = 0, nk = 0;
+        if (blk < nblk) {
+            for (int i = 0; i < D; ++i) {
+                tv[i] = t_origin[(int64_t)blk * D + i];
+                sv[i] = s_origin[(int64_t)blk * D + i];
+                if (tv[i] < a.dom_lo[i] || tv[i] + bs[i] > a.dom_lo[i] + a.n[i] || sv[i] < a.dom_lo[i] ||
+                    sv[i] + bs[i] > a.dom_lo[i] + a.n[i])
+                    fb = 1;
+            }
+            if (!fb) {
+                int blo[3] = {0, 0, 0}, bn[3] = {1, 1, 1}, nbk = 1;
+                for (int i = 0; i < D; ++i) {
+                    blo[i] = (int)((sv[i] - a.dom_lo[i]) / a.bucket[i]);
+                    bn[i] = (int)((sv[i] + bs[i] - 1 - a.dom_lo[i]) / a.bucket[i]) - blo[i] + 1;
+                    nbk *= bn[i];
+                }
+                int64_t beg = 0;
+                int cnt = 0;
+                if (nbk <= 32 && lane < nbk) {
+                    int r = lane, c[3] = {0, 0, 0};
+                    for (int i = D - 1; i >= 0; --i) {
+                        c[i] = blo[i] + r % bn[i];
+                        r /= bn[i];
+                    }
+                    int64_t bl = 0;
+                    for (int i = 0; i < D; ++i) bl = bl * a.nb[i] + c[i];
+                    beg = a.bucket_ptr[bl];
+                    cnt = (int)(a.bucket_ptr[bl + 1] - beg);
+                }
+                int off = cnt;  // inclusive warp prefix sum
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, off, d);
+                    if (lane >= d) off += v;
+                }
+                const int total = __shfl_sync(0xffffffffu, off, 31);
+                off -= cnt;
+                if (nbk > 32 || total > BT_IDS) {
+                    fb = 1;
+                } else {
+                    for (int q = 0; q < cnt; ++q) ids[off + q] = a.bucket_terms[beg + q];
+                    __syncwarp();
+                    int keep[2] = {0, 0}, idv[2] = {0, 0};
+                    for (int h = 0; h < 2; ++h) {
+                        const int pos = lane + 32 * h;
+                        if (pos >= total) continue;
+                        const int id = ids[pos];
+                        int f = 1;
+                        for (int j = 0; j < pos; ++j) f &= ids[j] != id;
+                        if (f) {
+                            const TermDesc& t = a.terms[id];
+                            for (int d = 0; d < D && f; ++d) {
+                                const int64_t o = tv[d] - sv[d];
+                                f &= (t.x_lo[d] <= sv[d] + bs[d] - 1) && (t.x_lo[d] + t.m[d] - 1 >= sv[d]) &&
+                                     (t.k_lo[d] <= o + bs[d] - 1) && (t.k_lo[d] + t.k_ext[d] - 1 >= o - (bs[d] - 1));
+                            }
+                        }
+                        keep[h] = f;
+                        idv[h] = id;
+                        first[pos] = f ? id : -1;
+                    }
+                    __syncwarp();
+                    nk = __popc(__ballot_sync(0xffffffffu, keep[0])) + __popc(__ballot_sync(0xffffffffu, keep[1]));
+                    if (nk > cap) {
+                        fb = 1;
+                    } else {
+                        for (int h = 0; h < 2; ++h) {
+                            if (!keep[h]) continue;
+                            int rank = 0;
+                            for (int j = 0; j < total; ++j) rank += first[j] >= 0 && first[j] < idv[h];
+                            cand_s[wid][rank] = idv[h];
+                        }
+                    }
+                }
+            }
+            if (!fb && nk == 0) {  // no term can contribute: an all-zero block
+                const int64_t n2 = (int64_t)npx * npx;
+                double* ob = out + (int64_t)blk * n2;
+                if ((reinterpret_cast<uintptr_t>(ob) & 15) == 0) {
+                    double2* o2 = reinterpret_cast<double2*>(ob);
+                    for (int64_t e = lane; e < n2 / 2; e += 32) o2[e] = make_double2(0.0, 0.0);
+                    if ((n2 & 1) && lane == 0) ob[n2 - 1] = 0.0;
+                } else {
+                    for (int64_t e = lane; e < n2; e += 32) ob[e] = 0.0;
+                }
+            }
+        }
+        if (lane == 0) {
+            nc_s[wid] = blk >= nblk ? 0 : fb ? -1 : nk;
+            for (int i = 0; i < 3; ++i) {
+                org_s[wid][i] = tv[i];
+                org_s[wid][3 + i] = sv[i];
+            }
+        }
+    }
+    __syncthreads();
+    // ---- phase 2: the CTA gathers its blocks that have candidates ----
     double* W = sm;               // [cap][npx]
     double* PH = sm + cap * npx;  // [cap][win]
     int* offs = reinterpret_cast<int*>(PH + cap * win);              // [npx] window offset of a point
     unsigned char* nzn = reinterpret_cast<unsigned char*>(offs + npx);  // [npx] nonzero-term count
     unsigned char* nzc = nzn + npx;                                   // [npx][BT_NZ] their indices
-    const int tid = threadIdx.x;
+    int any = 0;
+    for (int w = 0; w < BC_WARPS; ++w) any |= nc_s[w] != 0;
+    if (!any) return;
     int centre = 0;
     {
         int mul = 1;
@@ -387,23 +384,15 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, const int32_t
         }
         offs[p] = o;
     }
-    const int nwork = work[0];
-    for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
-        __syncthreads();
-        if (tid == 0) {
-            const int blk = work[1 + wi];
-            s_blk = blk;
-            for (int i = 0; i < 3; ++i) {
-                s_t[i] = i < D ? t_origin[(int64_t)blk * D + i] : 0;
-                s_s[i] = i < D ? s_origin[(int64_t)blk * D + i] : 0;
-            }
-            s_nc = cand_g[(int64_t)blk * (cap + 1)];
-        }
-        __syncthreads();
-        const int blk = s_blk;
-        const int nc = s_nc;
-        if (nc > 0 && tid < nc) cand[tid] = cand_g[(int64_t)blk * (cap + 1) + 1 + tid];
+    for (int w = 0; w < BC_WARPS; ++w) {
+        const int nc = nc_s[w];
+        if (nc == 0) continue;
+        const int blk = blockIdx.x * BC_WARPS + w;
+        const int64_t* s_t = org_s[w];
+        const int64_t* s_s = org_s[w] + 3;
+        const int* cand = cand_s[w];
         double* ob = out + (int64_t)blk * npx * npx;
+        __syncthreads();
         if (nc < 0) {  // per-entry path (out-of-domain entries flag `bad`)
             for (int e = tid; e < npx * npx; e += blockDim.x) {
                 int i = e / npx, j = e - (e / npx) * npx;
@@ -420,7 +409,6 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, const int32_t
             }
             continue;
         }
-        __syncthreads();
         for (int idx = tid; idx < nc * npx; idx += blockDim.x) {  // w_k on S (0 outside X_k)
             const int c = idx / npx;
             int j = idx - c * npx;
@@ -442,14 +430,14 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, const int32_t
         }
         for (int idx = tid; idx < nc * win; idx += blockDim.x) {  // phi_k^E on the offsets T - S
             const int c = idx / win;
-            int w = idx - c * win;
+            int w2 = idx - c * win;
             const TermDesc& t = a.terms[cand[c]];
             int64_t z[3];
             bool in = true;
             for (int d = D - 1; d >= 0; --d) {
                 const int wd = 2 * bs[d] - 1;
-                z[d] = s_t[d] - s_s[d] + (w % wd) - (bs[d] - 1) - t.k_lo[d];
-                w /= wd;
+                z[d] = s_t[d] - s_s[d] + (w2 % wd) - (bs[d] - 1) - t.k_lo[d];
+                w2 /= wd;
                 in = in && z[d] >= 0 && z[d] < t.k_ext[d];
             }
             double ph = 0.0;
@@ -503,11 +491,11 @@ cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, co
     return cudaGetLastError();
 }
 
-int64_t blocks_scratch_ints(int32_t nblk) { return 1 + (int64_t)nblk + (int64_t)nblk * (BT_CAP + 1); }
+int64_t blocks_scratch_ints(int32_t /*nblk*/) { return 1; }
 
 cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
                           const int32_t* bshape, const int32_t* bshape_host, double* out, int32_t* bad,
-                          int32_t* scratch, cudaStream_t st) {
+                          int32_t* /*scratch*/, cudaStream_t st) {
     if (nblk <= 0) return cudaSuccess;
     int64_t npx = 1, win = 1;
     for (int i = 0; i < a.D; ++i) {
@@ -520,24 +508,14 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
     }();
     const size_t smem = sizeof(double) * (size_t)cap * (size_t)(npx + win) + sizeof(int) * (size_t)npx +
                         (size_t)npx * (1 + BT_NZ) + 16;
-    if (smem <= 160 * 1024) {  // classify (zero blocks written there), then the tiled gather over the rest
+    if (smem <= 160 * 1024) {
         if (smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(k_blocks_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
         }
-        int32_t* work = scratch;                   // [0] count, [1..] block ids
-        int32_t* cand = scratch + 1 + nblk;        // [nblk][cap + 1]: count (-1: per-entry), ids
-        cudaError_t e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);
-        if (e != cudaSuccess) return e;
-        const int bs1 = a.D > 1 ? bshape_host[1] : 1, bs2 = a.D > 2 ? bshape_host[2] : 1;
-        k_blocks_classify<<<(unsigned)((nblk + BC_WARPS - 1) / BC_WARPS), 32 * BC_WARPS, 0, st>>>(
-            a, nblk, t_origin, s_origin, bshape_host[0], bs1, bs2, cap, out, work, cand);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-        const int per_sm = std::max<int>(1, (int)((220 * 1024) / (smem + 2048)));
-        const int grid = (int)std::min<int64_t>(nblk, 148LL * std::min(per_sm, 8));
-        k_blocks_tiled<<<grid, 256, smem, st>>>(a, work, cand, t_origin, s_origin, bshape_host[0], bs1, bs2, cap, out,
-                                                 bad);
+        k_blocks_tiled<<<(unsigned)((nblk + BC_WARPS - 1) / BC_WARPS), 32 * BC_WARPS, smem, st>>>(
+            a, nblk, t_origin, s_origin, bshape_host[0], a.D > 1 ? bshape_host[1] : 1, a.D > 2 ? bshape_host[2] : 1, cap,
+            out, bad);
         return cudaGetLastError();
     }
     k_blocks<<<148 * 16, 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape, out, bad);

@@ -56,6 +56,22 @@ int main() {
             std::printf("mode %d: apply rel %.3e  entry %.17g vs %.17g\n", mode, rel, e, e_want);
             if (!(rel <= 1e-11) || e != e_want) return 1;
         }
+        // shard by k with the NCCL reduce inside the library (a 1-rank communicator here: the
+        // pattern every rank of a multi-GPU job runs)
+        {
+            const std::vector<unsigned char> id = pcb::comm_unique_id();
+            const pcb_options so = pcb::shard_options(0, 1, &id, PCB_REDUCE_ALL);
+            pcb::ProductConvolutionOperator sop(dom, w, phi, &so);
+            const std::vector<double> got = sop.apply(f);
+            double num = 0, den = 0;
+            for (int i = 0; i < n * n; ++i) {
+                num += (got[i] - want[i]) * (got[i] - want[i]);
+                den += want[i] * want[i];
+            }
+            std::printf("sharded (NCCL %d, %d rank): apply rel %.3e\n", sop.info().comm_version, sop.info().comm_nranks,
+                        std::sqrt(num / den));
+            if (!(std::sqrt(num / den) <= 1e-11) || sop.info().comm_nranks != 1) return 4;
+        }
         // reference error behaviour
         pcb::ProductConvolutionOperator op(dom, w, phi);
         try {

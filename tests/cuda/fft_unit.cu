@@ -72,8 +72,11 @@ int run(const double2* dtw) {
             }
             cudaMemcpy(y.data(), dout, sizeof(double2) * NL * L, cudaMemcpyDeviceToHost);
             double err = 0, nrm = 0;
+            // every output bin for L <= 512; for longer lines 512 bins per line (a stride with a
+            // per-line offset, so every residue class is hit across lines and directions)
+            const int kstep = L <= 512 ? 1 : L / 512;
             for (int l = 0; l < NL; ++l)
-                for (int k = 0; k < L; ++k) {
+                for (int k = (l * 7 + (dir > 0) * 3 + rev) % kstep; k < L; k += kstep) {
                     long double re = 0, im = 0;
                     for (int n = 0; n < L; ++n) {
                         const long double ang = dir * 2.0L * 3.141592653589793238462643383279502884L * ((long long)n * k % L) / L;
