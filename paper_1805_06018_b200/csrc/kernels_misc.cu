@@ -57,9 +57,10 @@ __global__ void k_entries(EntryArgs a, int64_t cnt, const int64_t* __restrict__ 
 }
 
 __global__ void k_blocks(EntryArgs a, int32_t nblk, const int64_t* __restrict__ t_origin,
-                         const int64_t* __restrict__ s_origin, const int32_t* __restrict__ bshape,
-                         double* __restrict__ out, int32_t* bad) {
+                         const int64_t* __restrict__ s_origin, int bs0, int bs1, int bs2, double* __restrict__ out,
+                         int32_t* bad) {
     const int D = a.D;
+    const int bshape[3] = {bs0, bs1, bs2};
     int64_t bs = 1;
     for (int i = 0; i < D; ++i) bs *= bshape[i];
     const int64_t total = (int64_t)nblk * bs * bs;
@@ -491,11 +492,8 @@ cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, co
     return cudaGetLastError();
 }
 
-int64_t blocks_scratch_ints(int32_t /*nblk*/) { return 1; }
-
 cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
-                          const int32_t* bshape, const int32_t* bshape_host, double* out, int32_t* bad,
-                          int32_t* /*scratch*/, cudaStream_t st) {
+                          const int32_t* bshape_host, double* out, int32_t* bad, cudaStream_t st) {
     if (nblk <= 0) return cudaSuccess;
     int64_t npx = 1, win = 1;
     for (int i = 0; i < a.D; ++i) {
@@ -518,7 +516,8 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
             out, bad);
         return cudaGetLastError();
     }
-    k_blocks<<<148 * 16, 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape, out, bad);
+    k_blocks<<<148 * 16, 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape_host[0], a.D > 1 ? bshape_host[1] : 1,
+                                       a.D > 2 ? bshape_host[2] : 1, out, bad);
     return cudaGetLastError();
 }
 

@@ -35,6 +35,7 @@
 #include <string>
 #include <vector>
 
+#include <condition_variable>
 #include <thread>
 
 #include "comm.h"
@@ -323,7 +324,7 @@ struct pcb_op {
     // host-call staging
     pcb::DevBuf<double> st_in, st_out, st_aux;
     pcb::DevBuf<int64_t> st_i64a, st_i64b;
-    pcb::DevBuf<int32_t> st_flag, st_shape, st_blk;
+    pcb::DevBuf<int32_t> st_flag;
     cudaStream_t stream = nullptr;
     pcb_info info{};
     // per-kernel event profiling (pcb_profile_begin / pcb_profile_end)
@@ -2314,22 +2315,76 @@ PCB_API pcb_status pcb_apply_adjoint_batch_dev(pcb_op* op, int32_t B, const doub
     return apply_dev_common(op, true, B, dF, dG, stream);
 }
 
-// Host memcpy split over a few threads (pageable caller buffers <-> the pinned bounce slots).
-static void par_memcpy(void* dst, const void* src, size_t bytes) {
-    const size_t grain = (size_t)4 << 20;
-    const int nt = (int)std::min<size_t>(8, std::max<size_t>(1, bytes / grain));
-    if (nt <= 1) {
-        std::memcpy(dst, src, bytes);
-        return;
+// Host copies between pageable caller buffers and the pinned bounce slots: a persistent pool of
+// worker threads (created on first use; PCB_HOST_THREADS, default min(16, cores)) runs a list of
+// copies cut into ~1 MiB pieces, so the copy of sub-batch j+1 in and j-1 out run together on all
+// cores while the GPU works on sub-batch j.
+struct HostCopy {
+    void* dst;
+    const void* src;
+    size_t bytes;
+};
+
+class HostPool {
+  public:
+    static HostPool& get() {
+        static HostPool pool;
+        return pool;
     }
-    std::vector<std::thread> th;
-    const size_t part = (bytes / nt + 63) & ~(size_t)63;
-    for (int t = 0; t < nt; ++t) {
-        const size_t o = std::min(bytes, part * t), e = std::min(bytes, part * (t + 1));
-        if (e > o) th.emplace_back([=] { std::memcpy((char*)dst + o, (const char*)src + o, e - o); });
+    void copy(const std::vector<HostCopy>& list) {
+        const size_t piece = (size_t)1 << 20;
+        std::unique_lock<std::mutex> lk(mu_);
+        for (const HostCopy& c : list)
+            for (size_t o = 0; o < c.bytes; o += piece)
+                q_.push_back({(char*)c.dst + o, (const char*)c.src + o, std::min(piece, c.bytes - o)});
+        pending_ += q_.size();
+        cv_.notify_all();
+        // the caller works too
+        while (!q_.empty()) {
+            HostCopy c = q_.back();
+            q_.pop_back();
+            lk.unlock();
+            std::memcpy(c.dst, c.src, c.bytes);
+            lk.lock();
+            --pending_;
+        }
+        done_.wait(lk, [&] { return pending_ == 0; });
     }
-    for (auto& x : th) x.join();
-}
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+
+  private:
+    HostPool() {
+        int n = (int)std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
+        if (const char* e = std::getenv("PCB_HOST_THREADS")) n = std::max(1, std::atoi(e));
+        for (int i = 0; i < n - 1; ++i) th_.emplace_back([this] { work(); });
+    }
+    void work() {
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {
+            cv_.wait(lk, [&] { return stop_ || !q_.empty(); });
+            if (stop_) return;
+            HostCopy c = q_.back();
+            q_.pop_back();
+            lk.unlock();
+            std::memcpy(c.dst, c.src, c.bytes);
+            lk.lock();
+            if (--pending_ == 0) done_.notify_all();
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    std::vector<HostCopy> q_;
+    size_t pending_ = 0;
+    bool stop_ = false;
+    std::vector<std::thread> th_;
+};
 
 static bool host_pinned(const void* p) {
     cudaPointerAttributes at{};
@@ -2400,23 +2455,17 @@ static pcb_status apply_host_common(pcb_op* op, bool adjoint, int32_t B, const d
             offs[j] = off;
             off += (size_t)sizes[j] * op->N;
         }
-        auto drain = [&](size_t j) {  // pageable G: the bounce copy of sub-batch j out to the caller
-            PCB_CK(cudaEventSynchronize(ev_d2h[j & 1]));
-            par_memcpy(G + offs[j], op->bounce + 2 * slot + (j & 1) * slot, (size_t)sizes[j] * op->N * sizeof(double));
-        };
+        double* bin = op->bounce;                // 2 slots in
+        double* bout = op->bounce ? op->bounce + 2 * slot : nullptr;  // 2 slots out
+        auto bytes_of = [&](size_t j) { return (size_t)sizes[j] * op->N * sizeof(double); };
+        if (!pin_f) HostPool::get().copy({{bin, F, bytes_of(0)}});
         for (size_t j = 0; j < sizes.size(); ++j) {
             const int s = (int)(j & 1);
             const size_t n = (size_t)sizes[j] * op->N;
             double* din = op->st_in.p + s * slot;
             double* dout = op->st_out.p + s * slot;
-            const double* src = F + offs[j];
+            const double* src = pin_f ? F + offs[j] : bin + s * slot;
             if (j >= 2) PCB_CK(cudaStreamWaitEvent(op->s_h2d, ev_k[s], 0));  // kernels j-2 done with din
-            if (!pin_f) {
-                double* bin = op->bounce + s * slot;
-                if (j >= 2) PCB_CK(cudaEventSynchronize(ev_h2d[s]));  // H2D j-2 done with the bounce slot
-                par_memcpy(bin, src, n * sizeof(double));
-                src = bin;
-            }
             PCB_CK(cudaMemcpyAsync(din, src, n * sizeof(double), cudaMemcpyHostToDevice, op->s_h2d));
             PCB_CK(cudaEventRecord(ev_h2d[s], op->s_h2d));
             PCB_CK(cudaStreamWaitEvent(op->stream, ev_h2d[s], 0));
@@ -2424,13 +2473,27 @@ static pcb_status apply_host_common(pcb_op* op, bool adjoint, int32_t B, const d
             cudaEvent_t ready = full_apply(op, adjoint, sizes[j], din, dout);
             PCB_CK(cudaEventRecord(ev_k[s], op->stream));
             PCB_CK(cudaStreamWaitEvent(op->s_d2h, ready, 0));
-            double* dst = pin_g ? G + offs[j] : op->bounce + 2 * slot + s * slot;
-            if (!pin_g && j >= 2) PCB_CK(cudaStreamWaitEvent(op->s_d2h, ev_d2h[s], 0));  // (drained below)
+            double* dst = pin_g ? G + offs[j] : bout + s * slot;
             PCB_CK(cudaMemcpyAsync(dst, dout, n * sizeof(double), cudaMemcpyDeviceToHost, op->s_d2h));
             PCB_CK(cudaEventRecord(ev_d2h[s], op->s_d2h));
-            if (!pin_g && j >= 1) drain(j - 1);
+            // host side, while the GPU works on j: pageable F of j+1 into its bounce slot (free once
+            // H2D j-1 is done) and the bounce copy of j-1 out to pageable G (once D2H j-1 is done)
+            std::vector<HostCopy> copies;
+            if (!pin_f && j + 1 < sizes.size()) {
+                if (j >= 1) PCB_CK(cudaEventSynchronize(ev_h2d[(j + 1) & 1]));
+                copies.push_back({bin + ((j + 1) & 1) * slot, F + offs[j + 1], bytes_of(j + 1)});
+            }
+            if (!pin_g && j >= 1) {
+                PCB_CK(cudaEventSynchronize(ev_d2h[(j - 1) & 1]));
+                copies.push_back({G + offs[j - 1], bout + ((j - 1) & 1) * slot, bytes_of(j - 1)});
+            }
+            if (!copies.empty()) HostPool::get().copy(copies);
         }
-        if (!pin_g) drain(sizes.size() - 1);
+        if (!pin_g) {
+            const size_t last = sizes.size() - 1;
+            PCB_CK(cudaEventSynchronize(ev_d2h[last & 1]));
+            HostPool::get().copy({{G + offs[last], bout + (last & 1) * slot, bytes_of(last)}});
+        }
         PCB_CK(cudaStreamSynchronize(op->s_d2h));
         PCB_CK(cudaStreamSynchronize(op->stream));
         if (op->s_comm) PCB_CK(cudaStreamSynchronize(op->s_comm));
@@ -2485,15 +2548,9 @@ static void blocks_common(pcb_op* op, int32_t nblk, const int64_t* d_t, const in
         if (v < 1 || v > (1 << 20)) fail(PCB_EINVAL, "pcb_blocks: bad block shape");
         bs[a] = (int32_t)v;
     }
-    op->st_shape.ensure(3);
     op->st_flag.ensure(1);
-    op->st_blk.ensure((size_t)blocks_scratch_ints(nblk));
-    PCB_CK(cudaMemcpyAsync(op->st_shape.p, bs, sizeof(bs), cudaMemcpyHostToDevice, st));
     PCB_CK(cudaMemsetAsync(op->st_flag.p, 0, 4, st));
-    launch(op, st, "blocks", [&] {
-        return launch_blocks(entry_args(op), nblk, d_t, d_s, op->st_shape.p, bs, d_out, op->st_flag.p, op->st_blk.p,
-                             st);
-    });
+    launch(op, st, "blocks", [&] { return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, st); });
     if (host_check) {
         int32_t bad = 0;
         PCB_CK(cudaMemcpyAsync(&bad, op->st_flag.p, 4, cudaMemcpyDeviceToHost, st));
