@@ -234,22 +234,33 @@ __global__ void k_zero(double* p, int64_t n) {
 //     every entry sums over the staged terms in ascending k with the reference's IEEE mul/add --
 //     the same terms in the same order as entry_value, so the result is bit-identical.  Blocks that
 //     leave the domain or have too many candidates take the per-entry path.
-// Zero blocks cost one warp's stores; the few gathered blocks overlap the other CTAs' stores
-// instead of waiting behind them at a kernel boundary.
+// Zero blocks are written by the TMA engine: one lane issues cp.async.bulk copies of a zeroed 4 KiB
+// shared-memory tile to the block (no per-thread store traffic through the LSU).  Blocks with
+// candidates go to a device work queue that every CTA drains once its own classification is
+// done, so the few gathered blocks spread over the CTAs that finish first instead of
+// serializing in the CTA that classified them.
+constexpr int BZ_DOUBLES = 512;  // zero tile: 4 KiB
 constexpr int BT_CAP = 32;  // max staged candidate terms per block
 constexpr int BT_IDS = 64;  // gathered bucket entries (with duplicates) per block
 constexpr int BT_NZ = 8;    // listed nonzero-weight terms per source point
 constexpr int BC_WARPS = 8; // blocks (classifying warps) per CTA
 
+__device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(ssrc);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes) : "memory");
+}
+
+// scratch (int32): [0] queue reserve count, [1] queue taken count, [2, 2 + nblk) queue (blk + 1;
+// 0 = not yet published), then per block (cap + 1): candidate count (-1: per-entry path), ids
 __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk, const int64_t* __restrict__ t_origin,
                                                       const int64_t* __restrict__ s_origin, int bs0, int bs1, int bs2,
-                                                      int cap, double* __restrict__ out, int32_t* bad) {
+                                                      int cap, double* __restrict__ out, int32_t* bad,
+                                                      int32_t* __restrict__ scr) {
     extern __shared__ double sm[];
+    __shared__ int s_item;
     __shared__ int ids_s[BC_WARPS][BT_IDS];
     __shared__ int first_s[BC_WARPS][BT_IDS];
     __shared__ int cand_s[BC_WARPS][BT_CAP];
-    __shared__ int nc_s[BC_WARPS];  // candidates; 0: zero block (written), -1: per-entry path
-    __shared__ int64_t org_s[BC_WARPS][6];
     const int D = a.D;
     const int bs[3] = {bs0, bs1, bs2};
     int npx = 1, win = 1;
@@ -258,6 +269,13 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk,
         win *= 2 * bs[i] - 1;
     }
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    double* Z = sm;  // zero tile (the bulk stores' source)
+    for (int i = tid; i < BZ_DOUBLES; i += blockDim.x) Z[i] = 0.0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    int32_t* queue = scr + 2;
+    int32_t* cand_g = scr + 2 + nblk;
+    bool issued = false;  // this thread has bulk stores in flight (lane 0 of a zero-block warp)
     // ---- phase 1: classify (warp wid <-> block blk) ----
     {
         const int blk = blockIdx.x * BC_WARPS + wid;
@@ -338,36 +356,44 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk,
                     }
                 }
             }
-            if (!fb && nk == 0) {  // no term can contribute: an all-zero block
-                const int64_t n2 = (int64_t)npx * npx;
-                double* ob = out + (int64_t)blk * n2;
+            if (!fb && nk == 0) {  // no term can contribute: an all-zero block, written by the TMA engine
+                const int64_t bytes = (int64_t)npx * npx * 8;
+                char* ob = reinterpret_cast<char*>(out + (int64_t)blk * npx * npx);
                 if ((reinterpret_cast<uintptr_t>(ob) & 15) == 0) {
-                    double2* o2 = reinterpret_cast<double2*>(ob);
-                    for (int64_t e = lane; e < n2 / 2; e += 32) o2[e] = make_double2(0.0, 0.0);
-                    if ((n2 & 1) && lane == 0) ob[n2 - 1] = 0.0;
+                    if (lane == 0) {
+                        int64_t o = 0;
+                        for (; o + BZ_DOUBLES * 8 <= bytes; o += BZ_DOUBLES * 8) bulk_store_s2g(ob + o, Z, BZ_DOUBLES * 8);
+                        const int64_t tail = (bytes - o) & ~(int64_t)15;
+                        if (tail > 0) bulk_store_s2g(ob + o, Z, (uint32_t)tail);
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        if (bytes & 15) *reinterpret_cast<double*>(ob + bytes - 8) = 0.0;
+                        issued = true;
+                    }
                 } else {
-                    for (int64_t e = lane; e < n2; e += 32) ob[e] = 0.0;
+                    double* od = reinterpret_cast<double*>(ob);
+                    for (int64_t e = lane; e < (int64_t)npx * npx; e += 32) od[e] = 0.0;
                 }
-            }
-        }
-        if (lane == 0) {
-            nc_s[wid] = blk >= nblk ? 0 : fb ? -1 : nk;
-            for (int i = 0; i < 3; ++i) {
-                org_s[wid][i] = tv[i];
-                org_s[wid][3 + i] = sv[i];
+            } else if (lane == 0) {  // publish the block to the gather queue: candidates first
+                int32_t* cg = cand_g + (int64_t)blk * (cap + 1);
+                cg[0] = fb ? -1 : nk;
+                for (int c = 0; c < (fb ? 0 : nk); ++c) cg[1 + c] = cand_s[wid][c];
+                __threadfence();
+                const int slot = atomicAdd(scr, 1);
+                atomicExch(queue + slot, blk + 1);
             }
         }
     }
+    if (issued) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // Z is read; sm reusable
     __syncthreads();
-    // ---- phase 2: the CTA gathers its blocks that have candidates ----
-    double* W = sm;               // [cap][npx]
-    double* PH = sm + cap * npx;  // [cap][win]
+    // ---- phase 2: drain the gather queue ----
+    double* W = sm + BZ_DOUBLES;  // [cap][npx]
+    double* PH = W + cap * npx;   // [cap][win]
     int* offs = reinterpret_cast<int*>(PH + cap * win);              // [npx] window offset of a point
     unsigned char* nzn = reinterpret_cast<unsigned char*>(offs + npx);  // [npx] nonzero-term count
     unsigned char* nzc = nzn + npx;                                   // [npx][BT_NZ] their indices
-    int any = 0;
-    for (int w = 0; w < BC_WARPS; ++w) any |= nc_s[w] != 0;
-    if (!any) return;
+    __shared__ int s_nc;
+    __shared__ int s_cand[BT_CAP];
+    __shared__ int64_t s_t[3], s_s[3];
     int centre = 0;
     {
         int mul = 1;
@@ -385,15 +411,40 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk,
         }
         offs[p] = o;
     }
-    for (int w = 0; w < BC_WARPS; ++w) {
-        const int nc = nc_s[w];
-        if (nc == 0) continue;
-        const int blk = blockIdx.x * BC_WARPS + w;
-        const int64_t* s_t = org_s[w];
-        const int64_t* s_s = org_s[w] + 3;
-        const int* cand = cand_s[w];
-        double* ob = out + (int64_t)blk * npx * npx;
+    for (;;) {
+        if (tid == 0) {  // take the next published block, if any
+            int item = -1;
+            for (;;) {
+                const int tk = *reinterpret_cast<volatile int32_t*>(scr + 1);
+                const int rs = *reinterpret_cast<volatile int32_t*>(scr);
+                if (tk >= rs) break;
+                if (atomicCAS(scr + 1, tk, tk + 1) == tk) {
+                    item = tk;
+                    break;
+                }
+            }
+            if (item >= 0) {
+                int v;
+                while ((v = *reinterpret_cast<volatile int32_t*>(queue + item)) == 0) {
+                }
+                __threadfence();
+                item = v - 1;
+                const volatile int32_t* cg = cand_g + (int64_t)item * (cap + 1);
+                s_nc = cg[0];
+                for (int c = 0; c < s_nc; ++c) s_cand[c] = cg[1 + c];
+                for (int i = 0; i < 3; ++i) {
+                    s_t[i] = i < D ? t_origin[(int64_t)item * D + i] : 0;
+                    s_s[i] = i < D ? s_origin[(int64_t)item * D + i] : 0;
+                }
+            }
+            s_item = item;
+        }
         __syncthreads();
+        const int blk = s_item;
+        if (blk < 0) break;
+        const int nc = s_nc;
+        const int* cand = s_cand;
+        double* ob = out + (int64_t)blk * npx * npx;
         if (nc < 0) {  // per-entry path (out-of-domain entries flag `bad`)
             for (int e = tid; e < npx * npx; e += blockDim.x) {
                 int i = e / npx, j = e - (e / npx) * npx;
@@ -408,6 +459,7 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk,
                 ob[e] = entry_value(a, y, x, b);
                 if (b) atomicOr(bad, 1);
             }
+            __syncthreads();
             continue;
         }
         for (int idx = tid; idx < nc * npx; idx += blockDim.x) {  // w_k on S (0 outside X_k)
@@ -479,6 +531,7 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk,
             }
             ob[e] = sum;
         }
+        __syncthreads();
     }
 }
 
@@ -492,8 +545,10 @@ cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, co
     return cudaGetLastError();
 }
 
+int64_t blocks_scratch_ints(int32_t nblk) { return 2 + (int64_t)nblk + (int64_t)nblk * (BT_CAP + 1); }
+
 cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
-                          const int32_t* bshape_host, double* out, int32_t* bad, cudaStream_t st) {
+                          const int32_t* bshape_host, double* out, int32_t* bad, int32_t* scratch, cudaStream_t st) {
     if (nblk <= 0) return cudaSuccess;
     int64_t npx = 1, win = 1;
     for (int i = 0; i < a.D; ++i) {
@@ -504,16 +559,18 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
         const char* e = getenv("PCB_BLOCK_CAP");
         return e ? std::max(1, std::min(BT_CAP, atoi(e))) : 16;
     }();
-    const size_t smem = sizeof(double) * (size_t)cap * (size_t)(npx + win) + sizeof(int) * (size_t)npx +
-                        (size_t)npx * (1 + BT_NZ) + 16;
+    const size_t smem = sizeof(double) * ((size_t)BZ_DOUBLES + (size_t)cap * (size_t)(npx + win)) +
+                        sizeof(int) * (size_t)npx + (size_t)npx * (1 + BT_NZ) + 16;
     if (smem <= 160 * 1024) {
+        cudaError_t e0 = cudaMemsetAsync(scratch, 0, sizeof(int32_t) * (2 + (size_t)nblk), st);
+        if (e0 != cudaSuccess) return e0;
         if (smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(k_blocks_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
         }
         k_blocks_tiled<<<(unsigned)((nblk + BC_WARPS - 1) / BC_WARPS), 32 * BC_WARPS, smem, st>>>(
             a, nblk, t_origin, s_origin, bshape_host[0], a.D > 1 ? bshape_host[1] : 1, a.D > 2 ? bshape_host[2] : 1, cap,
-            out, bad);
+            out, bad, scratch);
         return cudaGetLastError();
     }
     k_blocks<<<148 * 16, 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape_host[0], a.D > 1 ? bshape_host[1] : 1,

@@ -324,7 +324,7 @@ struct pcb_op {
     // host-call staging
     pcb::DevBuf<double> st_in, st_out, st_aux;
     pcb::DevBuf<int64_t> st_i64a, st_i64b;
-    pcb::DevBuf<int32_t> st_flag;
+    pcb::DevBuf<int32_t> st_flag, st_blk;
     cudaStream_t stream = nullptr;
     pcb_info info{};
     // per-kernel event profiling (pcb_profile_begin / pcb_profile_end)
@@ -2549,8 +2549,10 @@ static void blocks_common(pcb_op* op, int32_t nblk, const int64_t* d_t, const in
         bs[a] = (int32_t)v;
     }
     op->st_flag.ensure(1);
+    op->st_blk.ensure((size_t)blocks_scratch_ints(nblk));
     PCB_CK(cudaMemsetAsync(op->st_flag.p, 0, 4, st));
-    launch(op, st, "blocks", [&] { return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, st); });
+    launch(op, st, "blocks",
+           [&] { return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, op->st_blk.p, st); });
     if (host_check) {
         int32_t bad = 0;
         PCB_CK(cudaMemcpyAsync(&bad, op->st_flag.p, 4, cudaMemcpyDeviceToHost, st));
