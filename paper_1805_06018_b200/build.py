@@ -31,7 +31,9 @@ E3_COLS = os.environ.get("PCB_E3_COLS", "24")  # 3-smooth engines of the cols pa
 E3_COLS_SMALL = os.environ.get("PCB_E3_COLS_SMALL", "96")  # cols: 3-smooth lengths <= this use 12 per thread
 E_COLS_SMALL = os.environ.get("PCB_E_COLS_SMALL", "64")  # cols: pow2 lengths <= this use 8 elements per thread
 RADIX_DESC_ROWS = os.environ.get("PCB_RADIX_DESC_ROWS", "1")  # rows: prefix radices largest first
-PER_SOURCE = {"kernels_rows.cu": [f"-DPCB_E2={E_ROWS}", f"-DPCB_RADIX_DESC={RADIX_DESC_ROWS}"],
+E3_ROWS_SMALL = os.environ.get("PCB_E3_ROWS_SMALL", "0")  # rows: 3-smooth lengths <= this use 12 per thread
+PER_SOURCE = {"kernels_rows.cu": [f"-DPCB_E2={E_ROWS}", f"-DPCB_RADIX_DESC={RADIX_DESC_ROWS}",
+                                  f"-DPCB_E3_SMALL_MAX={E3_ROWS_SMALL}"],
               "kernels_cols.cu": [f"-DPCB_E2={E_COLS}", f"-DPCB_E2_SMALL_MAX={E_COLS_SMALL}", f"-DPCB_E3={E3_COLS}",
                                   f"-DPCB_E3_SMALL_MAX={E3_COLS_SMALL}"],
               "kernels_mid.cu": [f"-DPCB_E2={E_MID}", f"-DPCB_E3={E3_MID}"]}

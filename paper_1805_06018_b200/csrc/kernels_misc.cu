@@ -252,12 +252,12 @@ __device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uin
 
 // scratch (int32): [0] queue reserve count, [1] queue taken count, [2, 2 + nblk) queue (blk + 1;
 // 0 = not yet published), then per block (cap + 1): candidate count (-1: per-entry path), ids
-__global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk, const int64_t* __restrict__ t_origin,
-                                                      const int64_t* __restrict__ s_origin, int bs0, int bs1, int bs2,
-                                                      int cap, double* __restrict__ out, int32_t* bad,
-                                                      int32_t* __restrict__ scr) {
-    extern __shared__ double sm[];
-    __shared__ int s_item;
+__global__ void __launch_bounds__(256) k_blocks_classify(EntryArgs a, int32_t nblk,
+                                                         const int64_t* __restrict__ t_origin,
+                                                         const int64_t* __restrict__ s_origin, int bs0, int bs1,
+                                                         int bs2, int cap, double* __restrict__ out,
+                                                         int32_t* __restrict__ scr) {
+    __shared__ __align__(128) double Z[BZ_DOUBLES];  // zero tile (the bulk stores' source)
     __shared__ int ids_s[BC_WARPS][BT_IDS];
     __shared__ int first_s[BC_WARPS][BT_IDS];
     __shared__ int cand_s[BC_WARPS][BT_CAP];
@@ -269,7 +269,6 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk,
         win *= 2 * bs[i] - 1;
     }
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    double* Z = sm;  // zero tile (the bulk stores' source)
     for (int i = tid; i < BZ_DOUBLES; i += blockDim.x) Z[i] = 0.0;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
@@ -373,25 +372,39 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk,
                     double* od = reinterpret_cast<double*>(ob);
                     for (int64_t e = lane; e < (int64_t)npx * npx; e += 32) od[e] = 0.0;
                 }
-            } else if (lane == 0) {  // publish the block to the gather queue: candidates first
+            } else if (lane == 0) {  // list the block for the gather kernel, with its candidates
                 int32_t* cg = cand_g + (int64_t)blk * (cap + 1);
                 cg[0] = fb ? -1 : nk;
                 for (int c = 0; c < (fb ? 0 : nk); ++c) cg[1 + c] = cand_s[wid][c];
-                __threadfence();
-                const int slot = atomicAdd(scr, 1);
-                atomicExch(queue + slot, blk + 1);
+                queue[atomicAdd(scr, 1)] = blk;
             }
         }
     }
-    if (issued) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // Z is read; sm reusable
-    __syncthreads();
-    // ---- phase 2: drain the gather queue ----
-    double* W = sm + BZ_DOUBLES;  // [cap][npx]
+    if (issued) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // Z read before the CTA exits
+}
+
+__global__ void __launch_bounds__(256) k_blocks_gather(EntryArgs a, const int64_t* __restrict__ t_origin,
+                                                       const int64_t* __restrict__ s_origin, int bs0, int bs1, int bs2,
+                                                       int cap, double* __restrict__ out, int32_t* bad,
+                                                       const int32_t* __restrict__ scr, int32_t nblk) {
+    extern __shared__ double sm[];
+    const int D = a.D;
+    const int bs[3] = {bs0, bs1, bs2};
+    int npx = 1, win = 1;
+    for (int i = 0; i < D; ++i) {
+        npx *= bs[i];
+        win *= 2 * bs[i] - 1;
+    }
+    const int tid = threadIdx.x;
+    const int32_t* queue = scr + 2;
+    const int32_t* cand_g = scr + 2 + nblk;
+    const int nwork = scr[0];
+    double* W = sm;               // [cap][npx]
     double* PH = W + cap * npx;   // [cap][win]
     int* offs = reinterpret_cast<int*>(PH + cap * win);              // [npx] window offset of a point
     unsigned char* nzn = reinterpret_cast<unsigned char*>(offs + npx);  // [npx] nonzero-term count
     unsigned char* nzc = nzn + npx;                                   // [npx][BT_NZ] their indices
-    __shared__ int s_nc;
+    __shared__ int s_nc, s_item;
     __shared__ int s_cand[BT_CAP];
     __shared__ int64_t s_t[3], s_s[3];
     int centre = 0;
@@ -411,37 +424,20 @@ __global__ void __launch_bounds__(256) k_blocks_tiled(EntryArgs a, int32_t nblk,
         }
         offs[p] = o;
     }
-    for (;;) {
-        if (tid == 0) {  // take the next published block, if any
-            int item = -1;
-            for (;;) {
-                const int tk = *reinterpret_cast<volatile int32_t*>(scr + 1);
-                const int rs = *reinterpret_cast<volatile int32_t*>(scr);
-                if (tk >= rs) break;
-                if (atomicCAS(scr + 1, tk, tk + 1) == tk) {
-                    item = tk;
-                    break;
-                }
-            }
-            if (item >= 0) {
-                int v;
-                while ((v = *reinterpret_cast<volatile int32_t*>(queue + item)) == 0) {
-                }
-                __threadfence();
-                item = v - 1;
-                const volatile int32_t* cg = cand_g + (int64_t)item * (cap + 1);
-                s_nc = cg[0];
-                for (int c = 0; c < s_nc; ++c) s_cand[c] = cg[1 + c];
-                for (int i = 0; i < 3; ++i) {
-                    s_t[i] = i < D ? t_origin[(int64_t)item * D + i] : 0;
-                    s_s[i] = i < D ? s_origin[(int64_t)item * D + i] : 0;
-                }
+    for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
+        if (tid == 0) {
+            const int item = queue[wi];
+            const int32_t* cg = cand_g + (int64_t)item * (cap + 1);
+            s_nc = cg[0];
+            for (int c = 0; c < s_nc; ++c) s_cand[c] = cg[1 + c];
+            for (int i = 0; i < 3; ++i) {
+                s_t[i] = i < D ? t_origin[(int64_t)item * D + i] : 0;
+                s_s[i] = i < D ? s_origin[(int64_t)item * D + i] : 0;
             }
             s_item = item;
         }
         __syncthreads();
         const int blk = s_item;
-        if (blk < 0) break;
         const int nc = s_nc;
         const int* cand = s_cand;
         double* ob = out + (int64_t)blk * npx * npx;
@@ -559,18 +555,24 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
         const char* e = getenv("PCB_BLOCK_CAP");
         return e ? std::max(1, std::min(BT_CAP, atoi(e))) : 16;
     }();
-    const size_t smem = sizeof(double) * ((size_t)BZ_DOUBLES + (size_t)cap * (size_t)(npx + win)) +
-                        sizeof(int) * (size_t)npx + (size_t)npx * (1 + BT_NZ) + 16;
-    if (smem <= 160 * 1024) {
-        cudaError_t e0 = cudaMemsetAsync(scratch, 0, sizeof(int32_t) * (2 + (size_t)nblk), st);
-        if (e0 != cudaSuccess) return e0;
+    const size_t smem = sizeof(double) * (size_t)cap * (size_t)(npx + win) + sizeof(int) * (size_t)npx +
+                        (size_t)npx * (1 + BT_NZ) + 16;
+    if (smem <= 160 * 1024) {  // classify (zero blocks written there), then gather the listed blocks
+        cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(int32_t), st);
+        if (e != cudaSuccess) return e;
         if (smem > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(k_blocks_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            e = cudaFuncSetAttribute(k_blocks_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
         }
-        k_blocks_tiled<<<(unsigned)((nblk + BC_WARPS - 1) / BC_WARPS), 32 * BC_WARPS, smem, st>>>(
-            a, nblk, t_origin, s_origin, bshape_host[0], a.D > 1 ? bshape_host[1] : 1, a.D > 2 ? bshape_host[2] : 1, cap,
-            out, bad, scratch);
+        const int bs1 = a.D > 1 ? bshape_host[1] : 1, bs2 = a.D > 2 ? bshape_host[2] : 1;
+        k_blocks_classify<<<(unsigned)((nblk + BC_WARPS - 1) / BC_WARPS), 32 * BC_WARPS, 0, st>>>(
+            a, nblk, t_origin, s_origin, bshape_host[0], bs1, bs2, cap, out, scratch);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        const int per_sm = std::max<int>(1, (int)((220 * 1024) / (smem + 2048)));
+        const int grid = (int)std::min<int64_t>(nblk, 148LL * std::min(per_sm, 4));
+        k_blocks_gather<<<grid, 256, smem, st>>>(a, t_origin, s_origin, bshape_host[0], bs1, bs2, cap, out, bad, scratch,
+                                                  nblk);
         return cudaGetLastError();
     }
     k_blocks<<<148 * 16, 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape_host[0], a.D > 1 ? bshape_host[1] : 1,
