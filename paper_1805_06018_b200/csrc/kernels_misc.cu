@@ -320,7 +320,22 @@ __global__ void __launch_bounds__(256) k_blocks_classify(EntryArgs a, int32_t nb
                 if (nbk > 32 || total > BT_IDS) {
                     fb = 1;
                 } else {
-                    for (int q = 0; q < cnt; ++q) ids[off + q] = a.bucket_terms[beg + q];
+                    // gathered list position pos -> (bucket b, entry pos - off_b): every lane loads
+                    // its two positions at once (one round trip instead of a serial loop per bucket)
+                    int64_t src[2] = {-1, -1};
+                    for (int b = 0; b < nbk; ++b) {
+                        const int ob = __shfl_sync(0xffffffffu, off, b);
+                        const int cb = __shfl_sync(0xffffffffu, cnt, b);
+                        const int64_t gb = __shfl_sync(0xffffffffu, beg, b);
+                        for (int h = 0; h < 2; ++h) {
+                            const int pos = lane + 32 * h;
+                            if (pos >= ob && pos < ob + cb) src[h] = gb + (pos - ob);
+                        }
+                    }
+                    int got[2];
+                    for (int h = 0; h < 2; ++h) got[h] = src[h] >= 0 ? a.bucket_terms[src[h]] : 0;
+                    for (int h = 0; h < 2; ++h)
+                        if (lane + 32 * h < total) ids[lane + 32 * h] = got[h];
                     __syncwarp();
                     int keep[2] = {0, 0}, idv[2] = {0, 0};
                     for (int h = 0; h < 2; ++h) {
@@ -407,6 +422,9 @@ __global__ void __launch_bounds__(256) k_blocks_gather(EntryArgs a, const int64_
     __shared__ int s_nc, s_item;
     __shared__ int s_cand[BT_CAP];
     __shared__ int64_t s_t[3], s_s[3];
+    // the candidates' geometry (one parallel load per candidate instead of per staged element)
+    __shared__ int64_t c_xlo[BT_CAP][3], c_klo[BT_CAP][3], c_woff[BT_CAP], c_poff[BT_CAP];
+    __shared__ int32_t c_m[BT_CAP][3], c_kext[BT_CAP][3];
     int centre = 0;
     {
         int mul = 1;
@@ -458,42 +476,54 @@ __global__ void __launch_bounds__(256) k_blocks_gather(EntryArgs a, const int64_
             __syncthreads();
             continue;
         }
+        if (tid < nc) {
+            const TermDesc& t = a.terms[cand[tid]];
+            for (int d = 0; d < 3; ++d) {
+                c_xlo[tid][d] = t.x_lo[d];
+                c_klo[tid][d] = t.k_lo[d];
+                c_m[tid][d] = t.m[d];
+                c_kext[tid][d] = t.k_ext[d];
+            }
+            c_woff[tid] = t.w_off;
+            c_poff[tid] = t.phi_off;
+        }
+        __syncthreads();
+#pragma unroll 4
         for (int idx = tid; idx < nc * npx; idx += blockDim.x) {  // w_k on S (0 outside X_k)
             const int c = idx / npx;
             int j = idx - c * npx;
-            const TermDesc& t = a.terms[cand[c]];
             int64_t u[3];
             bool in = true;
             for (int d = D - 1; d >= 0; --d) {
-                u[d] = s_s[d] + j % bs[d] - t.x_lo[d];
+                u[d] = s_s[d] + j % bs[d] - c_xlo[c][d];
                 j /= bs[d];
-                in = in && u[d] >= 0 && u[d] < t.m[d];
+                in = in && u[d] >= 0 && u[d] < c_m[c][d];
             }
             double wv = 0.0;
             if (in) {
                 int64_t wl = 0;
-                for (int d = 0; d < D; ++d) wl = wl * t.m[d] + u[d];
-                wv = a.w_pool[t.w_off + wl];
+                for (int d = 0; d < D; ++d) wl = wl * c_m[c][d] + u[d];
+                wv = a.w_pool[c_woff[c] + wl];
             }
             W[c * npx + (idx - c * npx)] = wv;
         }
+#pragma unroll 4
         for (int idx = tid; idx < nc * win; idx += blockDim.x) {  // phi_k^E on the offsets T - S
             const int c = idx / win;
             int w2 = idx - c * win;
-            const TermDesc& t = a.terms[cand[c]];
             int64_t z[3];
             bool in = true;
             for (int d = D - 1; d >= 0; --d) {
                 const int wd = 2 * bs[d] - 1;
-                z[d] = s_t[d] - s_s[d] + (w2 % wd) - (bs[d] - 1) - t.k_lo[d];
+                z[d] = s_t[d] - s_s[d] + (w2 % wd) - (bs[d] - 1) - c_klo[c][d];
                 w2 /= wd;
-                in = in && z[d] >= 0 && z[d] < t.k_ext[d];
+                in = in && z[d] >= 0 && z[d] < c_kext[c][d];
             }
             double ph = 0.0;
             if (in) {
                 int64_t zl = 0;
-                for (int d = 0; d < D; ++d) zl = zl * t.k_ext[d] + z[d];
-                ph = a.phi_pool[t.phi_off + zl];
+                for (int d = 0; d < D; ++d) zl = zl * c_kext[c][d] + z[d];
+                ph = a.phi_pool[c_poff[c] + zl];
             }
             PH[c * win + (idx - c * win)] = ph;
         }
