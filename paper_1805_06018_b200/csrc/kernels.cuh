@@ -146,9 +146,11 @@ struct EntryArgs {
 cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, const int64_t* x, double* out,
                            int32_t* bad, cudaStream_t st);
 // bshape_host: the block shape per axis (host array, passed by value); scratch: device int32 of
-// blocks_scratch_ints(nblk) (the gather queue and the candidate lists)
+// blocks_scratch_ints(nblk) (the work list and the candidate lists).  phase 0: classify (writes
+// the all-zero blocks, lists the others); phase 1: gather the listed blocks.
 cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
-                          const int32_t* bshape_host, double* out, int32_t* bad, int32_t* scratch, cudaStream_t st);
+                          const int32_t* bshape_host, double* out, int32_t* bad, int32_t* scratch, int phase,
+                          cudaStream_t st);
 int64_t blocks_scratch_ints(int32_t nblk);
 
 // block apply, direct form (small blocks)

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(256) k_blocks_classify(EntryArgs a, int32_t nb
                                                          const int64_t* __restrict__ t_origin,
                                                          const int64_t* __restrict__ s_origin, int bs0, int bs1,
                                                          int bs2, int cap, double* __restrict__ out,
-                                                         int32_t* __restrict__ scr) {
+                                                         int32_t* __restrict__ scr, int zero_mode) {
     __shared__ __align__(128) double Z[BZ_DOUBLES];  // zero tile (the bulk stores' source)
     __shared__ int ids_s[BC_WARPS][BT_IDS];
     __shared__ int first_s[BC_WARPS][BT_IDS];
@@ -370,10 +370,11 @@ __global__ void __launch_bounds__(256) k_blocks_classify(EntryArgs a, int32_t nb
                     }
                 }
             }
-            if (!fb && nk == 0) {  // no term can contribute: an all-zero block, written by the TMA engine
+            if (!fb && nk == 0) {  // no term can contribute: an all-zero block
                 const int64_t bytes = (int64_t)npx * npx * 8;
                 char* ob = reinterpret_cast<char*>(out + (int64_t)blk * npx * npx);
-                if ((reinterpret_cast<uintptr_t>(ob) & 15) == 0) {
+                const bool al16 = (reinterpret_cast<uintptr_t>(ob) & 15) == 0;
+                if (zero_mode == 0 && al16) {  // written by the TMA engine from the zero tile
                     if (lane == 0) {
                         int64_t o = 0;
                         for (; o + BZ_DOUBLES * 8 <= bytes; o += BZ_DOUBLES * 8) bulk_store_s2g(ob + o, Z, BZ_DOUBLES * 8);
@@ -383,10 +384,14 @@ __global__ void __launch_bounds__(256) k_blocks_classify(EntryArgs a, int32_t nb
                         if (bytes & 15) *reinterpret_cast<double*>(ob + bytes - 8) = 0.0;
                         issued = true;
                     }
-                } else {
+                } else if (zero_mode == 1 && al16) {  // 16-byte stores by the warp
+                    double2* o2 = reinterpret_cast<double2*>(ob);
+                    for (int64_t e = lane; e < bytes / 16; e += 32) o2[e] = make_double2(0.0, 0.0);
+                    if ((bytes & 15) && lane == 0) *reinterpret_cast<double*>(ob + bytes - 8) = 0.0;
+                } else if (zero_mode != 2) {
                     double* od = reinterpret_cast<double*>(ob);
                     for (int64_t e = lane; e < (int64_t)npx * npx; e += 32) od[e] = 0.0;
-                }
+                }  // zero_mode 2: the output was memset before the launch
             } else if (lane == 0) {  // list the block for the gather kernel, with its candidates
                 int32_t* cg = cand_g + (int64_t)blk * (cap + 1);
                 cg[0] = fb ? -1 : nk;
@@ -574,7 +579,8 @@ cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, co
 int64_t blocks_scratch_ints(int32_t nblk) { return 2 + (int64_t)nblk + (int64_t)nblk * (BT_CAP + 1); }
 
 cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
-                          const int32_t* bshape_host, double* out, int32_t* bad, int32_t* scratch, cudaStream_t st) {
+                          const int32_t* bshape_host, double* out, int32_t* bad, int32_t* scratch, int phase,
+                          cudaStream_t st) {
     if (nblk <= 0) return cudaSuccess;
     int64_t npx = 1, win = 1;
     for (int i = 0; i < a.D; ++i) {
@@ -585,28 +591,37 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
         const char* e = getenv("PCB_BLOCK_CAP");
         return e ? std::max(1, std::min(BT_CAP, atoi(e))) : 16;
     }();
+    // zero blocks: 0 = TMA bulk copies of a zero tile, 1 = 16-byte stores, 2 = one memset of the
+    // whole output before the classify pass (PCB_C5_ZERO)
+    static const int zero_mode = [] {
+        const char* e = getenv("PCB_C5_ZERO");
+        return e ? std::max(0, std::min(2, atoi(e))) : 2;
+    }();
     const size_t smem = sizeof(double) * (size_t)cap * (size_t)(npx + win) + sizeof(int) * (size_t)npx +
                         (size_t)npx * (1 + BT_NZ) + 16;
-    if (smem <= 160 * 1024) {  // classify (zero blocks written there), then gather the listed blocks
-        cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(int32_t), st);
-        if (e != cudaSuccess) return e;
-        if (smem > 48 * 1024) {
-            e = cudaFuncSetAttribute(k_blocks_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-        }
-        const int bs1 = a.D > 1 ? bshape_host[1] : 1, bs2 = a.D > 2 ? bshape_host[2] : 1;
-        k_blocks_classify<<<(unsigned)((nblk + BC_WARPS - 1) / BC_WARPS), 32 * BC_WARPS, 0, st>>>(
-            a, nblk, t_origin, s_origin, bshape_host[0], bs1, bs2, cap, out, scratch);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-        const int per_sm = std::max<int>(1, (int)((220 * 1024) / (smem + 2048)));
-        const int grid = (int)std::min<int64_t>(nblk, 148LL * std::min(per_sm, 4));
-        k_blocks_gather<<<grid, 256, smem, st>>>(a, t_origin, s_origin, bshape_host[0], bs1, bs2, cap, out, bad, scratch,
-                                                  nblk);
+    const int bs1 = a.D > 1 ? bshape_host[1] : 1, bs2 = a.D > 2 ? bshape_host[2] : 1;
+    if (smem > 160 * 1024) {  // too large to stage: the per-entry kernel does everything in phase 0
+        if (phase != 0) return cudaSuccess;
+        k_blocks<<<148 * 16, 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape_host[0], bs1, bs2, out, bad);
         return cudaGetLastError();
     }
-    k_blocks<<<148 * 16, 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape_host[0], a.D > 1 ? bshape_host[1] : 1,
-                                       a.D > 2 ? bshape_host[2] : 1, out, bad);
+    if (phase == 0) {  // classify (zero blocks written here), listing the others for phase 1
+        cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(int32_t), st);
+        if (e == cudaSuccess && zero_mode == 2)
+            e = cudaMemsetAsync(out, 0, sizeof(double) * (size_t)nblk * (size_t)(npx * npx), st);
+        if (e != cudaSuccess) return e;
+        k_blocks_classify<<<(unsigned)((nblk + BC_WARPS - 1) / BC_WARPS), 32 * BC_WARPS, 0, st>>>(
+            a, nblk, t_origin, s_origin, bshape_host[0], bs1, bs2, cap, out, scratch, zero_mode);
+        return cudaGetLastError();
+    }
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_blocks_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const int per_sm = std::max<int>(1, (int)((220 * 1024) / (smem + 2048)));
+    const int grid = (int)std::min<int64_t>(nblk, 148LL * std::min(per_sm, 4));
+    k_blocks_gather<<<grid, 256, smem, st>>>(a, t_origin, s_origin, bshape_host[0], bs1, bs2, cap, out, bad, scratch,
+                                              nblk);
     return cudaGetLastError();
 }
 

@@ -2551,8 +2551,10 @@ static void blocks_common(pcb_op* op, int32_t nblk, const int64_t* d_t, const in
     op->st_flag.ensure(1);
     op->st_blk.ensure((size_t)blocks_scratch_ints(nblk));
     PCB_CK(cudaMemsetAsync(op->st_flag.p, 0, 4, st));
-    launch(op, st, "blocks",
-           [&] { return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, op->st_blk.p, st); });
+    launch(op, st, "blocks(classify)",
+           [&] { return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, op->st_blk.p, 0, st); });
+    launch(op, st, "blocks(gather)",
+           [&] { return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, op->st_blk.p, 1, st); });
     if (host_check) {
         int32_t bad = 0;
         PCB_CK(cudaMemcpyAsync(&bad, op->st_flag.p, 4, cudaMemcpyDeviceToHost, st));

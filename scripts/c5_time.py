@@ -39,10 +39,12 @@ for _ in range(reps):
 torch.cuda.synchronize()
 prof = op.profile_end()
 kernel_ms = sum(v[0] for v in prof.values()) / reps
+split_ms = {k: v[0] / reps for k, v in prof.items()}
 hbm = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6552.0
 gbs = out.numel() * 8 / (ms * 1e-3) / 1e9
 kgbs = out.numel() * 8 / (kernel_ms * 1e-3) / 1e9
-res = {"blocks": nblk, "ms_per_call": ms, "kernel_ms": kernel_ms, "kernel_GBs": kgbs, "kernel_frac_hbm": kgbs / hbm,
+res = {"blocks": nblk, "ms_per_call": ms, "kernel_ms": kernel_ms, "split_ms": split_ms,
+       "zero_mode": os.environ.get("PCB_C5_ZERO", "default"), "kernel_GBs": kgbs, "kernel_frac_hbm": kgbs / hbm,
        "ms_per_launch": ms, "blocks_per_s": nblk / (ms * 1e-3),
        "entries_per_s": out.numel() / (ms * 1e-3), "output_GBs": gbs, "frac_hbm": gbs / hbm,
        "bound": "hbm (output written once; the gathers read ~KB per block, L2-resident)"}
