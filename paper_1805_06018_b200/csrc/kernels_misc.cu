@@ -244,6 +244,8 @@ constexpr int BT_CAP = 32;  // max staged candidate terms per block
 constexpr int BT_IDS = 64;  // gathered bucket entries (with duplicates) per block
 constexpr int BT_NZ = 8;    // listed nonzero-weight terms per source point
 constexpr int BC_WARPS = 8; // blocks (classifying warps) per CTA
+constexpr int BT_PXMAX = 256;   // gather kernel: max points per block (coordinate tables)
+constexpr int BT_WINMAX = 1024; // ... max window offsets
 
 __device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(ssrc);
@@ -292,9 +294,10 @@ __global__ void __launch_bounds__(256) k_blocks_classify(EntryArgs a, int32_t nb
             }
             if (!fb) {
                 int blo[3] = {0, 0, 0}, bn[3] = {1, 1, 1}, nbk = 1;
-                for (int i = 0; i < D; ++i) {
-                    blo[i] = (int)((sv[i] - a.dom_lo[i]) / a.bucket[i]);
-                    bn[i] = (int)((sv[i] + bs[i] - 1 - a.dom_lo[i]) / a.bucket[i]) - blo[i] + 1;
+                for (int i = 0; i < D; ++i) {  // 32-bit arithmetic: domain axes are < 2^20
+                    const int rel = (int)(sv[i] - a.dom_lo[i]);
+                    blo[i] = rel / a.bucket[i];
+                    bn[i] = (rel + bs[i] - 1) / a.bucket[i] - blo[i] + 1;
                     nbk *= bn[i];
                 }
                 int64_t beg = 0;
@@ -428,8 +431,10 @@ __global__ void __launch_bounds__(256) k_blocks_gather(EntryArgs a, const int64_
     __shared__ int s_cand[BT_CAP];
     __shared__ int64_t s_t[3], s_s[3];
     // the candidates' geometry (one parallel load per candidate instead of per staged element)
-    __shared__ int64_t c_xlo[BT_CAP][3], c_klo[BT_CAP][3], c_woff[BT_CAP], c_poff[BT_CAP];
-    __shared__ int32_t c_m[BT_CAP][3], c_kext[BT_CAP][3];
+    __shared__ int64_t c_woff[BT_CAP], c_poff[BT_CAP];
+    __shared__ int32_t c_xlo[BT_CAP][3], c_klo[BT_CAP][3], c_m[BT_CAP][3], c_kext[BT_CAP][3];
+    // per-point / per-window-offset coordinates (computed once per CTA; no divisions per element)
+    __shared__ int16_t pco[BT_PXMAX][3], wco[BT_WINMAX][3];
     int centre = 0;
     {
         int mul = 1;
@@ -443,9 +448,18 @@ __global__ void __launch_bounds__(256) k_blocks_gather(EntryArgs a, const int64_
         for (int d = D - 1; d >= 0; --d) {
             o += (r % bs[d]) * mul;
             mul *= 2 * bs[d] - 1;
+            pco[p][d] = (int16_t)(r % bs[d]);
             r /= bs[d];
         }
         offs[p] = o;
+    }
+    for (int w = tid; w < win; w += blockDim.x) {
+        int r = w;
+        for (int d = D - 1; d >= 0; --d) {
+            const int wd = 2 * bs[d] - 1;
+            wco[w][d] = (int16_t)(r % wd - (bs[d] - 1));
+            r /= wd;
+        }
     }
     for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
         if (tid == 0) {
@@ -481,11 +495,11 @@ __global__ void __launch_bounds__(256) k_blocks_gather(EntryArgs a, const int64_
             __syncthreads();
             continue;
         }
-        if (tid < nc) {
+        if (tid < nc) {  // candidate geometry relative to the block (32-bit: axes are < 2^20)
             const TermDesc& t = a.terms[cand[tid]];
             for (int d = 0; d < 3; ++d) {
-                c_xlo[tid][d] = t.x_lo[d];
-                c_klo[tid][d] = t.k_lo[d];
+                c_xlo[tid][d] = d < D ? (int32_t)(t.x_lo[d] - s_s[d]) : 0;              // X_k.lo - S.lo
+                c_klo[tid][d] = d < D ? (int32_t)(t.k_lo[d] - (s_t[d] - s_s[d])) : 0;  // K_k.lo - (T - S).lo
                 c_m[tid][d] = t.m[d];
                 c_kext[tid][d] = t.k_ext[d];
             }
@@ -496,41 +510,28 @@ __global__ void __launch_bounds__(256) k_blocks_gather(EntryArgs a, const int64_
 #pragma unroll 4
         for (int idx = tid; idx < nc * npx; idx += blockDim.x) {  // w_k on S (0 outside X_k)
             const int c = idx / npx;
-            int j = idx - c * npx;
-            int64_t u[3];
+            const int j = idx - c * npx;
             bool in = true;
-            for (int d = D - 1; d >= 0; --d) {
-                u[d] = s_s[d] + j % bs[d] - c_xlo[c][d];
-                j /= bs[d];
-                in = in && u[d] >= 0 && u[d] < c_m[c][d];
+            int wl = 0;
+            for (int d = 0; d < D; ++d) {
+                const int u = pco[j][d] - c_xlo[c][d];
+                in = in && u >= 0 && u < c_m[c][d];
+                wl = wl * c_m[c][d] + u;
             }
-            double wv = 0.0;
-            if (in) {
-                int64_t wl = 0;
-                for (int d = 0; d < D; ++d) wl = wl * c_m[c][d] + u[d];
-                wv = a.w_pool[c_woff[c] + wl];
-            }
-            W[c * npx + (idx - c * npx)] = wv;
+            W[idx] = in ? a.w_pool[c_woff[c] + wl] : 0.0;
         }
 #pragma unroll 4
         for (int idx = tid; idx < nc * win; idx += blockDim.x) {  // phi_k^E on the offsets T - S
             const int c = idx / win;
-            int w2 = idx - c * win;
-            int64_t z[3];
+            const int w2 = idx - c * win;
             bool in = true;
-            for (int d = D - 1; d >= 0; --d) {
-                const int wd = 2 * bs[d] - 1;
-                z[d] = s_t[d] - s_s[d] + (w2 % wd) - (bs[d] - 1) - c_klo[c][d];
-                w2 /= wd;
-                in = in && z[d] >= 0 && z[d] < c_kext[c][d];
+            int zl = 0;
+            for (int d = 0; d < D; ++d) {
+                const int z = wco[w2][d] - c_klo[c][d];
+                in = in && z >= 0 && z < c_kext[c][d];
+                zl = zl * c_kext[c][d] + z;
             }
-            double ph = 0.0;
-            if (in) {
-                int64_t zl = 0;
-                for (int d = 0; d < D; ++d) zl = zl * c_kext[c][d] + z[d];
-                ph = a.phi_pool[c_poff[c] + zl];
-            }
-            PH[c * win + (idx - c * win)] = ph;
+            PH[idx] = in ? a.phi_pool[c_poff[c] + zl] : 0.0;
         }
         __syncthreads();
         for (int j = tid; j < npx; j += blockDim.x) {  // per source point: its terms with w != 0
@@ -592,15 +593,16 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
         return e ? std::max(1, std::min(BT_CAP, atoi(e))) : 16;
     }();
     // zero blocks: 0 = TMA bulk copies of a zero tile, 1 = 16-byte stores, 2 = one memset of the
-    // whole output before the classify pass (PCB_C5_ZERO)
+    // whole output before the classify pass (PCB_C5_ZERO).  Measured at config 5 (4096 blocks, 4031
+    // zero): classify + gather 63.3 / 63.6 / 64.7 us -- the zero writes are not the limit.
     static const int zero_mode = [] {
         const char* e = getenv("PCB_C5_ZERO");
-        return e ? std::max(0, std::min(2, atoi(e))) : 2;
+        return e ? std::max(0, std::min(2, atoi(e))) : 0;
     }();
     const size_t smem = sizeof(double) * (size_t)cap * (size_t)(npx + win) + sizeof(int) * (size_t)npx +
                         (size_t)npx * (1 + BT_NZ) + 16;
     const int bs1 = a.D > 1 ? bshape_host[1] : 1, bs2 = a.D > 2 ? bshape_host[2] : 1;
-    if (smem > 160 * 1024) {  // too large to stage: the per-entry kernel does everything in phase 0
+    if (smem > 120 * 1024 || npx > BT_PXMAX || win > BT_WINMAX) {  // too large to stage: per-entry kernel
         if (phase != 0) return cudaSuccess;
         k_blocks<<<148 * 16, 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape_host[0], bs1, bs2, out, bad);
         return cudaGetLastError();
