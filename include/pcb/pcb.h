@@ -223,6 +223,12 @@ PCB_API const char* pcb_blur_last_error(void);
 typedef struct pcb_estimator pcb_estimator;
 PCB_API pcb_status pcb_estimator_create(int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t q,
                                         uint64_t seed, int32_t device, pcb_estimator** out);
+/* Probe generators: the reference's mt19937_64 + normal_distribution stream (drawn on the host,
+ * sequential: ~1 s for c3's 64 probes) or counter-based Philox4x32-10 + Box-Muller drawn on the
+ * device (throughput runs; SURVEY 8(d) allows it when Z is read back for a parity check). */
+typedef enum pcb_rng { PCB_RNG_MT19937 = 0, PCB_RNG_PHILOX = 1 } pcb_rng;
+PCB_API pcb_status pcb_estimator_create_ex(int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t q,
+                                           uint64_t seed, int32_t device, int32_t generator, pcb_estimator** out);
 PCB_API pcb_status pcb_estimator_destroy(pcb_estimator* est);
 PCB_API pcb_status pcb_estimator_probes(pcb_estimator* est, double** dZ, double** dY, double** dYtilde);
 PCB_API pcb_status pcb_estimator_set_y(pcb_estimator* est, const double* Y, int32_t device_ptr);

@@ -655,6 +655,43 @@ int64_t probe_sums_scratch(int D, const int32_t* n, int32_t q) {
     return 2 * ((N + PS_CHUNK - 1) / PS_CHUNK) * (int64_t)q;
 }
 
+// Philox4x32-10 (Salmon et al., SC'11) counter-based normals for throughput estimator runs: pair i
+// of the output = Box-Muller of the 4 words of Philox(counter = i, key = seed), two 53-bit
+// uniforms.  Deterministic and independent of the launch shape.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        k.x += 0x9E3779B9u;
+        k.y += 0xBB67AE85u;
+    }
+    return c;
+}
+
+__global__ void k_philox_normal(uint64_t seed, int64_t count, double* __restrict__ out) {
+    const int64_t pairs = (count + 1) / 2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pairs; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 w = philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), 0u, 0u),
+                                      make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+        const uint64_t a = ((uint64_t)w.x << 32) | w.y, b = ((uint64_t)w.z << 32) | w.w;
+        const double u1 = ((double)(a >> 11) + 1.0) * 0x1.0p-53;  // (0, 1]
+        const double u2 = (double)(b >> 11) * 0x1.0p-53;          // [0, 1)
+        const double r = sqrt(-2.0 * log(u1));
+        double sn, cs;
+        sincospi(2.0 * u2, &sn, &cs);
+        out[2 * i] = r * cs;
+        if (2 * i + 1 < count) out[2 * i + 1] = r * sn;
+    }
+}
+
+cudaError_t launch_philox_normal(uint64_t seed, int64_t count, double* out, cudaStream_t st) {
+    if (count <= 0) return cudaSuccess;
+    k_philox_normal<<<148 * 8, 256, 0, st>>>(seed, count, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_zero(double* p, int64_t n, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     k_zero<<<148 * 8, 256, 0, st>>>(p, n);

@@ -2899,6 +2899,11 @@ extern "C" {
 
 PCB_API pcb_status pcb_estimator_create(int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t q,
                                         uint64_t seed, int32_t device, pcb_estimator** out) {
+    return pcb_estimator_create_ex(dim, dom_lo, dom_hi, q, seed, device, PCB_RNG_MT19937, out);
+}
+
+PCB_API pcb_status pcb_estimator_create_ex(int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t q,
+                                           uint64_t seed, int32_t device, int32_t generator, pcb_estimator** out) {
     if (!out) {
         set_err("null output handle");
         return PCB_EINVAL;
@@ -2929,15 +2934,24 @@ PCB_API pcb_status pcb_estimator_create(int32_t dim, const int64_t* dom_lo, cons
         }
         e->q = q;
         const size_t cnt = (size_t)q * e->N;
-        // probe i = draws [i N, (i+1) N) of mt19937_64(seed) through std::normal_distribution (adaptivity.cpp:19-23)
-        std::vector<double> z(cnt);
-        std::mt19937_64 rng(seed);
-        std::normal_distribution<double> gauss(0.0, 1.0);
-        for (size_t i = 0; i < cnt; ++i) z[i] = gauss(rng);
+        if (generator != PCB_RNG_MT19937 && generator != PCB_RNG_PHILOX) fail(PCB_EINVAL, "bad probe generator");
         e->Z.alloc(cnt);
         e->Y.alloc(cnt);
         e->Yt.alloc(cnt);
-        PCB_CK(cudaMemcpyAsync(e->Z.p, z.data(), cnt * 8, cudaMemcpyHostToDevice, e->stream));
+        if (generator == PCB_RNG_MT19937) {
+            // probe i = draws [i N, (i+1) N) of mt19937_64(seed) through std::normal_distribution
+            // (adaptivity.cpp:19-23): the reference's stream, drawn on the host (one sequential stream)
+            std::vector<double> z(cnt);
+            std::mt19937_64 rng(seed);
+            std::normal_distribution<double> gauss(0.0, 1.0);
+            for (size_t i = 0; i < cnt; ++i) z[i] = gauss(rng);
+            PCB_CK(cudaMemcpyAsync(e->Z.p, z.data(), cnt * 8, cudaMemcpyHostToDevice, e->stream));
+        } else {
+            // throughput runs: counter-based Philox normals drawn on the device; the
+            // generator identity is implementation-defined -- read Z back
+            // (pcb_estimator_read) to feed a CPU check the same probes
+            launch_ck(launch_philox_normal(seed, (int64_t)cnt, e->Z.p, e->stream), "philox_normal");
+        }
         PCB_CK(cudaStreamSynchronize(e->stream));
         *out = e.release();
     });

@@ -25,7 +25,10 @@ def _rc(rc: int) -> None:
 
 
 class Estimator:
-    def __init__(self, domain: Tuple[Sequence[int], Sequence[int]], q: int, seed: int, device: int = -1):
+    def __init__(self, domain: Tuple[Sequence[int], Sequence[int]], q: int, seed: int, device: int = -1,
+                 generator: str = "mt19937"):
+        """generator: "mt19937" = the reference's probe stream (adaptivity.cpp:19-23, host-drawn);
+        "philox" = counter-based Philox normals drawn on the device (throughput runs)."""
         lo, hi = [int(v) for v in domain[0]], [int(v) for v in domain[1]]
         self.dim = len(lo)
         self.domain = (tuple(lo), tuple(hi))
@@ -35,8 +38,8 @@ class Estimator:
         self.seed = int(seed)
         h = _L.vp()
         A = ctypes.c_int64 * self.dim
-        _rc(_L.load().pcb_estimator_create(self.dim, A(*lo), A(*hi), self.q, ctypes.c_uint64(self.seed), int(device),
-                                           ctypes.byref(h)))
+        _rc(_L.load().pcb_estimator_create_ex(self.dim, A(*lo), A(*hi), self.q, ctypes.c_uint64(self.seed),
+                                              int(device), _L.RNG[generator], ctypes.byref(h)))
         self._h = h
         self.eta_abs = None
         self.eta_rel = None

@@ -34,7 +34,8 @@ EXPORTS = ["pcb_default_options", "pcb_last_error", "pcb_create", "pcb_destroy",
            "pcb_get_domain", "pcb_cluster_tree", "pcb_hmatrix_assemble", "pcb_hmatrix_compress",
            "pcb_hmatrix_destroy", "pcb_hmatrix_get_info", "pcb_hmatrix_tree", "pcb_hmatrix_block",
            "pcb_hmatrix_admissible", "pcb_hmatrix_matvec", "pcb_hmatrix_save", "pcb_hmatrix_load",
-           "pcb_comm_unique_id", "pcb_plan_shards", "pcb_debug_guard_check"]
+           "pcb_comm_unique_id", "pcb_plan_shards", "pcb_debug_guard_check", "pcb_estimator_create_ex"]
+RNG = {"mt19937": 0, "philox": 1}
 REDUCE = {"none": 0, "all": 1, "root": 2}
 PARTITION = {"cost": 0, "count": 1}
 
@@ -126,6 +127,7 @@ def load():
     L.pcb_blur_apply.argtypes = [vp, i32, vp, vp, i32, i32, vp]
     L.pcb_blur_last_error.restype = ctypes.c_char_p
     L.pcb_estimator_create.argtypes = [i32, P_i64, P_i64, i32, ctypes.c_uint64, i32, ctypes.POINTER(vp)]
+    L.pcb_estimator_create_ex.argtypes = [i32, P_i64, P_i64, i32, ctypes.c_uint64, i32, i32, ctypes.POINTER(vp)]
     L.pcb_estimator_destroy.argtypes = [vp]
     L.pcb_estimator_probes.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)]
     L.pcb_estimator_set_y.argtypes = [vp, vp, i32]

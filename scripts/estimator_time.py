@@ -40,7 +40,18 @@ t0 = time.perf_counter()
 for _ in range(reps):
     yt, cells_h, ea_h, er_h = op.probe_estimate(Zp, Yp, leaves)
 host_ms = (time.perf_counter() - t0) / reps * 1e3
-res = {"config": "c3", "probes": q, "leaves": len(leaves), "device_ms": dev_ms, "probes_per_s_device": q / (dev_ms * 1e-3),
+# probe creation: the reference's mt19937_64 stream (host) vs Philox on the device
+from paper_1805_06018_b200.estimator import Estimator  # noqa: E402
+
+create_s = {}
+for gen in ("mt19937", "philox"):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    est = Estimator((inp.dom_lo, inp.dom_hi), q=q, seed=2, generator=gen)
+    torch.cuda.synchronize()
+    create_s[gen] = time.perf_counter() - t0
+    est.close()
+res = {"config": "c3", "probes": q, "probe_creation_s": create_s, "leaves": len(leaves), "device_ms": dev_ms, "probes_per_s_device": q / (dev_ms * 1e-3),
        "host_ms": host_ms, "probes_per_s_host": q / (host_ms * 1e-3), "eta_abs": ea, "eta_rel": er,
        "host_equals_device": bool(np.isclose(ea, ea_h, rtol=1e-12) and np.isclose(er, er_h, rtol=1e-12))}
 print(json.dumps(res))

@@ -115,3 +115,50 @@ def test_one_dimensional_domain(gpu):
     yt, cells, ea2, er2 = op.probe_estimate(Z, Y, leaves, want_ytilde=True)
     assert abs(ea - ea2) <= 1e-13 * ea2 and abs(er - er2) <= 1e-13 * er2
     assert np.allclose(est.cells(leaves), cells, rtol=1e-13, atol=0)
+
+
+def _philox_ref(seed, count):
+    """numpy restatement of Philox4x32-10 + Box-Muller (the device generator's definition)."""
+    M0, M1, W0, W1 = 0xD2511F53, 0xCD9E8D57, 0x9E3779B9, 0xBB67AE85
+    pairs = (count + 1) // 2
+    i = np.arange(pairs, dtype=np.uint64)
+    c = [(i & 0xFFFFFFFF).astype(np.uint64), (i >> np.uint64(32)).astype(np.uint64), np.zeros_like(i), np.zeros_like(i)]
+    k0, k1 = np.uint64(seed & 0xFFFFFFFF), np.uint64(seed >> 32)
+    mask = np.uint64(0xFFFFFFFF)
+    for _ in range(10):
+        p0 = np.uint64(M0) * c[0]
+        p1 = np.uint64(M1) * c[2]
+        hi0, lo0 = p0 >> np.uint64(32), p0 & mask
+        hi1, lo1 = p1 >> np.uint64(32), p1 & mask
+        c = [(hi1 ^ c[1] ^ k0) & mask, lo1, (hi0 ^ c[3] ^ k1) & mask, lo0]
+        k0 = (k0 + np.uint64(W0)) & mask
+        k1 = (k1 + np.uint64(W1)) & mask
+    a = (c[0] << np.uint64(32)) | c[1]
+    b = (c[2] << np.uint64(32)) | c[3]
+    u1 = ((a >> np.uint64(11)).astype(np.float64) + 1.0) * 2.0 ** -53
+    u2 = (b >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    r = np.sqrt(-2.0 * np.log(u1))
+    out = np.empty(2 * pairs)
+    out[0::2] = r * np.cos(2 * np.pi * u2)
+    out[1::2] = r * np.sin(2 * np.pi * u2)
+    return out[:count]
+
+
+def test_philox_probes_and_parity(gpu):
+    """Device-drawn Philox probes (throughput runs): the documented generator (numpy restatement,
+    bits of the uniforms exact, normals to 1e-13), N(0,1) moments, and the estimator on those
+    probes equals pcb_probe_estimate fed the same Z read back."""
+    inp = inputs.small_lattice(**SMALL2D)
+    N = inp.n_points
+    est = Estimator((inp.dom_lo, inp.dom_hi), q=6, seed=2024, generator="philox")
+    Z, _, _ = est.read()
+    ref = _philox_ref(2024, 6 * N).reshape(6, N)
+    assert np.allclose(Z, ref, rtol=0, atol=1e-13 * np.abs(ref).max())
+    big = Estimator((inp.dom_lo, inp.dom_hi), q=400, seed=5, generator="philox").read()[0].reshape(-1)
+    assert abs(big.mean()) < 0.01 and abs(big.var() - 1.0) < 0.01
+    op = ProductConvolutionOperator.from_inputs(inp)
+    Y = 0.5 * normal_vectors(4, 6, N)
+    est.set_y(Y)
+    ea, er = est.update(op, range(op.rank))
+    _, _, ea2, er2 = op.probe_estimate(Z, Y, [])
+    assert abs(ea - ea2) <= 1e-12 * ea2 and abs(er - er2) <= 1e-12 * er2
