@@ -146,8 +146,9 @@ struct EntryArgs {
 cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, const int64_t* x, double* out,
                            int32_t* bad, cudaStream_t st);
 // bshape_host: the block shape per axis (host array, passed by value); scratch: device int32 of
-// blocks_scratch_ints(nblk) (the work list and the candidate lists).  phase 0: classify (writes
-// the all-zero blocks, lists the others); phase 1: gather the listed blocks.
+// blocks_scratch_ints(nblk) (the work lists and the candidate lists).  phase 0: classify (writes
+// or lists the all-zero blocks, lists the others); phase 1: gather the listed blocks; phase 2: the
+// listed zero blocks (independent of phase 1: run it on a second stream).
 cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
                           const int32_t* bshape_host, double* out, int32_t* bad, int32_t* scratch, int phase,
                           cudaStream_t st);

@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(256) k_blocks_classify(EntryArgs a, int32_t nb
     __syncthreads();
     int32_t* queue = scr + 2;
     int32_t* cand_g = scr + 2 + nblk;
+    int32_t* zlist = cand_g + (int64_t)nblk * (cap + 1);
     bool issued = false;  // this thread has bulk stores in flight (lane 0 of a zero-block warp)
     // ---- phase 1: classify (warp wid <-> block blk) ----
     {
@@ -391,6 +392,8 @@ __global__ void __launch_bounds__(256) k_blocks_classify(EntryArgs a, int32_t nb
                     double2* o2 = reinterpret_cast<double2*>(ob);
                     for (int64_t e = lane; e < bytes / 16; e += 32) o2[e] = make_double2(0.0, 0.0);
                     if ((bytes & 15) && lane == 0) *reinterpret_cast<double*>(ob + bytes - 8) = 0.0;
+                } else if (zero_mode == 3) {  // listed for k_blocks_zero, which runs beside the gather
+                    if (lane == 0) zlist[atomicAdd(scr + 1, 1)] = blk;
                 } else if (zero_mode != 2) {
                     double* od = reinterpret_cast<double*>(ob);
                     for (int64_t e = lane; e < (int64_t)npx * npx; e += 32) od[e] = 0.0;
@@ -404,6 +407,26 @@ __global__ void __launch_bounds__(256) k_blocks_classify(EntryArgs a, int32_t nb
         }
     }
     if (issued) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // Z read before the CTA exits
+}
+
+// zero_mode 3: the all-zero blocks listed by the classify pass, one warp per block, 16-byte stores
+// (runs on a second stream concurrently with k_blocks_gather: the two write disjoint blocks)
+__global__ void __launch_bounds__(256) k_blocks_zero(const int32_t* __restrict__ scr, int32_t nblk, int cap, int npx,
+                                                     double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * BC_WARPS + (threadIdx.x >> 5);
+    if (i >= scr[1]) return;
+    const int32_t* zlist = scr + 2 + nblk + (int64_t)nblk * (cap + 1);
+    const int blk = zlist[i];
+    const int64_t n2 = (int64_t)npx * npx;
+    double* ob = out + (int64_t)blk * n2;
+    if ((reinterpret_cast<uintptr_t>(ob) & 15) == 0) {
+        double2* o2 = reinterpret_cast<double2*>(ob);
+        for (int64_t e = lane; e < n2 / 2; e += 32) o2[e] = make_double2(0.0, 0.0);
+        if ((n2 & 1) && lane == 0) ob[n2 - 1] = 0.0;
+    } else {
+        for (int64_t e = lane; e < n2; e += 32) ob[e] = 0.0;
+    }
 }
 
 __global__ void __launch_bounds__(256) k_blocks_gather(EntryArgs a, const int64_t* __restrict__ t_origin,
@@ -577,7 +600,7 @@ cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, co
     return cudaGetLastError();
 }
 
-int64_t blocks_scratch_ints(int32_t nblk) { return 2 + (int64_t)nblk + (int64_t)nblk * (BT_CAP + 1); }
+int64_t blocks_scratch_ints(int32_t nblk) { return 2 + (int64_t)nblk + (int64_t)nblk * (BT_CAP + 1) + nblk; }
 
 cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
                           const int32_t* bshape_host, double* out, int32_t* bad, int32_t* scratch, int phase,
@@ -592,12 +615,13 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
         const char* e = getenv("PCB_BLOCK_CAP");
         return e ? std::max(1, std::min(BT_CAP, atoi(e))) : 16;
     }();
-    // zero blocks: 0 = TMA bulk copies of a zero tile, 1 = 16-byte stores, 2 = one memset of the
-    // whole output before the classify pass (PCB_C5_ZERO).  Measured at config 5 (4096 blocks, 4031
-    // zero): classify + gather 63.3 / 63.6 / 64.7 us -- the zero writes are not the limit.
+    // zero blocks: 0 = TMA bulk copies of a zero tile inside the classify pass, 1 = 16-byte stores
+    // there, 2 = one memset of the whole output before it, 3 = listed by the classify pass and
+    // written by k_blocks_zero on a second stream while the gather runs (PCB_C5_ZERO).  Measured at
+    // config 5 (4096 blocks, 4031 zero): modes 0/1/2 63.3 / 63.6 / 64.7 us.
     static const int zero_mode = [] {
         const char* e = getenv("PCB_C5_ZERO");
-        return e ? std::max(0, std::min(2, atoi(e))) : 0;
+        return e ? std::max(0, std::min(3, atoi(e))) : 3;
     }();
     const size_t smem = sizeof(double) * (size_t)cap * (size_t)(npx + win) + sizeof(int) * (size_t)npx +
                         (size_t)npx * (1 + BT_NZ) + 16;
@@ -607,8 +631,14 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
         k_blocks<<<148 * 16, 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape_host[0], bs1, bs2, out, bad);
         return cudaGetLastError();
     }
-    if (phase == 0) {  // classify (zero blocks written here), listing the others for phase 1
-        cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(int32_t), st);
+    if (phase == 2) {  // zero_mode 3: the listed zero blocks (on a second stream, beside phase 1)
+        if (zero_mode != 3) return cudaSuccess;
+        k_blocks_zero<<<(unsigned)((nblk + BC_WARPS - 1) / BC_WARPS), 32 * BC_WARPS, 0, st>>>(scratch, nblk, cap, (int)npx,
+                                                                                          out);
+        return cudaGetLastError();
+    }
+    if (phase == 0) {  // classify (zero blocks written or listed here), listing the others for phase 1
+        cudaError_t e = cudaMemsetAsync(scratch, 0, 2 * sizeof(int32_t), st);
         if (e == cudaSuccess && zero_mode == 2)
             e = cudaMemsetAsync(out, 0, sizeof(double) * (size_t)nblk * (size_t)(npx * npx), st);
         if (e != cudaSuccess) return e;

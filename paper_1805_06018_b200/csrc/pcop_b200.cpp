@@ -317,6 +317,7 @@ struct pcb_op {
     int reduce = PCB_REDUCE_NONE;
     int comm_chunks = 4;
     cudaStream_t s_comm = nullptr;
+    cudaStream_t s_aux = nullptr;   // second stream of the block gather (zero blocks)
     // entry gather
     int32_t bucket[3] = {1, 1, 1}, nb[3] = {1, 1, 1};
     pcb::DevBuf<int64_t> bucket_ptr;
@@ -2150,6 +2151,10 @@ PCB_API pcb_status pcb_destroy(pcb_op* op) {
         cudaStreamDestroy(op->s_comm);
     }
     if (op->comm) comm_destroy(op->comm);
+    if (op->s_aux) {
+        cudaStreamSynchronize(op->s_aux);
+        cudaStreamDestroy(op->s_aux);
+    }
     if (op->bounce) cudaFreeHost(op->bounce);
     for (cudaEvent_t e : op->ev_io)
         if (e) cudaEventDestroy(e);
@@ -2553,8 +2558,17 @@ static void blocks_common(pcb_op* op, int32_t nblk, const int64_t* d_t, const in
     PCB_CK(cudaMemsetAsync(op->st_flag.p, 0, 4, st));
     launch(op, st, "blocks(classify)",
            [&] { return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, op->st_blk.p, 0, st); });
+    // the zero blocks on a second stream beside the gather of the others (disjoint outputs)
+    if (!op->s_aux) PCB_CK(cudaStreamCreateWithFlags(&op->s_aux, cudaStreamNonBlocking));
+    PCB_CK(cudaEventRecord(op_event(op, 6), st));
+    PCB_CK(cudaStreamWaitEvent(op->s_aux, op_event(op, 6), 0));
+    launch(op, op->s_aux, "blocks(zero)", [&] {
+        return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, op->st_blk.p, 2, op->s_aux);
+    });
     launch(op, st, "blocks(gather)",
            [&] { return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, op->st_blk.p, 1, st); });
+    PCB_CK(cudaEventRecord(op_event(op, 7), op->s_aux));
+    PCB_CK(cudaStreamWaitEvent(st, op_event(op, 7), 0));
     if (host_check) {
         int32_t bad = 0;
         PCB_CK(cudaMemcpyAsync(&bad, op->st_flag.p, 4, cudaMemcpyDeviceToHost, st));
