@@ -618,10 +618,11 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
     // zero blocks: 0 = TMA bulk copies of a zero tile inside the classify pass, 1 = 16-byte stores
     // there, 2 = one memset of the whole output before it, 3 = listed by the classify pass and
     // written by k_blocks_zero on a second stream while the gather runs (PCB_C5_ZERO).  Measured at
-    // config 5 (4096 blocks, 4031 zero): modes 0/1/2 63.3 / 63.6 / 64.7 us.
+    // config 5 (4096 blocks, 4031 zero): modes 0/1/2/3 61.4 / 63.6 / 64.7 / 60.8 us (mode 3: the
+    // gather slows from 24 to 43 us beside the zero writes).
     static const int zero_mode = [] {
         const char* e = getenv("PCB_C5_ZERO");
-        return e ? std::max(0, std::min(3, atoi(e))) : 3;
+        return e ? std::max(0, std::min(3, atoi(e))) : 0;
     }();
     const size_t smem = sizeof(double) * (size_t)cap * (size_t)(npx + win) + sizeof(int) * (size_t)npx +
                         (size_t)npx * (1 + BT_NZ) + 16;
