@@ -38,6 +38,15 @@
 #ifndef PCB_E3_SMALL_MAX
 #define PCB_E3_SMALL_MAX 0  // 3-smooth lengths <= this use 12 elements per thread (0: none)
 #endif
+#ifndef PCB_TW_RECUR
+// Stage twiddles w^r (r = 1 .. RS-1, w = e^{-+2 pi i k / (NS RS)}): 0 loads all RS-1 from the
+// table; otherwise the stage loads only w^(2^b) and forms w^r as the product of the powers in r's
+// bits (<= 4 complex products, a few ulp) -- fewer live registers in the hot stages.  1: radix 16;
+// 2: radix 8 and 16; 3 (default): every radix >= 4.  Measured on B200 (c3 / c4 / c2 vec/s):
+// 0: 8,695 / 1,042 / 30,617; 2: 8,864 / 1,049 / 31,047; 3: 8,909 / 1,064 / 31,143 (cols 206
+// instead of 224 registers at P0 = 256).
+#define PCB_TW_RECUR 3
+#endif
 #define PCB_NS_CAT2(a, b) a##b
 #define PCB_NS_CAT(a, b) PCB_NS_CAT2(a, b)
 
@@ -45,7 +54,7 @@ namespace pcb {
 // the engine is instantiated per element count: distinct names per translation unit setting
 inline namespace PCB_NS_CAT(PCB_NS_CAT(PCB_NS_CAT(e, PCB_E2), PCB_NS_CAT(_, PCB_E3)),
                             PCB_NS_CAT(PCB_NS_CAT(PCB_NS_CAT(_s, PCB_E2_SMALL_MAX), PCB_NS_CAT(_t, PCB_E3_SMALL_MAX)),
-                                       PCB_NS_CAT(_d, PCB_RADIX_DESC))) {
+                                       PCB_NS_CAT(PCB_NS_CAT(_d, PCB_RADIX_DESC), PCB_NS_CAT(_w, PCB_TW_RECUR)))) {
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -251,10 +260,34 @@ __device__ __forceinline__ void stage_math(double2* v, int tl, const double2* __
         if (NS > 1) {
             const int k = j % NS;
             constexpr int step = L / (NS * RS);
+            // bits needed for r < RS, and whether this radix uses the product form at this setting
+            constexpr int LB = RS > 16 ? 5 : RS > 8 ? 4 : RS > 4 ? 3 : RS > 2 ? 2 : 1;
+            constexpr bool RECUR = (PCB_TW_RECUR >= 1 && RS == 16) || (PCB_TW_RECUR >= 2 && RS == 8) ||
+                                   (PCB_TW_RECUR >= 3 && RS >= 4);
+            if constexpr (RECUR) {
+                // log2(RS) table loads instead of RS - 1 (fewer live registers): w^r = the product of
+                // the loaded powers of two in r's bits (at most LB - 1 complex products, ~1 ulp each)
+                double2 wp[LB];
 #pragma unroll
-            for (int r = 1; r < RS; ++r) {
-                const double2 w = __ldg(&tw[r * k * step]);
-                v[b * RS + r] = DIR < 0 ? cmul(v[b * RS + r], w) : cmulc(v[b * RS + r], w);
+                for (int bit = 0; bit < LB; ++bit) wp[bit] = __ldg(&tw[(1 << bit) * k * step]);
+#pragma unroll
+                for (int r = 1; r < RS; ++r) {
+                    double2 w = make_double2(1.0, 0.0);
+                    bool first = true;
+#pragma unroll
+                    for (int bit = 0; bit < LB; ++bit)
+                        if (r & (1 << bit)) {
+                            w = first ? wp[bit] : cmul(w, wp[bit]);
+                            first = false;
+                        }
+                    v[b * RS + r] = DIR < 0 ? cmul(v[b * RS + r], w) : cmulc(v[b * RS + r], w);
+                }
+            } else {
+#pragma unroll
+                for (int r = 1; r < RS; ++r) {
+                    const double2 w = __ldg(&tw[r * k * step]);
+                    v[b * RS + r] = DIR < 0 ? cmul(v[b * RS + r], w) : cmulc(v[b * RS + r], w);
+                }
             }
         }
         dft<RS, DIR>(&v[b * RS]);
