@@ -9,7 +9,7 @@
 using namespace pcb;
 
 template <int L, int DIR, bool REV>
-__global__ void k_test(const double2* in, double2* out, const double2* tw) {
+__global__ void __launch_bounds__(1024) k_test(const double2* in, double2* out, const double2* tw) {
     constexpr int NL = 2;
     constexpr int E = FftCfg<L>::R;
     constexpr int PS = 3;
@@ -65,7 +65,8 @@ int run(const double2* dtw) {
             if (dir < 0 && !rev) launch(k_test<L, -1, false>, NL * FftCfg<L>::TPL, sizeof(double2) * SmemLine<L, 2, 3>::WORDS, din, dout, dtw);
             if (dir > 0 && rev) launch(k_test<L, 1, true>, NL * FftCfg<L>::TPL, sizeof(double2) * SmemLine<L, 2, 3>::WORDS, din, dout, dtw);
             if (dir > 0 && !rev) launch(k_test<L, 1, false>, NL * FftCfg<L>::TPL, sizeof(double2) * SmemLine<L, 2, 3>::WORDS, din, dout, dtw);
-            cudaError_t e = cudaDeviceSynchronize();
+            cudaError_t e = cudaGetLastError();  // a launch failure (e.g. resources) is not sticky
+            if (e == cudaSuccess) e = cudaDeviceSynchronize();
             if (e != cudaSuccess) {
                 printf("L=%d cuda error %s\n", L, cudaGetErrorString(e));
                 return 1;
