@@ -390,8 +390,14 @@ __global__ void __launch_bounds__(NL * FftCfg<P1>::TPL) k_mid(PassArgs a) {
 
 // ---------------------------------------------------------------------------
 // cols: axis-0 pass with the frequency-domain product (K3).
+#ifdef PCB_COLS_MAXNREG  // A/B: a register ceiling for the long-column pass (occupancy vs load batching)
+#define PCB_COLS_BOUNDS(P0, NL) __launch_bounds__(NL * FftCfg<P0>::TPL, P0 <= 64 ? PCB_COLS_MINB_SMALL : 1) \
+    __maxnreg__(P0 <= 64 ? 255 : PCB_COLS_MAXNREG)
+#else
+#define PCB_COLS_BOUNDS(P0, NL) __launch_bounds__(NL * FftCfg<P0>::TPL, P0 <= 64 ? PCB_COLS_MINB_SMALL : PCB_COLS_MINB)
+#endif
 template <int P0, int NL, int MODE>
-__global__ void __launch_bounds__(NL * FftCfg<P0>::TPL, P0 <= 64 ? PCB_COLS_MINB_SMALL : PCB_COLS_MINB) k_cols(PassArgs a) {
+__global__ void PCB_COLS_BOUNDS(P0, NL) k_cols(PassArgs a) {
     constexpr int R = FftCfg<P0>::R;
     constexpr int RF = FirstPos<P0>::RF;
     constexpr int RL = LastPos<P0>::RL;
