@@ -288,12 +288,14 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
         const double2 zn = buf[sidx<NL, PS>(k == 0 ? 0 : N - k, ll)];
         const double2 A = make_double2(0.5 * (zk.x + zn.x), 0.5 * (zk.y - zn.y));
         const double2 Bm = make_double2(0.5 * (zk.y + zn.y), -0.5 * (zk.x - zn.x));  // (zk - conj zn)/(2i)
-        S_item[row + k] = cadd(A, cmul(__ldg(&twP[k]), Bm));
+        const double2 wk = __ldg(&twP[k]);
+        S_item[row + k] = cadd(A, cmul(wk, Bm));
         if (k == 0) {
-            S_item[row + N] = cadd(A, cmul(__ldg(&twP[N]), Bm));
+            S_item[row + N] = cadd(A, cmul(make_double2(-1.0, 0.0), Bm));  // W^N = -1
         } else if (2 * k != N) {
+            // W^(N-k) = -conj(W^k) (P = 2N): no second table load
             const double2 Ac = make_double2(A.x, -A.y), Bc = make_double2(Bm.x, -Bm.y);
-            S_item[row + N - k] = cadd(Ac, cmul(__ldg(&twP[N - k]), Bc));
+            S_item[row + N - k] = cadd(Ac, cmul(make_double2(-wk.x, wk.y), Bc));
         }
     }
 }
@@ -855,13 +857,16 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
                     const double2* x = stg + ((cur * NL + l) * MB + j) * SLS;
                     const double sc = mb[m0 + j].scale;
                     const int dl = mb[m0 + j].delta;
+                    // the phase of bin N - k is (-1)^dl conj(phase of bin k) (P = 2N): one table load per pair
+                    const double sn = (dl & 1) ? -1.0 : 1.0;
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int k = tl + r * TPL;
                         double2 xk = x[k], xn = x[N - k];
                         if (dl != 0) {
-                            xk = cmul(xk, __ldg(&twP[(k * dl) % P]));
-                            xn = cmul(xn, __ldg(&twP[((N - k) * dl) % P]));
+                            const double2 w = __ldg(&twP[(k * dl) % P]);
+                            xk = cmul(xk, w);
+                            xn = cmul(xn, make_double2(sn * w.x, -sn * w.y));
                         }
                         zk[r] = make_double2(fma(sc, xk.x, zk[r].x), fma(sc, xk.y, zk[r].y));
                         zn[r] = make_double2(fma(sc, xn.x, zn[r].x), fma(sc, xn.y, zn[r].y));
@@ -958,13 +963,16 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
                     const double2* x = stg + ((cur * NL + l) * MB + j) * SL;
                     const double sc = mb[m0 + j].scale;
                     const int dl = mb[m0 + j].delta;
+                    // the phase of bin N - k is (-1)^dl conj(phase of bin k) (P = 2N): one table load per pair
+                    const double sn = (dl & 1) ? -1.0 : 1.0;
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int k = tl + r * TPL;
                         double2 xk = x[k], xn = x[N - k];
                         if (dl != 0) {
-                            xk = cmul(xk, __ldg(&twP[(k * dl) % P]));
-                            xn = cmul(xn, __ldg(&twP[((N - k) * dl) % P]));
+                            const double2 w = __ldg(&twP[(k * dl) % P]);
+                            xk = cmul(xk, w);
+                            xn = cmul(xn, make_double2(sn * w.x, -sn * w.y));
                         }
                         zk[r] = make_double2(fma(sc, xk.x, zk[r].x), fma(sc, xk.y, zk[r].y));
                         zn[r] = make_double2(fma(sc, xn.x, zn[r].x), fma(sc, xn.y, zn[r].y));
