@@ -39,6 +39,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Atilde-apply vectors/sec (fp64)"
+
+
+def emit(line: dict) -> None:  # replaced in main() by the writer to the saved stdout
+    print(json.dumps(line), flush=True)
 UNIT = "vectors/s"
 
 # workload definitions; c3 is the headline (BASELINE.json north_star target)
@@ -259,7 +263,7 @@ def run_reference(args, rank, world):
                                                          "operator built per BASELINE.json)",
             "config": workload_config(args.config), "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def source_hash() -> str:
@@ -279,6 +283,15 @@ def source_hash() -> str:
 
 
 def main():
+    # exactly one JSON line on stdout: everything else the process writes to fd 1 (NCCL's init
+    # banner and NCCL_DEBUG=INFO log lines, library prints) goes to stderr
+    json_out = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
+    os.environ.setdefault("NCCL_DEBUG", "INFO")  # NCCL init logs (ranks, NVLS / transport choice) on stderr
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    global emit
+    emit = lambda line: (json_out.write(json.dumps(line) + "\n"), json_out.flush())  # noqa: E731
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -531,7 +544,7 @@ def main():
         }
         if rhs:
             line["rhs_weak"] = rhs
-        print(json.dumps(line), flush=True)
+        emit(line)
     op.close()
     if use_dist:
         dist.barrier()
