@@ -153,6 +153,8 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
                           const int32_t* bshape_host, double* out, int32_t* bad, int32_t* scratch, int phase,
                           cudaStream_t st);
 int64_t blocks_scratch_ints(int32_t nblk);
+// how the all-zero blocks are written (see launch_blocks; 3: phase 2 runs beside phase 1, 4: beside phase 0)
+int blocks_zero_mode();
 
 // block apply, direct form (small blocks)
 cudaError_t launch_block_direct(const EntryArgs& a, int32_t nblk, int64_t max_t, const int64_t* t_lo,

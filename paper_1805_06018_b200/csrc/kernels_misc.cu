@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(256) k_blocks_classify(EntryArgs a, int32_t nb
                 } else if (zero_mode != 2) {
                     double* od = reinterpret_cast<double*>(ob);
                     for (int64_t e = lane; e < (int64_t)npx * npx; e += 32) od[e] = 0.0;
-                }  // zero_mode 2: the output was memset before the launch
+                }  // zero_mode 2 / 4: the output is memset before / beside the launch
             } else if (lane == 0) {  // list the block for the gather kernel, with its candidates
                 int32_t* cg = cand_g + (int64_t)blk * (cap + 1);
                 cg[0] = fb ? -1 : nk;
@@ -600,6 +600,14 @@ cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, co
     return cudaGetLastError();
 }
 
+int blocks_zero_mode() {
+    static const int mode = [] {
+        const char* e = getenv("PCB_C5_ZERO");
+        return e ? std::max(0, std::min(4, atoi(e))) : 0;
+    }();
+    return mode;
+}
+
 int64_t blocks_scratch_ints(int32_t nblk) { return 2 + (int64_t)nblk + (int64_t)nblk * (BT_CAP + 1) + nblk; }
 
 cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
@@ -615,15 +623,15 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
         const char* e = getenv("PCB_BLOCK_CAP");
         return e ? std::max(1, std::min(BT_CAP, atoi(e))) : 16;
     }();
-    // zero blocks: 0 = TMA bulk copies of a zero tile inside the classify pass, 1 = 16-byte stores
-    // there, 2 = one memset of the whole output before it, 3 = listed by the classify pass and
-    // written by k_blocks_zero on a second stream while the gather runs (PCB_C5_ZERO).  Measured at
-    // config 5 (4096 blocks, 4031 zero): modes 0/1/2/3 61.4 / 63.6 / 64.7 / 60.8 us (mode 3: the
-    // gather slows from 24 to 43 us beside the zero writes).
-    static const int zero_mode = [] {
-        const char* e = getenv("PCB_C5_ZERO");
-        return e ? std::max(0, std::min(3, atoi(e))) : 0;
-    }();
+    // zero blocks (blocks_zero_mode, PCB_C5_ZERO): 0 = TMA bulk copies of a zero tile inside the
+    // classify pass, 1 = 16-byte stores there, 2 = one memset of the whole output before it, 3 =
+    // listed by the classify pass and written by k_blocks_zero on a second stream while the gather
+    // runs, 4 = the memset on a second stream while the classify pass runs, the gather after both.
+    // Measured at config 5 (4096 blocks, 4031 zero): modes 0/1/2/3/4 61.4 / 63.6 / 64.7 / 59.2 /
+    // 73.7 us -- the classify and gather passes are chains of dependent loads and slow down beside
+    // a concurrent zero stream (gather 24 -> 42 us in mode 3, classify 18 -> 54 us in mode 4), so the
+    // default (0) keeps the passes apart.
+    const int zero_mode = blocks_zero_mode();
     const size_t smem = sizeof(double) * (size_t)cap * (size_t)(npx + win) + sizeof(int) * (size_t)npx +
                         (size_t)npx * (1 + BT_NZ) + 16;
     const int bs1 = a.D > 1 ? bshape_host[1] : 1, bs2 = a.D > 2 ? bshape_host[2] : 1;
@@ -632,7 +640,9 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
         k_blocks<<<148 * 16, 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape_host[0], bs1, bs2, out, bad);
         return cudaGetLastError();
     }
-    if (phase == 2) {  // zero_mode 3: the listed zero blocks (on a second stream, beside phase 1)
+    if (phase == 2) {  // the zero writes on a second stream: mode 4 the memset of the whole output
+                       // (beside phase 0), mode 3 the listed zero blocks (beside phase 1)
+        if (zero_mode == 4) return cudaMemsetAsync(out, 0, sizeof(double) * (size_t)nblk * (size_t)(npx * npx), st);
         if (zero_mode != 3) return cudaSuccess;
         k_blocks_zero<<<(unsigned)((nblk + BC_WARPS - 1) / BC_WARPS), 32 * BC_WARPS, 0, st>>>(scratch, nblk, cap, (int)npx,
                                                                                           out);
@@ -640,7 +650,7 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
     }
     if (phase == 0) {  // classify (zero blocks written or listed here), listing the others for phase 1
         cudaError_t e = cudaMemsetAsync(scratch, 0, 2 * sizeof(int32_t), st);
-        if (e == cudaSuccess && zero_mode == 2)
+        if (e == cudaSuccess && zero_mode == 2)  // (mode 4: phase 2 on the second stream)
             e = cudaMemsetAsync(out, 0, sizeof(double) * (size_t)nblk * (size_t)(npx * npx), st);
         if (e != cudaSuccess) return e;
         k_blocks_classify<<<(unsigned)((nblk + BC_WARPS - 1) / BC_WARPS), 32 * BC_WARPS, 0, st>>>(

@@ -2556,19 +2556,26 @@ static void blocks_common(pcb_op* op, int32_t nblk, const int64_t* d_t, const in
     op->st_flag.ensure(1);
     op->st_blk.ensure((size_t)blocks_scratch_ints(nblk));
     PCB_CK(cudaMemsetAsync(op->st_flag.p, 0, 4, st));
-    launch(op, st, "blocks(classify)",
-           [&] { return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, op->st_blk.p, 0, st); });
-    // the zero blocks on a second stream beside the gather of the others (disjoint outputs)
-    if (!op->s_aux) PCB_CK(cudaStreamCreateWithFlags(&op->s_aux, cudaStreamNonBlocking));
-    PCB_CK(cudaEventRecord(op_event(op, 6), st));
-    PCB_CK(cudaStreamWaitEvent(op->s_aux, op_event(op, 6), 0));
-    launch(op, op->s_aux, "blocks(zero)", [&] {
-        return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, op->st_blk.p, 2, op->s_aux);
-    });
-    launch(op, st, "blocks(gather)",
-           [&] { return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, op->st_blk.p, 1, st); });
-    PCB_CK(cudaEventRecord(op_event(op, 7), op->s_aux));
-    PCB_CK(cudaStreamWaitEvent(st, op_event(op, 7), 0));
+    // phase 0 classifies the blocks, phase 1 gathers the ones with candidate terms, phase 2 writes
+    // the all-zero ones on a second stream beside phase 0 (mode 4) or phase 1 (mode 3)
+    auto phase = [&](int ph, cudaStream_t s2) {
+        return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, op->st_blk.p, ph, s2);
+    };
+    const int zm = blocks_zero_mode();
+    const bool aux = zm == 3 || zm == 4;
+    if (aux && !op->s_aux) PCB_CK(cudaStreamCreateWithFlags(&op->s_aux, cudaStreamNonBlocking));
+    auto fork = [&] {
+        PCB_CK(cudaEventRecord(op_event(op, 6), st));
+        PCB_CK(cudaStreamWaitEvent(op->s_aux, op_event(op, 6), 0));
+        launch(op, op->s_aux, "blocks(zero)", [&] { return phase(2, op->s_aux); });
+        PCB_CK(cudaEventRecord(op_event(op, 7), op->s_aux));
+    };
+    if (zm == 4) fork();
+    launch(op, st, "blocks(classify)", [&] { return phase(0, st); });
+    if (zm == 3) fork();
+    if (zm == 4) PCB_CK(cudaStreamWaitEvent(st, op_event(op, 7), 0));  // the memset before the gather's writes
+    launch(op, st, "blocks(gather)", [&] { return phase(1, st); });
+    if (zm == 3) PCB_CK(cudaStreamWaitEvent(st, op_event(op, 7), 0));
     if (host_check) {
         int32_t bad = 0;
         PCB_CK(cudaMemcpyAsync(&bad, op->st_flag.p, 4, cudaMemcpyDeviceToHost, st));
