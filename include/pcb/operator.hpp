@@ -8,6 +8,7 @@
 #define PCB_OPERATOR_HPP
 
 #include <cstdint>
+#include <new>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -40,6 +41,27 @@ inline void check(pcb_status st) {
     if (st == PCB_EINVAL) throw std::invalid_argument(msg);
     throw std::runtime_error(msg);
 }
+
+// std::allocator over page-locked host memory (pcb_host_alloc): vectors allocated with it go
+// straight to the copy engines in apply_batch (no bounce staging).
+template <typename T>
+struct pinned_allocator {
+    using value_type = T;
+    pinned_allocator() = default;
+    template <typename U>
+    pinned_allocator(const pinned_allocator<U>&) {}
+    T* allocate(size_t n) {
+        void* p = nullptr;
+        if (pcb_host_alloc(static_cast<uint64_t>(n) * sizeof(T), &p) != PCB_OK) throw std::bad_alloc();
+        return static_cast<T*>(p);
+    }
+    void deallocate(T* p, size_t) { pcb_host_free(p); }
+    template <typename U>
+    bool operator==(const pinned_allocator<U>&) const { return true; }
+    template <typename U>
+    bool operator!=(const pinned_allocator<U>&) const { return false; }
+};
+using pinned_vector = std::vector<double, pinned_allocator<double>>;
 
 // A fresh 128-byte NCCL id for pcb_options.nccl_id (shard-by-k with the reduce inside the
 // library): create it on one rank and send it to the others (MPI_Bcast, a file, a socket ...).
@@ -107,6 +129,14 @@ class ProductConvolutionOperator {
     std::vector<double> apply_adjoint(const std::vector<double>& f) const { return run(f, 1, true); }
     // B vectors, vector-major
     std::vector<double> apply_batch(const std::vector<double>& F, int32_t B) const { return run(F, B, false); }
+    // pinned buffers (pinned_vector): no bounce staging on either side
+    void apply_batch(const pinned_vector& F, pinned_vector& G, int32_t B, bool adjoint = false) const {
+        const int64_t N = domain_.num_points();
+        if (static_cast<int64_t>(F.size()) != N * B)
+            throw std::invalid_argument(adjoint ? "PCOp::apply_adjoint: shape mismatch" : "PCOp::apply: shape mismatch");
+        G.resize(F.size());
+        check(adjoint ? pcb_apply_adjoint_batch(op_, B, F.data(), G.data()) : pcb_apply_batch(op_, B, F.data(), G.data()));
+    }
     std::vector<double> apply_adjoint_batch(const std::vector<double>& F, int32_t B) const {
         return run(F, B, true);
     }

@@ -301,6 +301,13 @@ PCB_API pcb_status pcb_hmatrix_load(const char* path, pcb_hmatrix** out);
  * without PCB_GUARD. */
 PCB_API pcb_status pcb_debug_guard_check(int64_t* n_regions, int64_t* n_bad_bytes);
 
+/* Page-locked host memory for the host-buffer calls: F and G in pinned memory go straight to the
+ * copy engines (c3: 5.5k vectors/s end to end), pageable buffers are staged through the handle's
+ * pinned bounce slots by host threads (~1.2k vectors/s, host-memory-bound).  pcb::pinned_allocator
+ * (operator.hpp) wraps these for std::vector. */
+PCB_API pcb_status pcb_host_alloc(uint64_t bytes, void** out);
+PCB_API pcb_status pcb_host_free(void* p);
+
 /* Number of kernels this library has launched in the process (all handles). */
 PCB_API long long pcb_launch_count(void);
 

@@ -2013,6 +2013,34 @@ PCB_API pcb_status pcb_debug_guard_check(int64_t* n_regions, int64_t* n_bad_byte
     });
 }
 
+PCB_API pcb_status pcb_host_alloc(uint64_t bytes, void** out) {
+    if (!out) {
+        set_err("pcb_host_alloc: null output");
+        return PCB_EINVAL;
+    }
+    *out = nullptr;
+    if (bytes == 0) return PCB_OK;
+    const cudaError_t e = cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        *out = nullptr;
+        set_err(std::string("cudaHostAlloc failed: ") + cudaGetErrorString(e));
+        return e == cudaErrorMemoryAllocation ? PCB_ENOMEM : PCB_ECUDA;
+    }
+    return PCB_OK;
+}
+
+PCB_API pcb_status pcb_host_free(void* p) {
+    if (!p) return PCB_OK;
+    const cudaError_t e = cudaFreeHost(p);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        set_err(std::string("cudaFreeHost failed: ") + cudaGetErrorString(e));
+        return PCB_ECUDA;
+    }
+    return PCB_OK;
+}
+
 PCB_API pcb_status pcb_comm_unique_id(void* id128) {
     if (!id128) {
         set_err("pcb_comm_unique_id: null output");

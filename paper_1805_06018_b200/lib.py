@@ -34,7 +34,8 @@ EXPORTS = ["pcb_default_options", "pcb_last_error", "pcb_create", "pcb_destroy",
            "pcb_get_domain", "pcb_cluster_tree", "pcb_hmatrix_assemble", "pcb_hmatrix_compress",
            "pcb_hmatrix_destroy", "pcb_hmatrix_get_info", "pcb_hmatrix_tree", "pcb_hmatrix_block",
            "pcb_hmatrix_admissible", "pcb_hmatrix_matvec", "pcb_hmatrix_save", "pcb_hmatrix_load",
-           "pcb_comm_unique_id", "pcb_plan_shards", "pcb_debug_guard_check", "pcb_estimator_create_ex"]
+           "pcb_comm_unique_id", "pcb_plan_shards", "pcb_debug_guard_check", "pcb_estimator_create_ex",
+           "pcb_host_alloc", "pcb_host_free"]
 RNG = {"mt19937": 0, "philox": 1}
 REDUCE = {"none": 0, "all": 1, "root": 2}
 PARTITION = {"cost": 0, "count": 1}
@@ -149,6 +150,8 @@ def load():
     L.pcb_hmatrix_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
     L.pcb_comm_unique_id.argtypes = [vp]
     L.pcb_debug_guard_check.argtypes = [P_i64, P_i64]
+    L.pcb_host_alloc.argtypes = [ctypes.c_uint64, ctypes.POINTER(vp)]
+    L.pcb_host_free.argtypes = [vp]
     L.pcb_plan_shards.argtypes = [i32, P_i64, P_i64, i32, P_i64, P_i64, ctypes.POINTER(vp), P_i64, P_i64,
                                   ctypes.POINTER(vp), i32, i32, vp, vp]
     for n in EXPORTS:

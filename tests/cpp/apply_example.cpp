@@ -72,6 +72,16 @@ int main() {
                         std::sqrt(num / den));
             if (!(std::sqrt(num / den) <= 1e-11) || sop.info().comm_nranks != 1) return 4;
         }
+        // pinned host buffers (pcb::pinned_vector): the copy-engine path, same result
+        {
+            pcb::ProductConvolutionOperator pop(dom, w, phi);
+            pcb::pinned_vector pf(f.begin(), f.end()), pg;
+            pop.apply_batch(pf, pg, 1);
+            const std::vector<double> ref = pop.apply(f);
+            for (int i = 0; i < n * n; ++i)
+                if (pg[i] != ref[i]) return 5;
+            std::printf("pinned_vector apply: bitwise equal to the pageable path\n");
+        }
         // reference error behaviour
         pcb::ProductConvolutionOperator op(dom, w, phi);
         try {
