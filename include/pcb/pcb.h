@@ -145,6 +145,19 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
                               const int64_t* points, const int64_t* w_lo, const int64_t* w_hi,
                               const double* const* w_vals, const int64_t* phi_lo, const int64_t* phi_hi,
                               const double* const* phi_vals, const pcb_options* opt, pcb_op** out);
+/* Single-process multi-GPU (SURVEY 8(e) from one process, as the reference's own callers are):
+ * one handle over ndev devices, shard s (the planner's cost-balanced block s of ndev) on
+ * devices[s].  Apply / adjoint / estimator calls take buffers on devices[0] (or host buffers); F
+ * reaches the other devices by a scatter + all-gather of peer copies, each shard computes its
+ * partial on its own device, and the partials are summed by the library's own reduction kernel
+ * (slice s summed on devices[s] from peer loads, stored into G over NVLink; shard order,
+ * deterministic).  Entries / blocks are served by shard 0 (every shard holds all the terms for
+ * them).  devices may repeat (several shards on one GPU).  No nccl_id in opt. */
+PCB_API pcb_status pcb_create_multi(int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t r,
+                                    const int64_t* points, const int64_t* w_lo, const int64_t* w_hi,
+                                    const double* const* w_vals, const int64_t* phi_lo, const int64_t* phi_hi,
+                                    const double* const* phi_vals, const pcb_options* opt, const int32_t* devices,
+                                    int32_t ndev, pcb_op** out);
 PCB_API pcb_status pcb_destroy(pcb_op* op);
 PCB_API pcb_status pcb_get_info(const pcb_op* op, pcb_info* info);
 

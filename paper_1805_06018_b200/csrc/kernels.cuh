@@ -169,6 +169,9 @@ cudaError_t launch_probe_sums(int D, const int32_t* n, int32_t nbox, const int64
                               int32_t q, const double* Yt, const double* Y, double* d2, double* y2, cudaStream_t st);
 
 cudaError_t launch_zero(double* p, int64_t n, cudaStream_t st);
+// out[off + i] = sum over t of parts[t][off + i], i < len (multi-device reduction; peer pointers)
+cudaError_t launch_sum_parts(const double* const* d_parts, int nparts, int64_t off, int64_t len, double* out,
+                             cudaStream_t st);
 // count N(0,1) draws from Philox4x32-10 (counter = pair index, key = seed) + Box-Muller, on the device
 cudaError_t launch_philox_normal(uint64_t seed, int64_t count, double* out, cudaStream_t st);
 

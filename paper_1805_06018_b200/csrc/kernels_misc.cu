@@ -733,6 +733,25 @@ cudaError_t launch_philox_normal(uint64_t seed, int64_t count, double* out, cuda
     return cudaGetLastError();
 }
 
+// Multi-device reduction (pcb_create_multi): out[off + i] = sum_t parts[t][off + i] in shard order
+// (deterministic); parts and out may live on other devices (peer loads / stores over NVLink).
+__global__ void k_sum_parts(const double* const* __restrict__ parts, int nparts, int64_t off, int64_t len,
+                            double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int t = 0; t < nparts; ++t) s += parts[t][off + i];
+        out[off + i] = s;
+    }
+}
+
+cudaError_t launch_sum_parts(const double* const* d_parts, int nparts, int64_t off, int64_t len, double* out,
+                             cudaStream_t st) {
+    if (len <= 0) return cudaSuccess;
+    const int64_t blocks = std::min<int64_t>((len + 255) / 256, 148LL * 8);
+    k_sum_parts<<<(unsigned)blocks, 256, 0, st>>>(d_parts, nparts, off, len, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_zero(double* p, int64_t n, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     k_zero<<<148 * 8, 256, 0, st>>>(p, n);

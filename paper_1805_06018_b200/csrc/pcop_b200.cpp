@@ -318,6 +318,18 @@ struct pcb_op {
     int comm_chunks = 4;
     cudaStream_t s_comm = nullptr;
     cudaStream_t s_aux = nullptr;   // second stream of the block gather (zero blocks)
+    // single-process multi-GPU handle (pcb_create_multi): the shards' handles, one per device, and
+    // per shard its copy of the input (remote devices) and its partial output, B x N each
+    std::vector<pcb_op*> subs;
+    std::vector<int> sub_dev;
+    struct SubBuf {
+        double* fin = nullptr;
+        double* part = nullptr;
+        size_t n = 0;
+        cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // inputs in, partial done, slice reduced
+    };
+    std::vector<SubBuf> sbuf;
+    std::vector<double**> d_parts_s;  // per shard: a device array (on its device) of every partial pointer
     // entry gather
     int32_t bucket[3] = {1, 1, 1}, nb[3] = {1, 1, 1};
     pcb::DevBuf<int64_t> bucket_ptr;
@@ -2159,13 +2171,132 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
     return PCB_OK;
 }
 
+PCB_API pcb_status pcb_create_multi(int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi, int32_t r,
+                                    const int64_t* points, const int64_t* w_lo, const int64_t* w_hi,
+                                    const double* const* w_vals, const int64_t* phi_lo, const int64_t* phi_hi,
+                                    const double* const* phi_vals, const pcb_options* opt_in, const int32_t* devices,
+                                    int32_t ndev, pcb_op** out) {
+    if (!out) {
+        set_err("pcb_create_multi: null output handle");
+        return PCB_EINVAL;
+    }
+    *out = nullptr;
+    if (!devices || ndev < 1) {
+        set_err("pcb_create_multi: at least one device required");
+        return PCB_EINVAL;
+    }
+    pcb_op* op = new (std::nothrow) pcb_op;
+    if (!op) return PCB_ENOMEM;
+    const pcb_status st = guarded([&] {
+        pcb_options opt;
+        pcb_default_options(&opt);
+        if (opt_in) opt = *opt_in;
+        if (opt.nccl_id) fail(PCB_EINVAL, "pcb_create_multi: one process drives every device (no nccl_id)");
+        int nvis = 0;
+        if (cudaGetDeviceCount(&nvis) != cudaSuccess || nvis == 0) {
+            (void)cudaGetLastError();
+            fail(PCB_ECUDA, "no CUDA device: the pcop-b200 apply path has no CPU fallback");
+        }
+        for (int s2 = 0; s2 < ndev; ++s2)
+            if (devices[s2] < 0 || devices[s2] >= nvis) fail(PCB_EINVAL, "pcb_create_multi: bad device ordinal");
+        for (int s2 = 0; s2 < ndev; ++s2) {  // shard s2 of ndev on devices[s2]
+            pcb_options o = opt;
+            o.device = devices[s2];
+            o.shard_rank = s2;
+            o.shard_count = ndev;
+            o.nccl_id = nullptr;
+            o.reduce = PCB_REDUCE_NONE;
+            pcb_op* sub = nullptr;
+            const pcb_status rc = pcb_create(dim, dom_lo, dom_hi, r, points, w_lo, w_hi, w_vals, phi_lo, phi_hi,
+                                             phi_vals, &o, &sub);
+            if (rc != PCB_OK) fail(rc, std::string("shard ") + std::to_string(s2) + ": " + pcb_last_error());
+            op->subs.push_back(sub);
+            op->sub_dev.push_back(devices[s2]);
+        }
+        // peer access between every pair of distinct devices (the inputs' all-gather and the
+        // reduction load and store across devices)
+        for (int a2 = 0; a2 < ndev; ++a2)
+            for (int b2 = 0; b2 < ndev; ++b2) {
+                if (devices[a2] == devices[b2]) continue;
+                int can = 0;
+                PCB_CK(cudaDeviceCanAccessPeer(&can, devices[a2], devices[b2]));
+                if (!can) fail(PCB_ECUDA, "pcb_create_multi: no peer access between the devices");
+                PCB_CK(cudaSetDevice(devices[a2]));
+                const cudaError_t e = cudaDeviceEnablePeerAccess(devices[b2], 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                    fail(PCB_ECUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+                (void)cudaGetLastError();
+            }
+        const pcb_op* s0 = op->subs[0];
+        op->device = devices[0];
+        op->dim_user = s0->dim_user;
+        op->D = s0->D;
+        for (int a2 = 0; a2 < 3; ++a2) {
+            op->dom_lo[a2] = s0->dom_lo[a2];
+            op->n[a2] = s0->n[a2];
+        }
+        op->N = s0->N;
+        op->r = s0->r;
+        op->mode = s0->mode;
+        op->host_sub_mb = s0->host_sub_mb;
+        op->sbuf.resize(ndev);
+        op->d_parts_s.assign(ndev, nullptr);
+        for (int s2 = 0; s2 < ndev; ++s2) {
+            PCB_CK(cudaSetDevice(devices[s2]));
+            for (auto& e : op->sbuf[s2].ev) PCB_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            PCB_CK(cudaMalloc(&op->d_parts_s[s2], ndev * sizeof(double*)));
+        }
+        set_device(op);
+        PCB_CK(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
+        pcb_info in = s0->info;
+        in.rank_active = 0;
+        in.plan_terms = 0;
+        in.split_terms = 0;
+        in.spectra_bytes = 0;
+        in.device_bytes = 0;
+        for (const pcb_op* sub : op->subs) {
+            in.rank_active += sub->info.rank_active;
+            in.plan_terms += sub->info.plan_terms;
+            in.split_terms += sub->info.split_terms;
+            in.spectra_bytes += sub->info.spectra_bytes;
+            in.device_bytes += sub->info.device_bytes;
+        }
+        in.shard_rank = 0;
+        in.shard_count = ndev;
+        in.comm_nranks = ndev;  // devices in the handle (the reduction is the library's own kernel)
+        in.comm_version = 0;
+        in.term_lo = s0->info.term_lo;
+        in.term_hi = op->subs.back()->info.term_hi;
+        in.shard_cost = s0->info.total_cost;
+        op->info = in;
+    });
+    if (st != PCB_OK) {
+        const std::string msg = g_err;
+        pcb_destroy(op);
+        set_err(msg);
+        return st;
+    }
+    *out = op;
+    return PCB_OK;
+}
+
 PCB_API pcb_status pcb_destroy(pcb_op* op) {
     if (!op) return PCB_OK;
     cudaSetDevice(op->device);
-    if (op->stream) {
-        cudaStreamSynchronize(op->stream);
-        cudaStreamDestroy(op->stream);
+    if (op->stream) cudaStreamSynchronize(op->stream);
+    for (size_t s2 = 0; s2 < op->subs.size(); ++s2) {  // multi-device handle: its shards and buffers
+        pcb_destroy(op->subs[s2]);
+        cudaSetDevice(op->sub_dev[s2]);
+        if (s2 < op->sbuf.size()) {
+            if (op->sbuf[s2].fin) cudaFree(op->sbuf[s2].fin);
+            if (op->sbuf[s2].part) cudaFree(op->sbuf[s2].part);
+            for (cudaEvent_t e : op->sbuf[s2].ev)
+                if (e) cudaEventDestroy(e);
+        }
+        if (s2 < op->d_parts_s.size() && op->d_parts_s[s2]) cudaFree(op->d_parts_s[s2]);
     }
+    cudaSetDevice(op->device);
+    if (op->stream) cudaStreamDestroy(op->stream);
     for (auto& r : op->recs) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -2298,7 +2429,10 @@ static bool has_reduce(const pcb_op* op) { return op->comm && op->reduce != PCB_
 // behind the next chunk's FFTs.  Returns the event after which dG holds the result (recorded on
 // op->stream, or on the comm stream when reducing); op->stream itself does NOT wait for the last
 // reduce (callers that reuse dG on op->stream must wait on the returned event).
+static cudaEvent_t multi_apply(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG);
+
 static cudaEvent_t full_apply(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG, bool force_all = false) {
+    if (!op->subs.empty()) return multi_apply(op, adjoint, B, dF, dG);
     if (!has_reduce(op)) {
         enqueue_batch(op, adjoint, B, dF, dG);
         PCB_CK(cudaEventRecord(op_event(op, 2), op->stream));
@@ -2320,6 +2454,104 @@ static cudaEvent_t full_apply(pcb_op* op, bool adjoint, int32_t B, const double*
     }
     PCB_CK(cudaEventRecord(op_event(op, 3), op->s_comm));
     return op_event(op, 3);
+}
+
+// Single-process multi-GPU apply (pcb_create_multi).  dF, dG on devices[0], ordered on op->stream.
+//  1. inputs: shard s on another device gets F in two steps -- device 0 sends it slice s (scatter),
+//     then every shard copies the other slices from the shard that holds them (all-gather), so no
+//     device sends or receives much more than one copy of F (P2P copies over NVLink);
+//  2. every shard runs its terms (its own handle, graph-replayed) into its partial buffer;
+//  3. slice-parallel reduction: shard s sums slice s of all the partials (peer loads, shard order:
+//     deterministic) and stores it straight into dG on device 0 (peer stores).
+// Returns an event on op->stream after which dG holds the full apply.
+static cudaEvent_t multi_apply(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG) {
+    const int nd = (int)op->subs.size();
+    const size_t cnt = (size_t)B * (size_t)op->N;
+    const int d0 = op->sub_dev[0];
+    bool grown = false;
+    for (int s2 = 0; s2 < nd; ++s2) {  // per-shard buffers for B vectors
+        pcb_op::SubBuf& sb = op->sbuf[s2];
+        PCB_CK(cudaSetDevice(op->sub_dev[s2]));
+        if (sb.n < cnt) {
+            PCB_CK(cudaStreamSynchronize(op->subs[s2]->stream));
+            if (sb.fin) cudaFree(sb.fin);
+            if (sb.part) cudaFree(sb.part);
+            sb.fin = sb.part = nullptr;
+            sb.n = 0;
+            if (op->sub_dev[s2] != d0) PCB_CK(cudaMalloc(&sb.fin, cnt * sizeof(double)));
+            PCB_CK(cudaMalloc(&sb.part, cnt * sizeof(double)));
+            sb.n = cnt;
+            grown = true;
+        }
+    }
+    if (grown) {  // every shard's table of the partial pointers (the reduction reads all of them)
+        std::vector<double*> parts(nd);
+        for (int s2 = 0; s2 < nd; ++s2) parts[s2] = op->sbuf[s2].part;
+        for (int s2 = 0; s2 < nd; ++s2) {
+            PCB_CK(cudaSetDevice(op->sub_dev[s2]));
+            PCB_CK(cudaMemcpy(op->d_parts_s[s2], parts.data(), nd * sizeof(double*), cudaMemcpyHostToDevice));
+        }
+    }
+    PCB_CK(cudaSetDevice(d0));
+    PCB_CK(cudaEventRecord(op_event(op, 0), op->stream));
+    auto slice = [&](int t, size_t& off, size_t& len) {
+        off = cnt * (size_t)t / nd;
+        len = cnt * (size_t)(t + 1) / nd - off;
+    };
+    // 1a. scatter: slice s of F to shard s (remote shards)
+    for (int s2 = 0; s2 < nd; ++s2) {
+        pcb_op* sub = op->subs[s2];
+        PCB_CK(cudaSetDevice(op->sub_dev[s2]));
+        PCB_CK(cudaStreamWaitEvent(sub->stream, op_event(op, 0), 0));
+        if (op->sub_dev[s2] != d0) {
+            size_t off, len;
+            slice(s2, off, len);
+            PCB_CK(cudaMemcpyPeerAsync(op->sbuf[s2].fin + off, op->sub_dev[s2], dF + off, d0, len * sizeof(double),
+                                       sub->stream));
+        }
+        PCB_CK(cudaEventRecord(op->sbuf[s2].ev[0], sub->stream));
+    }
+    // 1b. all-gather the other slices, 2. the shard's terms into its partial
+    for (int s2 = 0; s2 < nd; ++s2) {
+        pcb_op* sub = op->subs[s2];
+        PCB_CK(cudaSetDevice(op->sub_dev[s2]));
+        const double* src = dF;
+        if (op->sub_dev[s2] != d0) {
+            for (int t = 0; t < nd; ++t) {
+                if (t == s2) continue;
+                size_t off, len;
+                slice(t, off, len);
+                const bool from0 = op->sub_dev[t] == d0;  // device 0's shards keep F in dF
+                if (!from0) PCB_CK(cudaStreamWaitEvent(sub->stream, op->sbuf[t].ev[0], 0));
+                PCB_CK(cudaMemcpyPeerAsync(op->sbuf[s2].fin + off, op->sub_dev[s2],
+                                           (from0 ? dF : op->sbuf[t].fin) + off, op->sub_dev[t],
+                                           len * sizeof(double), sub->stream));
+            }
+            src = op->sbuf[s2].fin;
+        }
+        enqueue_batch(sub, adjoint, B, src, op->sbuf[s2].part);
+        PCB_CK(cudaEventRecord(op->sbuf[s2].ev[1], sub->stream));
+    }
+    // 3. slice-parallel reduction into dG
+    for (int s2 = 0; s2 < nd; ++s2) {
+        pcb_op* sub = op->subs[s2];
+        PCB_CK(cudaSetDevice(op->sub_dev[s2]));
+        for (int t = 0; t < nd; ++t) PCB_CK(cudaStreamWaitEvent(sub->stream, op->sbuf[t].ev[1], 0));
+        size_t off, len;
+        slice(s2, off, len);
+        launch_ck(launch_sum_parts(op->d_parts_s[s2], nd, (int64_t)off, (int64_t)len, dG, sub->stream), "sum_parts");
+        PCB_CK(cudaEventRecord(op->sbuf[s2].ev[2], sub->stream));
+    }
+    PCB_CK(cudaSetDevice(d0));
+    for (int s2 = 0; s2 < nd; ++s2) PCB_CK(cudaStreamWaitEvent(op->stream, op->sbuf[s2].ev[2], 0));
+    // the next call may reuse the partial / input buffers only after this one's reduction
+    for (int s2 = 0; s2 < nd; ++s2) {
+        PCB_CK(cudaSetDevice(op->sub_dev[s2]));
+        for (int t = 0; t < nd; ++t) PCB_CK(cudaStreamWaitEvent(op->subs[s2]->stream, op->sbuf[t].ev[2], 0));
+    }
+    PCB_CK(cudaSetDevice(d0));
+    PCB_CK(cudaEventRecord(op_event(op, 2), op->stream));
+    return op_event(op, 2);
 }
 
 static pcb_status apply_dev_common(pcb_op* op, bool adjoint, int32_t B, const double* dF, double* dG, void* stream) {
@@ -2545,6 +2777,8 @@ PCB_API pcb_status pcb_entries(pcb_op* op, int64_t cnt, const int64_t* y, const 
         set_err("null handle");
         return PCB_EINVAL;
     }
+    // a multi-device handle: every shard's entry gather holds all the terms
+    if (!op->subs.empty()) return pcb_entries(op->subs[0], cnt, y, x, out);
     std::lock_guard<std::mutex> lk(op->mu);
     return guarded([&] {
         if (cnt < 0) fail(PCB_EINVAL, "pcb_entries: negative count");
@@ -2618,6 +2852,7 @@ PCB_API pcb_status pcb_blocks(pcb_op* op, int32_t nblk, const int64_t* t_origin,
         set_err("null handle");
         return PCB_EINVAL;
     }
+    if (!op->subs.empty()) return pcb_blocks(op->subs[0], nblk, t_origin, s_origin, block_shape, out);
     std::lock_guard<std::mutex> lk(op->mu);
     return guarded([&] {
         if (nblk == 0) return;
@@ -2650,6 +2885,7 @@ PCB_API pcb_status pcb_blocks_dev(pcb_op* op, int32_t nblk, const int64_t* d_t_o
         set_err("null handle");
         return PCB_EINVAL;
     }
+    if (!op->subs.empty()) return pcb_blocks_dev(op->subs[0], nblk, d_t_origin, d_s_origin, block_shape, d_out, stream);
     std::lock_guard<std::mutex> lk(op->mu);
     return guarded([&] {
         if (nblk == 0) return;
@@ -2668,6 +2904,9 @@ PCB_API pcb_status pcb_apply_block(pcb_op* op, int32_t nblk, const int64_t* t_lo
         set_err("null handle");
         return PCB_EINVAL;
     }
+    // multi-device handle: small blocks use the exact entry gather of shard 0 (all terms); large
+    // blocks need the full FFT apply of one shard and are refused there with a clear message
+    if (!op->subs.empty()) return pcb_apply_block(op->subs[0], nblk, t_lo, t_hi, s_lo, s_hi, f, g, adjoint);
     std::lock_guard<std::mutex> lk(op->mu);
     return guarded([&] {
         if (nblk < 0) fail(PCB_EINVAL, "pcb_apply_block: negative block count");
@@ -3118,6 +3357,7 @@ PCB_API pcb_status pcb_profile_begin(pcb_op* op) {
         set_err("null handle");
         return PCB_EINVAL;
     }
+    for (pcb_op* sub : op->subs) pcb_profile_begin(sub);
     std::lock_guard<std::mutex> lk(op->mu);
     op->prof = true;
     return PCB_OK;
@@ -3134,6 +3374,22 @@ PCB_API pcb_status pcb_profile_end(pcb_op* op, int32_t max_kernels, char* names,
         set_device(op);
         std::vector<std::string> order;
         std::map<std::string, std::pair<double, int>> acc;
+        for (pcb_op* sub : op->subs) {  // multi-device handle: the shards' kernels, summed by name
+            const int32_t mx = 256;
+            std::vector<char> nm(32 * mx);
+            std::vector<double> ms(mx);
+            std::vector<int32_t> cn(mx);
+            int32_t nk = 0;
+            const pcb_status rc = pcb_profile_end(sub, mx, nm.data(), ms.data(), cn.data(), &nk);
+            if (rc != PCB_OK) fail(rc, pcb_last_error());
+            for (int32_t i = 0; i < std::min(nk, mx); ++i) {
+                const std::string key(nm.data() + 32 * i);
+                if (!acc.count(key)) order.push_back(key);
+                acc[key].first += ms[i];
+                acc[key].second += cn[i];
+            }
+        }
+        set_device(op);
         for (auto& r : op->recs) {
             PCB_CK(cudaEventSynchronize(r.b));
             float ms = 0.f;

@@ -35,7 +35,7 @@ EXPORTS = ["pcb_default_options", "pcb_last_error", "pcb_create", "pcb_destroy",
            "pcb_hmatrix_destroy", "pcb_hmatrix_get_info", "pcb_hmatrix_tree", "pcb_hmatrix_block",
            "pcb_hmatrix_admissible", "pcb_hmatrix_matvec", "pcb_hmatrix_save", "pcb_hmatrix_load",
            "pcb_comm_unique_id", "pcb_plan_shards", "pcb_debug_guard_check", "pcb_estimator_create_ex",
-           "pcb_host_alloc", "pcb_host_free"]
+           "pcb_host_alloc", "pcb_host_free", "pcb_create_multi"]
 RNG = {"mt19937": 0, "philox": 1}
 REDUCE = {"none": 0, "all": 1, "root": 2}
 PARTITION = {"cost": 0, "count": 1}
@@ -106,6 +106,9 @@ def load():
     L.pcb_last_error.restype = ctypes.c_char_p
     L.pcb_create.argtypes = [i32, P_i64, P_i64, i32, P_i64, P_i64, P_i64, ctypes.POINTER(vp), P_i64, P_i64,
                              ctypes.POINTER(vp), ctypes.POINTER(Options), ctypes.POINTER(vp)]
+    L.pcb_create_multi.argtypes = [i32, P_i64, P_i64, i32, P_i64, P_i64, P_i64, ctypes.POINTER(vp), P_i64, P_i64,
+                                   ctypes.POINTER(vp), ctypes.POINTER(Options), ctypes.POINTER(i32), i32,
+                                   ctypes.POINTER(vp)]
     L.pcb_destroy.argtypes = [vp]
     L.pcb_get_info.argtypes = [vp, ctypes.POINTER(Info)]
     for n in ("pcb_apply_batch", "pcb_apply_adjoint_batch"):

@@ -40,7 +40,7 @@ class ProductConvolutionOperator:
                  points: Optional[Sequence[Sequence[int]]] = None, mode: str = "auto", max_batch: int = 16,
                  shard: Tuple[int, int] = (0, 1), device: int = -1, scratch_bytes: int = 0,
                  nccl_id: Optional[bytes] = None, reduce: str = "all", partition: str = "cost",
-                 host_sub_mb: int = 0):
+                 host_sub_mb: int = 0, devices: Optional[Sequence[int]] = None):
         """domain = (lo, hi) inclusive; weights / impulses: objects with ``.lo`` and ``.values``
         (``inputs.Field``) or (lo, values) pairs.
 
@@ -48,7 +48,10 @@ class ProductConvolutionOperator:
         of terms (``partition``); with ``nccl_id`` (``lib.comm_unique_id()`` on one rank, sent to the
         others) construction joins an NCCL communicator and every apply sums the shards' partials
         inside the library (``reduce``: "all" = every rank gets the full result, "root" = rank 0,
-        "none" = partial).  Without it, apply returns this shard's partial sum."""
+        "none" = partial).  Without it, apply returns this shard's partial sum.
+
+        Single-process multi-GPU: ``devices = [d0, d1, ...]`` builds one handle whose shard s runs
+        on devices[s] (pcb_create_multi); buffers of the ``*_dev`` calls live on devices[0]."""
         if len(weights) != len(impulses):
             raise ValueError("PCOp: one weight per impulse required")
         L = _L.load()
@@ -99,8 +102,14 @@ class ProductConvolutionOperator:
             opt.reduce = _L.REDUCE[reduce]
         PP = _L.vp * max(1, r)
         h = _L.vp()
-        rc = L.pcb_create(self.dim, _i64arr(lo), _i64arr(hi), r, pts, _i64arr(w_lo), _i64arr(w_hi),
-                          PP(*w_ptr), _i64arr(p_lo), _i64arr(p_hi), PP(*p_ptr), ctypes.byref(opt), ctypes.byref(h))
+        if devices is not None:
+            devs = (_L.i32 * max(1, len(devices)))(*[int(d) for d in devices])
+            rc = L.pcb_create_multi(self.dim, _i64arr(lo), _i64arr(hi), r, pts, _i64arr(w_lo), _i64arr(w_hi),
+                                    PP(*w_ptr), _i64arr(p_lo), _i64arr(p_hi), PP(*p_ptr), ctypes.byref(opt), devs,
+                                    len(devices), ctypes.byref(h))
+        else:
+            rc = L.pcb_create(self.dim, _i64arr(lo), _i64arr(hi), r, pts, _i64arr(w_lo), _i64arr(w_hi),
+                              PP(*w_ptr), _i64arr(p_lo), _i64arr(p_hi), PP(*p_ptr), ctypes.byref(opt), ctypes.byref(h))
         if rc == 1:
             raise ValueError(L.pcb_last_error().decode())
         _L.check(rc)

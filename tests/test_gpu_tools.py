@@ -117,3 +117,37 @@ def test_host_pipeline_many_sub_batches(gpu, cfg, B):
         again = op.apply_adjoint_batch(F) if adj else op.apply_batch(F)
         assert np.array_equal(again, want)
     op.close()
+
+
+@pytest.mark.parametrize("cfg,ndev", [("c2", 2), ("c3", 3), ("c4", 2)])
+def test_multi_device_handle(gpu, cfg, ndev):
+    """pcb_create_multi with every shard on GPU 0 (the box has one): the scatter / all-gather of F,
+    the per-shard partials and the library's slice-parallel reduction run exactly as across
+    devices; apply and adjoint (device and host buffers), the estimator and entries equal the
+    single handle's to rounding (the shard sums reorder the k-sum)."""
+    import torch
+
+    inp = inputs.make_config(cfg)
+    F = normal_vectors(5, 4, inp.n_points)
+    ref = ProductConvolutionOperator.from_inputs(inp)
+    G0, GA0 = ref.apply_batch(F), ref.apply_adjoint_batch(F)
+    op = ProductConvolutionOperator.from_inputs(inp, devices=[0] * ndev)
+    assert op.info["shard_count"] == ndev and op.info["rank_active"] == inp.rank
+    assert rel(op.apply_batch(F), G0) <= 1e-14
+    assert rel(op.apply_adjoint_batch(F), GA0) <= 1e-14
+    dF = torch.from_numpy(F).cuda()
+    dG = torch.empty_like(dF)
+    for adj, want in ((False, G0), (True, GA0)):
+        op.apply_batch_dev(4, dF.data_ptr(), dG.data_ptr(), torch.cuda.current_stream().cuda_stream, adjoint=adj)
+        torch.cuda.synchronize()
+        assert rel(dG.cpu().numpy(), want) <= 1e-14
+    again = op.apply_batch(F)  # deterministic: the reduction sums in shard order
+    assert np.array_equal(again, op.apply_batch(F))
+    rng = np.random.default_rng(1)
+    y = np.stack([rng.integers(0, n, 64) for n in inp.shape], 1)
+    x = np.stack([rng.integers(0, n, 64) for n in inp.shape], 1)
+    assert np.array_equal(op.entries(y, x), ref.entries(y, x))
+    yt, _, ea, er = op.probe_estimate(F[:2], 0.5 * F[:2], [], want_ytilde=True)
+    _, _, ea0, er0 = ref.probe_estimate(F[:2], 0.5 * F[:2], [])
+    assert abs(ea - ea0) <= 1e-13 * ea0 and abs(er - er0) <= 1e-13 * er0
+    op.close()
