@@ -60,6 +60,14 @@ def main():
             op.probe_estimate(Z, Z * 0.5, [(lo, hi)])
             guards_ok(f"{name}/{mode}")
             op.close()
+    # the single-process multi-device handle (every shard on GPU 0): partials + reduction kernel
+    inp = inputs.make_config("c2")
+    op = ProductConvolutionOperator.from_inputs(inp, devices=[0, 0, 0])
+    F = normal_vectors(4, 3, inp.n_points)
+    op.apply_batch(F)
+    op.apply_adjoint_batch(F)
+    guards_ok("c2/multi")
+    op.close()
     # config 5: the tiled dense-block gather and its zero-block path, all 4096 blocks
     from headline_common import c5_origins
 
