@@ -52,6 +52,9 @@
 #ifndef PCB_RINV_ALIAS
 #define PCB_RINV_ALIAS 1  // per-entry gather: split straight into registers, stage doubles as FFT buffer
 #endif
+#ifndef PCB_BUNDLE_TWREC
+#define PCB_BUNDLE_TWREC 1  // bundled gather: member phases from phase(tl) and powers of phase(TPL)
+#endif
 #ifndef PCB_BUNDLE_ALIAS
 #define PCB_BUNDLE_ALIAS 1  // with XPF: stage buffer 1 doubles as the FFT / xs buffer (smem per CTA)
 #endif
@@ -859,12 +862,31 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
                     const int dl = mb[m0 + j].delta;
                     // the phase of bin N - k is (-1)^dl conj(phase of bin k) (P = 2N): one table load per pair
                     const double sn = (dl & 1) ? -1.0 : 1.0;
+#if PCB_BUNDLE_TWREC
+                    // k = tl + r TPL: phase(k) = phase(tl) u^r, u = phase(TPL); u^r from u, u^2, u^4 (<= 3
+                    // products): 1 + log2(R) table loads per member instead of R
+                    constexpr int LR = R >= 16 ? 4 : R >= 8 ? 3 : R >= 4 ? 2 : 1;
+                    double2 up[LR];
+                    double2 w0 = make_double2(1.0, 0.0);
+                    if (dl != 0) {
+                        w0 = __ldg(&twP[(tl * dl) % P]);
+#pragma unroll
+                        for (int bit = 0; bit < LR; ++bit) up[bit] = __ldg(&twP[(((1 << bit) * TPL) * dl) % P]);
+                    }
+#endif
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int k = tl + r * TPL;
                         double2 xk = x[k], xn = x[N - k];
                         if (dl != 0) {
+#if PCB_BUNDLE_TWREC
+                            double2 w = w0;
+#pragma unroll
+                            for (int bit = 0; bit < LR; ++bit)
+                                if (r & (1 << bit)) w = cmul(w, up[bit]);
+#else
                             const double2 w = __ldg(&twP[(k * dl) % P]);
+#endif
                             xk = cmul(xk, w);
                             xn = cmul(xn, make_double2(sn * w.x, -sn * w.y));
                         }
@@ -965,12 +987,31 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
                     const int dl = mb[m0 + j].delta;
                     // the phase of bin N - k is (-1)^dl conj(phase of bin k) (P = 2N): one table load per pair
                     const double sn = (dl & 1) ? -1.0 : 1.0;
+#if PCB_BUNDLE_TWREC
+                    // k = tl + r TPL: phase(k) = phase(tl) u^r, u = phase(TPL); u^r from u, u^2, u^4 (<= 3
+                    // products): 1 + log2(R) table loads per member instead of R
+                    constexpr int LR = R >= 16 ? 4 : R >= 8 ? 3 : R >= 4 ? 2 : 1;
+                    double2 up[LR];
+                    double2 w0 = make_double2(1.0, 0.0);
+                    if (dl != 0) {
+                        w0 = __ldg(&twP[(tl * dl) % P]);
+#pragma unroll
+                        for (int bit = 0; bit < LR; ++bit) up[bit] = __ldg(&twP[(((1 << bit) * TPL) * dl) % P]);
+                    }
+#endif
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int k = tl + r * TPL;
                         double2 xk = x[k], xn = x[N - k];
                         if (dl != 0) {
+#if PCB_BUNDLE_TWREC
+                            double2 w = w0;
+#pragma unroll
+                            for (int bit = 0; bit < LR; ++bit)
+                                if (r & (1 << bit)) w = cmul(w, up[bit]);
+#else
                             const double2 w = __ldg(&twP[(k * dl) % P]);
+#endif
                             xk = cmul(xk, w);
                             xn = cmul(xn, make_double2(sn * w.x, -sn * w.y));
                         }

@@ -11,7 +11,7 @@ for cfg in ${CFGS:-c3}; do
 import json
 d = json.load(open("gpurun_out/ab_${cfg}_$tag.json"))
 r = d["roofline"]
-print("$cfg", "$tag", round(d["value"]), round(d["e2e"]["value"]), round(d["ms_per_step"], 3), r["kernel"], round(r["kernel_ms_per_step"], 3), round(r["frac"], 3))
+print("$cfg", "$tag", round(d["value"]), round(d["e2e"]["value"]), round(d["ms_per_step"], 3), r["kernel"], round(r["kernel_ms_per_step"], 3), round(r["frac"], 3), {k: round(v, 3) for k, v in d["kernels_ms_per_step"].items()})
 PY
   done
 done
