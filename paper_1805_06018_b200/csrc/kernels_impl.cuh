@@ -79,6 +79,18 @@
 #ifndef PCB_COLS_THREADS
 #define PCB_COLS_THREADS 64
 #endif
+#ifndef PCB_SPLIT3_MIN
+// Last-axis half lengths N = 3 * 2^a >= this run as F = 3 interleaved power-of-two sub-lines of
+// M = N / 3 points on the 8-element engine (64-register row kernels), with the radix-3 butterfly
+// folded into the passes that touch the data anyway: the forward gather (decimation in frequency:
+// sub-line s gets y_s[j] = w_N^{sj} sum_t w_3^{st} z[j + tM], and FFT_M(y_s)[k] = Z[3k + s]) and the
+// inverse's output pass (decimation in time: z[j + tM] = sum_s w_3^{-st} w_N^{-sj} IFFT_M(Z[3. + s])[j]).
+// 0: the generic 24-element 3-smooth engine for every 3-smooth length.
+#define PCB_SPLIT3_MIN 96
+#endif
+#ifndef PCB_ROWS_THREADS_S3
+#define PCB_ROWS_THREADS_S3 96  // threads per CTA of the split-3 row kernels (3 sub-lines per line)
+#endif
 #ifndef PCB_COLS_MINB
 #define PCB_COLS_MINB 1
 #endif
@@ -94,16 +106,36 @@ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
 template <int NL>
 constexpr int PSH = ilog2c(NL) > 3 ? ilog2c(NL) : 3;
 
+// Row-pass engine of half length N: F sub-lines of M = N / F points per line (F = 1: the line itself).
+template <int N>
+struct RowCfg {
+    static constexpr bool S3 = PCB_SPLIT3_MIN > 0 && N >= PCB_SPLIT3_MIN && N % 3 == 0 && is_pow2c(N / 3);
+    static constexpr int F = S3 ? 3 : 1;
+    static constexpr int M = N / F;
+    static constexpr int TPL = FftCfg<M>::TPL;  // threads per sub-line
+    static constexpr int R = FftCfg<M>::R;      // elements per thread
+    static constexpr bool P2 = FftCfg<M>::P2;   // power-of-two engine: the 64-register launch shape
+    static constexpr int THREADS = S3 ? PCB_ROWS_THREADS_S3 : PCB_ROWS_THREADS;
+    // min CTAs/SM scaled to the CTA size (mb is stated for 64-thread CTAs)
+    static constexpr int minb(int nl, int mb) {
+        const int nt = nl * F * TPL;
+        const int v = nt <= 64 ? mb : mb * 64 / nt;
+        return v < 1 ? 1 : v;
+    }
+};
+
 // bundled gather (aliased layout): staged-line stride, >= N + 1 and large enough that one stage
 // buffer (NL lines) holds the FFT exchange buffer and the real output lines xs
 template <int N, int NL>
 __host__ __device__ constexpr int stage_stride_b() {
-    constexpr int words = SmemLine<N, NL, PSH<NL>>::WORDS;
+    constexpr int words = SmemLine<RowCfg<N>::M, RowCfg<N>::F * NL, PSH<RowCfg<N>::F * NL>>::WORDS;
     constexpr int xsw = (NL * (2 * N + 1) + 1) / 2;
     constexpr int need = words > xsw ? words : xsw;
     constexpr int base = (N + 1) * NL >= need ? N + 1 : (need + NL - 1) / NL;
     // lanes l of a 128-bit quarter-warp read x[l * stride + k] for 8 / NL consecutive k: with
     // stride = 8 / NL (mod 8) they fall in distinct bank groups (also for x[N - k])
+    // (split-3 lines: threads are ordered (tl, s, l) with l fastest and own the bins 3 tl + s + ..., so
+    // the same rule holds)
     constexpr int q = NL >= 8 ? 1 : 8 / NL;
     return PCB_SLS_CF ? base + ((q - base % 8) % 8 + 8) % 8 : base;
 }
@@ -117,6 +149,35 @@ __device__ __forceinline__ const double2* twtab(const double2* tw) {
 template <int LEN, int NL>
 constexpr int smem_words() {
     return SmemLine<LEN, NL, PSH<NL>>::WORDS;
+}
+// FFT exchange buffer of a row-pass CTA: F * NL interleaved sub-lines of M points
+template <int N, int NL>
+constexpr int row_words() {
+    return SmemLine<RowCfg<N>::M, RowCfg<N>::F * NL, PSH<RowCfg<N>::F * NL>>::WORDS;
+}
+// split-3 inverse, last step (decimation in time), in place on the real output lines xs: the
+// sub-line results y_s[j] sit at complex position s M + j of line ll; (z[j], z[j + M], z[j + 2M]) =
+// DFT3^{-1}(y_0[j], conj(w_N^j) y_1[j], conj(w_N^{2j}) y_2[j]).  One thread per (line, j): no hazards.
+template <int N, int NT, int XS>
+__device__ __forceinline__ void split3_time_pass(double* xs, int nlines, const double2* __restrict__ twN) {
+    constexpr int M = N / 3;
+    for (int idx = threadIdx.x; idx < nlines * M; idx += NT) {
+        const int ll = idx / M;
+        const int j = idx - ll * M;
+        double* x = xs + ll * XS + 2 * j;
+        double2 u0 = make_double2(x[0], x[1]);
+        double2 u1 = make_double2(x[2 * M], x[2 * M + 1]);
+        double2 u2 = make_double2(x[4 * M], x[4 * M + 1]);
+        u1 = cmulc(u1, __ldg(&twN[j]));
+        u2 = cmulc(u2, __ldg(&twN[2 * j]));
+        dft3<+1>(u0, u1, u2);
+        x[0] = u0.x;
+        x[1] = u0.y;
+        x[2 * M] = u1.x;
+        x[2 * M + 1] = u1.y;
+        x[4 * M] = u2.x;
+        x[4 * M + 1] = u2.y;
+    }
 }
 
 // pad shift of the column pass: with 4 lines per tile its first forward and first inverse stages
@@ -162,14 +223,16 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // w_k . f on the footprint window, ADJ gathers g on the output window (both
 // staged through shared memory with cp.async), SPEC places the trimmed kernel.
 template <int N, int NL, int MODE>
-__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_MINB : (N <= 48 ? PCB_ROWS_MINB_SHORT3 : PCB_ROWS_MINB_MIXED)) k_rows_fwd(PassArgs a) {
-    constexpr int R = FftCfg<N>::R;
-    constexpr int RF = FirstPos<N>::RF;
-    constexpr int NT = NL * FftCfg<N>::TPL;
-    constexpr int PS = PSH<NL>;
+__global__ void __launch_bounds__(NL * RowCfg<N>::F * RowCfg<N>::TPL, RowCfg<N>::P2 ? RowCfg<N>::minb(NL, PCB_ROWS_MINB) : (N <= 48 ? PCB_ROWS_MINB_SHORT3 : PCB_ROWS_MINB_MIXED)) k_rows_fwd(PassArgs a) {
+    using RC = RowCfg<N>;
+    constexpr int F = RC::F, M = RC::M, NLS = F * NL;  // NLS interleaved sub-lines of M points
+    constexpr int R = RC::R;
+    constexpr int RF = FirstPos<M>::RF;
+    constexpr int NT = NLS * RC::TPL;
+    constexpr int PS = PSH<NLS>;
     extern __shared__ double2 buf[];
-    // layout: buf [smem_words] | line meta
-    int64_t* m_src = reinterpret_cast<int64_t*>(buf + smem_words<N, NL>());
+    // layout: buf [row_words] | line meta
+    int64_t* m_src = reinterpret_cast<int64_t*>(buf + row_words<N, NL>());
     int64_t* m_row = m_src + NL;
     int64_t* m_w = m_row + NL;
     int* m_lo = reinterpret_cast<int*>(m_w + NL);  // valid positions [m_lo, m_hi) along the line
@@ -237,44 +300,86 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
     __syncthreads();
 
     // phase 1: z[j] = (x[2j], x[2j+1]) gathered straight into the first-stage registers
-    const int l = threadIdx.x % NL;
-    const int tl = threadIdx.x / NL;
+    // thread (sub-line sl = s * NL + l, tl): sub-line s of line l (F = 1: the line itself)
+    const int sl = threadIdx.x % NLS;
+    const int s = sl / NL;
+    const int l = sl - s * NL;
+    const int tl = threadIdx.x / NLS;
     double2 v[R];
     {
         const int lo = m_lo[l], hi = m_hi[l];
         const int64_t src = m_src[l];
         const int64_t wsrc = m_w[l];
+        auto load_z = [&](int p) {  // z[p] = (x[2p], x[2p+1]) of line l, zero outside [lo, hi)
+            double xv[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int u = 2 * p + h;
+                double x = 0.0;
+                if (u >= lo && u < hi) {
+                    if (MODE == RF_APPLY) x = __ldg(&a.in[src + u]) * __ldg(&a.w_pool[wsrc + u]);
+                    else if (MODE == RF_ADJ) x = __ldg(&a.in[src + u]);
+                    else {
+                        const int64_t zl = imod(u + td.s[ax] - td.x_lo[ax] - td.k_lo[ax], a.P[ax]);
+                        if (zl < td.k_ext[ax]) x = a.phi_pool[src + zl];
+                    }
+                }
+                xv[h] = x;
+            }
+            return make_double2(xv[0], xv[1]);
+        };
+        // split-3: output s of the radix-3 butterfly over (z[p], z[p + M], z[p + 2M]), times w_N^{s p}.
+        // The three sub-line threads of a line read the same inputs, so the lines are staged once in
+        // shared memory (stride N + 1: the NL lines fall in distinct bank groups; the FFT buffer is
+        // free until the first stage's store, which follows a barrier)
+        if constexpr (F == 3) {
+            static_assert(NL * (N + 1) <= row_words<N, NL>(), "staged input lines exceed the FFT buffer");
+            double* xin = reinterpret_cast<double*>(buf);
+            for (int idx = threadIdx.x; idx < NL * 2 * N; idx += NT) {
+                const int ll = idx / (2 * N);
+                const int u = idx - ll * 2 * N;
+                double x = 0.0;
+                if (u >= m_lo[ll] && u < m_hi[ll]) {
+                    if (MODE == RF_APPLY) x = __ldg(&a.in[m_src[ll] + u]) * __ldg(&a.w_pool[m_w[ll] + u]);
+                    else if (MODE == RF_ADJ) x = __ldg(&a.in[m_src[ll] + u]);
+                    else {
+                        const int64_t zl = imod(u + td.s[ax] - td.x_lo[ax] - td.k_lo[ax], a.P[ax]);
+                        if (zl < td.k_ext[ax]) x = a.phi_pool[m_src[ll] + zl];
+                    }
+                }
+                xin[ll * 2 * (N + 1) + u] = x;
+            }
+            __syncthreads();
+        }
+        const double c3 = s == 0 ? 0.0 : s == 1 ? 0.86602540378443864676 : -0.86602540378443864676;
+        const double h3 = s == 0 ? 1.0 : -0.5;
+        const double2* twN = twtab<N>(a.tw);
 #pragma unroll
         for (int b = 0; b < R / RF; ++b)
 #pragma unroll
             for (int r = 0; r < RF; ++r) {
-                const int p = FirstPos<N>::pos(tl, b, r);
-                double xv[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int u = 2 * p + h;
-                    double x = 0.0;
-                    if (u >= lo && u < hi) {
-                        if (MODE == RF_APPLY) x = __ldg(&a.in[src + u]) * __ldg(&a.w_pool[wsrc + u]);
-                        else if (MODE == RF_ADJ) x = __ldg(&a.in[src + u]);
-                        else {
-                            const int64_t zl = imod(u + td.s[ax] - td.x_lo[ax] - td.k_lo[ax], a.P[ax]);
-                            if (zl < td.k_ext[ax]) x = a.phi_pool[src + zl];
-                        }
-                    }
-                    xv[h] = x;
+                const int p = FirstPos<M>::pos(tl, b, r);
+                if constexpr (F == 1) {
+                    v[b * RF + r] = load_z(p);
+                } else {
+                    const double2* zin = buf + l * (N + 1);
+                    const double2 z0 = zin[p], z1 = zin[p + M], z2 = zin[p + 2 * M];
+                    const double2 t1 = cadd(z1, z2), t2 = csub(z1, z2);
+                    const double2 y = make_double2(fma(c3, t2.y, fma(h3, t1.x, z0.x)), fma(-c3, t2.x, fma(h3, t1.y, z0.y)));
+                    v[b * RF + r] = s == 0 ? y : cmul(y, __ldg(&twN[s * p]));
                 }
-                v[b * RF + r] = make_double2(xv[0], xv[1]);
             }
     }
-    fft_fwd_order<N, -1, NL, PS>(v, buf, l, tl, twtab<N>(a.tw));
+    fft_fwd_order<M, -1, NLS, PS>(v, buf, sl, tl, twtab<M>(a.tw));
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int pos = mid_pos<N>(tl, r);
-        buf[sidx<NL, PS>(pos, l)] = v[r];
+        const int pos = mid_pos<M>(tl, r);
+        buf[sidx<NLS, PS>(pos, sl)] = v[r];
     }
     __syncthreads();
+    // Z[k] of line ll: element k / F of its sub-line k % F
+    auto zat = [&](int k, int ll) { return buf[sidx<NLS, PS>(k / F, (k % F) * NL + ll)]; };
 
     // phase 3: even/odd split X[k] = A[k] + W^k B[k], k = 0..N
     const double2* twP = twtab<2 * N>(a.tw);
@@ -287,8 +392,8 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
         const int k = idx - ll * NH;
         const int64_t row = m_row[ll];
         if (row < 0) continue;
-        const double2 zk = buf[sidx<NL, PS>(k, ll)];
-        const double2 zn = buf[sidx<NL, PS>(k == 0 ? 0 : N - k, ll)];
+        const double2 zk = zat(k, ll);
+        const double2 zn = zat(k == 0 ? 0 : N - k, ll);
         const double2 A = make_double2(0.5 * (zk.x + zn.x), 0.5 * (zk.y - zn.y));
         const double2 Bm = make_double2(0.5 * (zk.y + zn.y), -0.5 * (zk.x - zn.x));  // (zk - conj zn)/(2i)
         const double2 wk = __ldg(&twP[k]);
@@ -641,13 +746,15 @@ __global__ void PCB_COLS_BOUNDS(P0, NL) k_cols(PassArgs a) {
 // output positions p = t mod blockDim, so contributions to one position are
 // added by one thread in ascending entry order (deterministic, no atomics).
 template <int N, int NL, int MODE>
-__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_MINB : (N <= 48 ? PCB_ROWS_MINB_SHORT3 : PCB_ROWS_MINB_MIXED)) k_rows_inv(PassArgs a) {
-    constexpr int R = FftCfg<N>::R;
-    constexpr int RL = LastPos<N>::RL;
-    constexpr int NT = NL * FftCfg<N>::TPL;
+__global__ void __launch_bounds__(NL * RowCfg<N>::F * RowCfg<N>::TPL, RowCfg<N>::P2 ? RowCfg<N>::minb(NL, PCB_ROWS_MINB) : (N <= 48 ? PCB_ROWS_MINB_SHORT3 : PCB_ROWS_MINB_MIXED)) k_rows_inv(PassArgs a) {
+    using RC = RowCfg<N>;
+    constexpr int F = RC::F, M = RC::M, NLS = F * NL;  // NLS interleaved sub-lines of M points
+    constexpr int R = RC::R;
+    constexpr int RL = LastPos<M>::RL;
+    constexpr int NT = NLS * RC::TPL;
     constexpr int XS = 2 * N + 1;  // padded real line stride: conflict-free column writes
-    constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
-                                                                          : (NL * (2 * N + 1) + 1) / 2;
+    constexpr int BUFW = row_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? row_words<N, NL>()
+                                                                        : (NL * (2 * N + 1) + 1) / 2;
     extern __shared__ double2 buf[];
     const int64_t aline = blockIdx.x;
     const int vec = blockIdx.y;
@@ -674,8 +781,10 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
     const int64_t e_beg = a.line_ptr[aline];
     const int64_t e_end = a.line_ptr[aline + 1];
     const double2* twP = twtab<2 * N>(a.tw);
-    const int l = threadIdx.x % NL;
-    const int tl = threadIdx.x / NL;
+    const int sl = threadIdx.x % NLS;  // sub-line s of staged line l (F = 1: the line itself)
+    const int s = sl / NL;
+    const int l = sl - s * NL;
+    const int tl = threadIdx.x / NLS;
     for (int i = ulo + threadIdx.x; i < uhi; i += NT) acc[i - ulo] = 0.0;
 
     for (int64_t e0 = e_beg; e0 < e_end; e0 += NL) {
@@ -693,8 +802,8 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
         double2 v[R];
 #if PCB_RINV_ALIAS
 #pragma unroll
-        for (int r = 0; r < R; ++r) {  // z[k], k = mid_pos(tl, r), of line l: the FFT's input registers
-            const int k = mid_pos<N>(tl, r);
+        for (int r = 0; r < R; ++r) {  // z[k], k = F mid_pos(tl, r) + s, of line l: the FFT's input registers
+            const int k = F * mid_pos<M>(tl, r) + s;
             double2 z = czero();
             if (l < ne) {
                 const double2 xk = stage[l * SLS + k];
@@ -720,6 +829,7 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
                 const double2 O = cmulc(Dd, __ldg(&twP[k]));                // * exp(+2 pi i k / P)
                 z = make_double2(E.x - O.y, E.y + O.x);                     // E + i O
             }
+            static_assert(F == 1, "the unaliased per-entry gather has no split-3 path");
             buf[sidx<NL, PSH<NL>>(k, ll)] = z;
         }
         __syncthreads();
@@ -729,17 +839,21 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
             v[r] = buf[sidx<NL, PSH<NL>>(pos, l)];
         }
 #endif
-        fft_rev_order<N, +1, NL, PSH<NL>>(v, fbuf, l, tl, twtab<N>(a.tw));
+        fft_rev_order<M, +1, NLS, PSH<NLS>>(v, fbuf, sl, tl, twtab<M>(a.tw));
         __syncthreads();
 #pragma unroll
         for (int bb = 0; bb < R / RL; ++bb)
 #pragma unroll
             for (int r = 0; r < RL; ++r) {
-                const int p = LastPos<N>::pos(tl, bb, r);
+                const int p = s * M + LastPos<M>::pos(tl, bb, r);
                 xs[l * XS + 2 * p] = v[bb * RL + r].x;
                 xs[l * XS + 2 * p + 1] = v[bb * RL + r].y;
             }
         __syncthreads();
+        if constexpr (F == 3) {
+            split3_time_pass<N, NT, XS>(xs, ne, twtab<N>(a.tw));
+            __syncthreads();
+        }
         for (int ll = 0; ll < ne; ++ll) {
             const int lo = meta[ll].lo, hi = meta[ll].hi;
             const double* x = xs + ll * XS - meta[ll].sh;
@@ -768,15 +882,20 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
 // scaled by A_k(line) / prod P (no phase: one placement), summed, transformed once, and the
 // result multiplied by the family's last-axis weight row c (header w_off) as it accumulates.
 template <int N, int NL, int ADJ>
-__global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_MINB_B : (N <= 48 ? PCB_ROWS_MINB_SHORT3 : PCB_ROWS_MINB_MIXED))
+__global__ void __launch_bounds__(NL * RowCfg<N>::F * RowCfg<N>::TPL, RowCfg<N>::P2 ? RowCfg<N>::minb(NL, PCB_ROWS_MINB_B) : (N <= 48 ? PCB_ROWS_MINB_SHORT3 : PCB_ROWS_MINB_MIXED))
     k_rows_inv_b(PassArgs a) {
-    constexpr int R = FftCfg<N>::R;
-    constexpr int RL = LastPos<N>::RL;
-    constexpr int NT = NL * FftCfg<N>::TPL;
-    constexpr int TPL = FftCfg<N>::TPL;
+    using RC = RowCfg<N>;
+    // split-3 lengths: the lane's F sub-line thread groups own the bins k = F k' + s (k' the M-point
+    // inverse's input position), so each group's accumulators feed its sub-line transform directly
+    constexpr int F = RC::F, M = RC::M, NLS = F * NL;
+    constexpr int R = RC::R;
+    constexpr int RL = LastPos<M>::RL;
+    constexpr int NT = NLS * RC::TPL;
+    constexpr int TPL = RC::TPL;   // threads per sub-line
+    constexpr int TPLN = F * TPL;  // threads per lane (staging loops)
     constexpr int XS = 2 * N + 1;
-    constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
-                                                                          : (NL * (2 * N + 1) + 1) / 2;
+    constexpr int BUFW = row_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? row_words<N, NL>()
+                                                                        : (NL * (2 * N + 1) + 1) / 2;
     constexpr int P = 2 * N;
     constexpr int MB = PCB_BUNDLE_MB;
     constexpr int SL = N + 1;  // staged line length
@@ -806,8 +925,11 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
     const int64_t b_beg = a.line_ptr[aline];
     const int64_t b_end = a.line_ptr[aline + 1];
     const double2* twP = twtab<P>(a.tw);
-    const int l = threadIdx.x % NL;
-    const int tl = threadIdx.x / NL;
+    const int sl = threadIdx.x % NLS;  // sub-line s of lane l (F = 1: the lane itself)
+    const int s = sl / NL;
+    const int l = sl - s * NL;
+    const int tl = threadIdx.x / NLS;
+    const int tln = tl * F + s;  // thread index within the lane
     for (int i = ulo + threadIdx.x; i < uhi; i += NT) acc[i - ulo] = 0.0;
 
 #if PCB_BUNDLE_XPF
@@ -820,7 +942,7 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
             if (m0 + j < cnt) {
                 const double2* src = a.T + mb[m0 + j].t_off + vec * mb[m0 + j].t_vst;
                 double2* dst = stg + ((buf_i * NL + l) * MB + j) * SLS;
-                for (int i = tl; i < SL; i += TPL) cp_async16(&dst[i], src + i);
+                for (int i = tln; i < SL; i += TPLN) cp_async16(&dst[i], src + i);
             }
         asm volatile("cp.async.commit_group;\n" ::);
     };
@@ -869,14 +991,14 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
                     double2 up[LR];
                     double2 w0 = make_double2(1.0, 0.0);
                     if (dl != 0) {
-                        w0 = __ldg(&twP[(tl * dl) % P]);
+                        w0 = __ldg(&twP[(tln * dl) % P]);
 #pragma unroll
-                        for (int bit = 0; bit < LR; ++bit) up[bit] = __ldg(&twP[(((1 << bit) * TPL) * dl) % P]);
+                        for (int bit = 0; bit < LR; ++bit) up[bit] = __ldg(&twP[(((1 << bit) * TPLN) * dl) % P]);
                     }
 #endif
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        const int k = tl + r * TPL;
+                        const int k = tln + r * TPLN;  // = F (tl + r TPL) + s
                         double2 xk = x[k], xn = x[N - k];
                         if (dl != 0) {
 #if PCB_BUNDLE_TWREC
@@ -911,23 +1033,27 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
         double2 v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int k = tl + r * TPL;
+            const int k = tln + r * TPLN;
             const double2 E = make_double2(zk[r].x + zn[r].x, zk[r].y - zn[r].y);   // Z[k] + conj Z[N-k]
             const double2 Dd = make_double2(zk[r].x - zn[r].x, zk[r].y + zn[r].y);  // Z[k] - conj Z[N-k]
             const double2 O = cmulc(Dd, __ldg(&twP[k]));                            // * exp(+2 pi i k / P)
             v[r] = make_double2(E.x - O.y, E.y + O.x);                              // E + i O
         }
-        fft_rev_order<N, +1, NL, PSH<NL>>(v, fbuf, l, tl, twtab<N>(a.tw));
+        fft_rev_order<M, +1, NLS, PSH<NLS>>(v, fbuf, sl, tl, twtab<M>(a.tw));
         __syncthreads();
 #pragma unroll
         for (int bb = 0; bb < R / RL; ++bb)
 #pragma unroll
             for (int r = 0; r < RL; ++r) {
-                const int p = LastPos<N>::pos(tl, bb, r);
+                const int p = s * M + LastPos<M>::pos(tl, bb, r);
                 xs[l * XS + 2 * p] = v[bb * RL + r].x;
                 xs[l * XS + 2 * p + 1] = v[bb * RL + r].y;
             }
         __syncthreads();
+        if constexpr (F == 3) {
+            split3_time_pass<N, NT, XS>(xs, nb, twtab<N>(a.tw));
+            __syncthreads();
+        }
         for (int ll = 0; ll < nb; ++ll) {
             const int lo = meta[ll].lo, hi = meta[ll].hi;
             const double* x = xs + ll * XS - meta[ll].sh;
@@ -945,6 +1071,7 @@ __global__ void __launch_bounds__(NL * FftCfg<N>::TPL, FftCfg<N>::P2 ? PCB_ROWS_
         metaN = t;
     }
 #else
+    static_assert(F == 1, "the single-batch bundled gather has no split-3 path");
     for (int64_t b0 = b_beg; b0 < b_end; b0 += NL) {
         const int nb = (int)((b_end - b0) < NL ? (b_end - b0) : NL);
         __syncthreads();  // previous batch finished with meta / xs
@@ -1076,8 +1203,12 @@ cudaError_t launch_dyn(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_
 
 template <int LEN>
 constexpr int rows_nl() {  // lines per CTA for the last-axis passes: ~PCB_ROWS_THREADS threads
-    constexpr int t = PCB_ROWS_THREADS / FftCfg<LEN>::TPL;
+    constexpr int t = RowCfg<LEN>::THREADS / (RowCfg<LEN>::F * RowCfg<LEN>::TPL);
     return t < 1 ? 1 : (t > 32 ? 32 : t);
+}
+template <int LEN>
+constexpr int rows_threads() {
+    return rows_nl<LEN>() * RowCfg<LEN>::F * RowCfg<LEN>::TPL;
 }
 template <int P>
 constexpr int cols_nl() {  // column-tile width of the axis-0 / axis-1 passes (>= 2: 32-B runs)

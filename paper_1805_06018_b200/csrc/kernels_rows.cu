@@ -10,8 +10,8 @@ cudaError_t rows_fwd_n(const PassArgs& a, cudaStream_t st) {
     const int64_t maxlines = MODE == RF_SPEC ? (a.D == 2 ? a.P[0] : (int64_t)a.P[0] * a.P[1]) : a.lines_max;
     const int items = (MODE == RF_ADJ && a.global) ? a.B : a.n_slots * (MODE == RF_SPEC ? 1 : a.B);
     dim3 grid((unsigned)((maxlines + NL - 1) / NL), (unsigned)items);
-    const size_t smem = sizeof(double2) * smem_words<N, NL>() + NL * (3 * sizeof(int64_t) + 2 * sizeof(int));
-    return launch_dyn(k_rows_fwd<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
+    const size_t smem = sizeof(double2) * row_words<N, NL>() + NL * (3 * sizeof(int64_t) + 2 * sizeof(int));
+    return launch_dyn(k_rows_fwd<N, NL, MODE>, grid, dim3(rows_threads<N>()), smem, st, a);
 }
 
 template <int MODE>
@@ -28,8 +28,8 @@ cudaError_t rows_fwd_mode(const PassArgs& a, cudaStream_t st) {
 template <int N, int MODE>
 cudaError_t rows_inv_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
     constexpr int NL = rows_nl<N>();
-    constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
-                                                                          : (NL * (2 * N + 1) + 1) / 2;
+    constexpr int BUFW = row_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? row_words<N, NL>()
+                                                                        : (NL * (2 * N + 1) + 1) / 2;
     dim3 grid((unsigned)n_lines, (unsigned)a.B);
 #if PCB_RINV_ALIAS
     const size_t stage_words = (size_t)NL * stage_stride_b<N, NL>();
@@ -38,14 +38,14 @@ cudaError_t rows_inv_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
 #endif
     const size_t smem = sizeof(double2) * stage_words + sizeof(double) * ((size_t)a.n[a.D - 1] + 1) +
                         NL * sizeof(GatherEntry) + 16;
-    return launch_dyn(k_rows_inv<N, NL, MODE>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
+    return launch_dyn(k_rows_inv<N, NL, MODE>, grid, dim3(rows_threads<N>()), smem, st, a);
 }
 
 template <int N, int ADJ>
 cudaError_t rows_inv_b_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
     constexpr int NL = rows_nl<N>();
-    constexpr int BUFW = smem_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? smem_words<N, NL>()
-                                                                          : (NL * (2 * N + 1) + 1) / 2;
+    constexpr int BUFW = row_words<N, NL>() > (NL * (2 * N + 1) + 1) / 2 ? row_words<N, NL>()
+                                                                        : (NL * (2 * N + 1) + 1) / 2;
     dim3 grid((unsigned)n_lines, (unsigned)a.B);
 #if PCB_BUNDLE_XPF && PCB_BUNDLE_ALIAS
     const size_t stage_words = (size_t)2 * NL * PCB_BUNDLE_MB * stage_stride_b<N, NL>();
@@ -54,7 +54,7 @@ cudaError_t rows_inv_b_n(const PassArgs& a, int64_t n_lines, cudaStream_t st) {
 #endif
     const size_t smem = sizeof(double2) * stage_words + sizeof(double) * ((size_t)a.n[a.D - 1] + 1) +
                         (1 + PCB_BUNDLE_XPF) * NL * sizeof(GatherEntry) + 16;
-    return launch_dyn(k_rows_inv_b<N, NL, ADJ>, grid, dim3(NL * FftCfg<N>::TPL), smem, st, a);
+    return launch_dyn(k_rows_inv_b<N, NL, ADJ>, grid, dim3(rows_threads<N>()), smem, st, a);
 }
 
 template <int MODE>

@@ -155,11 +155,13 @@ struct DevBuf {
 
 // Plan switches, fixed per handle at create (defaults, overridable for A/B measurement by env):
 //   PCB_POW2=1        power-of-two FFT sizes only
-//   PCB_MIXED_LAST=1  3-smooth sizes on the R2C axis too (default: only in 3-D)
+//   PCB_MIXED_LAST    R2C-axis sizes: 0 powers of two only (default in 2-D), 1 every 3-smooth size
+//                     (default in 3-D), 2 powers of two and 3 * 2^a with P/2 >= 96, the lengths the row
+//                     passes run as 3 interleaved power-of-two sub-lines (kernels_impl.cuh PCB_SPLIT3_MIN)
 //   PCB_BUNDLE=0      one C2R per gather entry in the LOCAL apply (default: bundles in 2-D)
 struct PlanSwitches {
     bool pow2_only = false;
-    bool mixed_last = false;
+    int mixed_last = 0;
     bool bundle = true;
     bool families = true;  // PCB_FAMILIES=0: per-term row transforms even for separable weights
     // PCB_CHAINS=1: column chains in the 2-D LOCAL apply.  Measured on B200 (c3): the gather gets
@@ -179,14 +181,18 @@ struct PlanSwitches {
 
 // Smallest compiled FFT size >= max(v, 16): 2^a * {1, 3, 9}.  The last (R2C) axis also needs its
 // half length P/2 compiled for the row passes.
-int64_t fft_size_at_least(int64_t v, bool last_axis, bool mixed_last, bool pow2_only) {
+int64_t fft_size_at_least(int64_t v, bool last_axis, int mixed_last, bool pow2_only) {
+    auto last_ok = [&](int64_t h) {  // half length h of the R2C axis
+        if (is_pow2c((int)h)) return true;
+        if (pow2_only || mixed_last == 0) return false;
+        if (mixed_last == 2) return h >= 96 && h % 3 == 0 && is_pow2c((int)(h / 3));
+        return true;
+    };
     for (int64_t p = 16; p <= (last_axis ? 4096 : 4096); p += 8) {
         if (p < v) continue;
         if (!fft_len_ok((int)p)) continue;
         if (pow2_only && !is_pow2c((int)p)) continue;
-        if (last_axis && (!fft_len_ok((int)(p / 2)) || p / 2 > 2048 ||
-                          ((pow2_only || !mixed_last) && !is_pow2c((int)(p / 2)))))
-            continue;
+        if (last_axis && (!fft_len_ok((int)(p / 2)) || p / 2 > 2048 || !last_ok(p / 2))) continue;
         if (!last_axis && cols_tile_width((int)p) < 0) continue;
         return p;
     }
@@ -2079,9 +2085,9 @@ PCB_API pcb_status pcb_plan_shards(int32_t dim, const int64_t* dom_lo, const int
         if (partition != PCB_PARTITION_COST && partition != PCB_PARTITION_COUNT)
             fail(PCB_EINVAL, "pcb_plan_shards: bad partition");
         std::unique_ptr<pcb_op> op(new pcb_op);
-        op->sw.mixed_last = dim == 3;  // as pcb_create
+        op->sw.mixed_last = dim == 3 ? 1 : 0;  // as pcb_create
         if (const char* e = getenv("PCB_POW2")) op->sw.pow2_only = atoi(e) != 0;
-        if (const char* e = getenv("PCB_MIXED_LAST")) op->sw.mixed_last = atoi(e) != 0;
+        if (const char* e = getenv("PCB_MIXED_LAST")) op->sw.mixed_last = atoi(e);
         plan(op.get(), dim, dom_lo, dom_hi, r, w_lo, w_hi, w_vals, phi_lo, phi_hi, phi_vals, opt, true);
         for (int k = 0; k < r; ++k) {
             if (owner) owner[k] = op->shard_of[k];
@@ -2120,10 +2126,14 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
         if (prop.major < 10) fail(PCB_ECUDA, "pcop-b200 kernels are built for sm_100a (Blackwell B200)");
         op->max_batch = opt.max_batch > 0 ? opt.max_batch : 16;
         if (const char* e = getenv("PCB_POW2")) op->sw.pow2_only = atoi(e) != 0;
-        // 3-smooth sizes on the R2C axis pay off in 3-D (c4: +4%) but not in 2-D, where the
-        // 24-element row kernels lose more to register pressure than they save (c3, c2: measured)
-        op->sw.mixed_last = dim == 3;
-        if (const char* e = getenv("PCB_MIXED_LAST")) op->sw.mixed_last = atoi(e) != 0;
+        // 3-smooth sizes on the R2C axis pay off in 3-D (c4: +4%).  In 2-D the 24-element row kernels
+        // lose more to register pressure than they save (c3, c2: measured).  Mode 2 (only the 3 * 2^a
+        // lengths the row passes run as three power-of-two sub-lines) makes the column pass 14% faster
+        // at c3 (3.43 -> 2.94 ms) but the tighter periods hold half as many bundle members and add a
+        // size class to the gather (rows_inv 2.40 -> 2.91 ms, rows_fwd 1.10 -> 1.40 ms): 9,245 ->
+        // 8,878 vec/s, so 2-D keeps powers of two by default
+        op->sw.mixed_last = dim == 3 ? 1 : 0;
+        if (const char* e = getenv("PCB_MIXED_LAST")) op->sw.mixed_last = atoi(e);
         // frequency-domain bundles pay in 2-D (c3 rows_inv 3.85 -> 3.36 ms); 3-D lines gather many
         // short same-shift entries and the per-entry path is faster there (c4: measured)
         op->sw.bundle = dim == 2;

@@ -368,6 +368,43 @@ def test_bundled_gather_matches_per_entry_gather(gpu, name, monkeypatch):
         assert rel(b[i], a[i]) <= 1e-14
 
 
+@pytest.mark.parametrize("name", ["c2", "c3"])
+@pytest.mark.parametrize("bundle", ["1", "0"])
+def test_split3_rows_match_power_of_two_rows(gpu, name, bundle, monkeypatch):
+    """PCB_MIXED_LAST=2: last-axis sizes 3 * 2^a (192, 384) run as three interleaved power-of-two
+    sub-lines in the row passes (radix-3 butterfly in the forward gather / the inverse's output
+    pass).  Same operator as the power-of-two plan: apply and adjoint, bundled and per-entry gathers,
+    and the spectra built through the same forward kernels."""
+    inp = inputs.make_config(name)
+    F = normal_vectors(12, 2, inp.n_points)
+    monkeypatch.setenv("PCB_BUNDLE", bundle)
+    monkeypatch.setenv("PCB_MIXED_LAST", "0")
+    p2 = ProductConvolutionOperator.from_inputs(inp, mode="local")
+    monkeypatch.setenv("PCB_MIXED_LAST", "2")
+    s3 = ProductConvolutionOperator.from_inputs(inp, mode="local")
+    assert s3.info["spectra_bytes"] < p2.info["spectra_bytes"]  # some classes moved to 192 / 384
+    a, b = p2.apply_batch(F), s3.apply_batch(F)
+    aa, ba = p2.apply_adjoint_batch(F), s3.apply_adjoint_batch(F)
+    for i in range(2):
+        assert rel(b[i], a[i]) <= 1e-13
+        assert rel(ba[i], aa[i]) <= 1e-13
+
+
+def test_split3_rows_vs_oracle_1d(gpu, monkeypatch):
+    """A 1-D operator whose line is 3 * 2^a under PCB_MIXED_LAST=2 (one sub-line CTA), vs the oracle."""
+    inp = inputs.small_lattice(n=300, dim=1, m=2, sigma=6.0)
+    ref = O.PCOperator.from_inputs(inp)
+    F = normal_vectors(13, 2, inp.n_points)
+    monkeypatch.setenv("PCB_MIXED_LAST", "2")
+    op = ProductConvolutionOperator.from_inputs(inp, mode="local")
+    last = op.info["fft_size"][0]
+    assert last % 3 == 0 and last // 2 >= 96, op.info["fft_size"]
+    G, GA = op.apply_batch(F), op.apply_adjoint_batch(F)
+    for i in range(2):
+        assert rel(G[i], ref.apply(F[i])) <= APPLY_TOL
+        assert rel(GA[i], ref.apply_adjoint(F[i])) <= APPLY_TOL
+
+
 @pytest.mark.parametrize("name", ["c2", "c3", "c4", "small2d", "small3d", "small1d"])
 def test_row_families_match_per_term_rows(gpu, name, monkeypatch):
     """Separable (tent) weights: terms sharing a last-axis weight factor share their row
