@@ -142,6 +142,8 @@ struct EntryArgs {
     int32_t nb[3];              // buckets per axis
     const int64_t* bucket_ptr;  // CSR over buckets (lexicographic)
     const int32_t* bucket_terms;
+    int64_t kun_lo[3], kun_hi[3];  // union of the terms' kernel boxes K_k (lo > hi: no term)
+    int32_t bucket_shift[3];       // log2 of the bucket edge when it is a power of two, else -1
 };
 cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, const int64_t* x, double* out,
                            int32_t* bad, cudaStream_t st);

@@ -338,6 +338,7 @@ struct pcb_op {
     std::vector<double**> d_parts_s;  // per shard: a device array (on its device) of every partial pointer
     // entry gather
     int32_t bucket[3] = {1, 1, 1}, nb[3] = {1, 1, 1};
+    int64_t kun_lo[3] = {1, 1, 1}, kun_hi[3] = {0, 0, 0};  // union of the kernel boxes (entry gather's zero test)
     pcb::DevBuf<int64_t> bucket_ptr;
     pcb::DevBuf<int32_t> bucket_terms;
     // host-call staging
@@ -1719,9 +1720,16 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             nbt *= op->nb[a];
         }
         std::vector<std::vector<int32_t>> lists(nbt);
+        bool any_k = false;
         for (int k = 0; k < r; ++k) {
             if (!op->has_x[k] || !op->has_k[k]) continue;
             const TermDesc& t = op->terms[k];
+            for (int a = 0; a < 3; ++a) {
+                const int64_t lo = a < D ? t.k_lo[a] : 0, hi = a < D ? t.k_lo[a] + t.k_ext[a] - 1 : 0;
+                op->kun_lo[a] = any_k ? std::min(op->kun_lo[a], lo) : lo;
+                op->kun_hi[a] = any_k ? std::max(op->kun_hi[a], hi) : hi;
+            }
+            any_k = true;
             int64_t b0[3] = {0, 0, 0}, b1[3] = {0, 0, 0};
             for (int a = 0; a < D; ++a) {
                 b0[a] = (t.x_lo[a] - op->dom_lo[a]) / op->bucket[a];
@@ -1972,6 +1980,11 @@ EntryArgs entry_args(pcb_op* op) {
         e.n[a] = op->n[a];
         e.bucket[a] = op->bucket[a];
         e.nb[a] = op->nb[a];
+        e.kun_lo[a] = op->kun_lo[a];
+        e.kun_hi[a] = op->kun_hi[a];
+        e.bucket_shift[a] = -1;
+        for (int sh = 0; sh < 30; ++sh)
+            if (op->bucket[a] == (1 << sh)) e.bucket_shift[a] = sh;
     }
     e.terms = op->d_terms.p;
     e.w_pool = op->w_pool.p;
@@ -2834,7 +2847,7 @@ static void blocks_common(pcb_op* op, int32_t nblk, const int64_t* d_t, const in
         return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, op->st_blk.p, ph, s2);
     };
     const int zm = blocks_zero_mode();
-    const bool aux = zm == 3 || zm == 4;
+    const bool aux = zm == 3 || zm == 4 || zm == 5;
     if (aux && !op->s_aux) PCB_CK(cudaStreamCreateWithFlags(&op->s_aux, cudaStreamNonBlocking));
     auto fork = [&] {
         PCB_CK(cudaEventRecord(op_event(op, 6), st));
@@ -2842,12 +2855,20 @@ static void blocks_common(pcb_op* op, int32_t nblk, const int64_t* d_t, const in
         launch(op, op->s_aux, "blocks(zero)", [&] { return phase(2, op->s_aux); });
         PCB_CK(cudaEventRecord(op_event(op, 7), op->s_aux));
     };
+    if (zm >= 5) {
+        // 5 (default): the zero fill on a second stream beside the blocks that need terms; 6: one stream
+        if (zm == 5) fork();
+        launch(op, st, "blocks(gather)", [&] { return phase(0, st); });
+        if (zm == 5) PCB_CK(cudaStreamWaitEvent(st, op_event(op, 7), 0));
+        else launch(op, st, "blocks(zero)", [&] { return phase(2, st); });
+    } else {
     if (zm == 4) fork();
     launch(op, st, "blocks(classify)", [&] { return phase(0, st); });
     if (zm == 3) fork();
     if (zm == 4) PCB_CK(cudaStreamWaitEvent(st, op_event(op, 7), 0));  // the memset before the gather's writes
     launch(op, st, "blocks(gather)", [&] { return phase(1, st); });
     if (zm == 3) PCB_CK(cudaStreamWaitEvent(st, op_event(op, 7), 0));
+    }
     if (host_check) {
         int32_t bad = 0;
         PCB_CK(cudaMemcpyAsync(&bad, op->st_flag.p, 4, cudaMemcpyDeviceToHost, st));
