@@ -148,15 +148,14 @@ struct EntryArgs {
 cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, const int64_t* x, double* out,
                            int32_t* bad, cudaStream_t st);
 // bshape_host: the block shape per axis (host array, passed by value); scratch: device int32 of
-// blocks_scratch_ints(nblk) (the work lists and the candidate lists).  phase 0: classify (writes
-// or lists the all-zero blocks, lists the others); phase 1: gather the listed blocks; phase 2: the
-// listed zero blocks (independent of phase 1: run it on a second stream).
+// blocks_scratch_ints(nblk) (the list of blocks that need terms).  phase 0: those blocks (scan, then
+// candidate search + gather); phase 1: the exact-zero blocks (independent of phase 0: run it on a
+// second stream when blocks_two_streams()).
 cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
                           const int32_t* bshape_host, double* out, int32_t* bad, int32_t* scratch, int phase,
                           cudaStream_t st);
 int64_t blocks_scratch_ints(int32_t nblk);
-// how the all-zero blocks are written (see launch_blocks; 3: phase 2 runs beside phase 1, 4: beside phase 0)
-int blocks_zero_mode();
+bool blocks_two_streams();
 
 // block apply, direct form (small blocks)
 cudaError_t launch_block_direct(const EntryArgs& a, int32_t nblk, int64_t max_t, const int64_t* t_lo,

@@ -223,22 +223,7 @@ __global__ void k_zero(double* p, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = 0.0;
 }
 
-// K6 for dense blocks (config 5), one CTA per 8 blocks, two phases:
-//  1. classify (one warp per block): the block's candidate terms -- listed in the buckets covering
-//     S, deduplicated, kept only when X_k meets S and the kernel box K_k meets the offsets T - S (any
-//     other term reads phi^E = 0 there: exact zeros, which leave the sum unchanged) -- in ascending
-//     k, the reference's summation order.  A block with no candidate is all zeros and its warp
-//     writes it with 16-byte stores (config 5: 4031 of the 4096 seed-3 blocks).
-//  2. gather (the whole CTA, block by block, for the CTA's blocks that have candidates): stage the
-//     candidates' weights on S and phi^E windows over T - S ((2 bs - 1) per axis) in shared memory;
-//     every entry sums over the staged terms in ascending k with the reference's IEEE mul/add --
-//     the same terms in the same order as entry_value, so the result is bit-identical.  Blocks that
-//     leave the domain or have too many candidates take the per-entry path.
-// Zero blocks are written by the TMA engine: one lane issues cp.async.bulk copies of a zeroed 4 KiB
-// shared-memory tile to the block (no per-thread store traffic through the LSU).  Blocks with
-// candidates go to a device work queue that every CTA drains once its own classification is
-// done, so the few gathered blocks spread over the CTAs that finish first instead of
-// serializing in the CTA that classified them.
+// K6 for dense blocks (config 5): constants and helpers; the passes follow below.
 #ifndef PCB_BZ_DOUBLES
 // zero tile: 32 KiB, one bulk copy per 64 x 64 block.  Measured at config 5 with the gather pass
 // beside the fill: 4 KiB tiles (8 copies per block) 42.7 us per call, 32 KiB 33.1 us -- fewer, larger
@@ -249,7 +234,7 @@ constexpr int BZ_DOUBLES = PCB_BZ_DOUBLES;
 constexpr int BT_CAP = 32;  // max staged candidate terms per block
 constexpr int BT_IDS = 64;  // gathered bucket entries (with duplicates) per block
 constexpr int BT_NZ = 8;    // listed nonzero-weight terms per source point
-constexpr int BC_WARPS = 8; // blocks (classifying warps) per CTA
+constexpr int BC_WARPS = 8; // blocks (warps) per zero-fill CTA
 constexpr int BT_PXMAX = 256;   // gather kernel: max points per block (coordinate tables)
 constexpr int BT_WINMAX = 1024; // ... max window offsets
 
@@ -272,347 +257,8 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
     return pol;
 }
 
-// scratch (int32): [0] queue reserve count, [1] queue taken count, [2, 2 + nblk) queue (blk + 1;
-// 0 = not yet published), then per block (cap + 1): candidate count (-1: per-entry path), ids
-__global__ void __launch_bounds__(256) k_blocks_classify(EntryArgs a, int32_t nblk,
-                                                         const int64_t* __restrict__ t_origin,
-                                                         const int64_t* __restrict__ s_origin, int bs0, int bs1,
-                                                         int bs2, int cap, double* __restrict__ out,
-                                                         int32_t* __restrict__ scr, int zero_mode) {
-    __shared__ __align__(128) double Z[BZ_DOUBLES];  // zero tile (the bulk stores' source)
-    __shared__ int ids_s[BC_WARPS][BT_IDS];
-    __shared__ int first_s[BC_WARPS][BT_IDS];
-    __shared__ int cand_s[BC_WARPS][BT_CAP];
-    const int D = a.D;
-    const int bs[3] = {bs0, bs1, bs2};
-    int npx = 1, win = 1;
-    for (int i = 0; i < D; ++i) {
-        npx *= bs[i];
-        win *= 2 * bs[i] - 1;
-    }
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    for (int i = tid; i < BZ_DOUBLES; i += blockDim.x) Z[i] = 0.0;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    int32_t* queue = scr + 2;
-    int32_t* cand_g = scr + 2 + nblk;
-    int32_t* zlist = cand_g + (int64_t)nblk * (cap + 1);
-    bool issued = false;  // this thread has bulk stores in flight (lane 0 of a zero-block warp)
-    // ---- phase 1: classify (warp wid <-> block blk) ----
-    {
-        const int blk = blockIdx.x * BC_WARPS + wid;
-        int* ids = ids_s[wid];
-        int* first = first_s[wid];
-        int64_t tv[3] = {0, 0, 0}, sv[3] = {0, 0, 0};
-        int fb = 0, nk = 0;
-        if (blk < nblk) {
-            for (int i = 0; i < D; ++i) {
-                tv[i] = t_origin[(int64_t)blk * D + i];
-                sv[i] = s_origin[(int64_t)blk * D + i];
-                if (tv[i] < a.dom_lo[i] || tv[i] + bs[i] > a.dom_lo[i] + a.n[i] || sv[i] < a.dom_lo[i] ||
-                    sv[i] + bs[i] > a.dom_lo[i] + a.n[i])
-                    fb = 1;
-            }
-            if (!fb) {
-                int blo[3] = {0, 0, 0}, bn[3] = {1, 1, 1}, nbk = 1;
-                for (int i = 0; i < D; ++i) {  // 32-bit arithmetic: domain axes are < 2^20
-                    const int rel = (int)(sv[i] - a.dom_lo[i]);
-                    blo[i] = rel / a.bucket[i];
-                    bn[i] = (rel + bs[i] - 1) / a.bucket[i] - blo[i] + 1;
-                    nbk *= bn[i];
-                }
-                int64_t beg = 0;
-                int cnt = 0;
-                if (nbk <= 32 && lane < nbk) {
-                    int r = lane, c[3] = {0, 0, 0};
-                    for (int i = D - 1; i >= 0; --i) {
-                        c[i] = blo[i] + r % bn[i];
-                        r /= bn[i];
-                    }
-                    int64_t bl = 0;
-                    for (int i = 0; i < D; ++i) bl = bl * a.nb[i] + c[i];
-                    beg = a.bucket_ptr[bl];
-                    cnt = (int)(a.bucket_ptr[bl + 1] - beg);
-                }
-                int off = cnt;  // inclusive warp prefix sum
-                for (int d = 1; d < 32; d <<= 1) {
-                    const int v = __shfl_up_sync(0xffffffffu, off, d);
-                    if (lane >= d) off += v;
-                }
-                const int total = __shfl_sync(0xffffffffu, off, 31);
-                off -= cnt;
-                if (nbk > 32 || total > BT_IDS) {
-                    fb = 1;
-                } else {
-                    // gathered list position pos -> (bucket b, entry pos - off_b): every lane loads
-                    // its two positions at once (one round trip instead of a serial loop per bucket)
-                    int64_t src[2] = {-1, -1};
-                    for (int b = 0; b < nbk; ++b) {
-                        const int ob = __shfl_sync(0xffffffffu, off, b);
-                        const int cb = __shfl_sync(0xffffffffu, cnt, b);
-                        const int64_t gb = __shfl_sync(0xffffffffu, beg, b);
-                        for (int h = 0; h < 2; ++h) {
-                            const int pos = lane + 32 * h;
-                            if (pos >= ob && pos < ob + cb) src[h] = gb + (pos - ob);
-                        }
-                    }
-                    int got[2];
-                    for (int h = 0; h < 2; ++h) got[h] = src[h] >= 0 ? a.bucket_terms[src[h]] : 0;
-                    for (int h = 0; h < 2; ++h)
-                        if (lane + 32 * h < total) ids[lane + 32 * h] = got[h];
-                    __syncwarp();
-                    int keep[2] = {0, 0}, idv[2] = {0, 0};
-                    for (int h = 0; h < 2; ++h) {
-                        const int pos = lane + 32 * h;
-                        if (pos >= total) continue;
-                        const int id = ids[pos];
-                        int f = 1;
-                        for (int j = 0; j < pos; ++j) f &= ids[j] != id;
-                        if (f) {
-                            const TermDesc& t = a.terms[id];
-                            for (int d = 0; d < D && f; ++d) {
-                                const int64_t o = tv[d] - sv[d];
-                                f &= (t.x_lo[d] <= sv[d] + bs[d] - 1) && (t.x_lo[d] + t.m[d] - 1 >= sv[d]) &&
-                                     (t.k_lo[d] <= o + bs[d] - 1) && (t.k_lo[d] + t.k_ext[d] - 1 >= o - (bs[d] - 1));
-                            }
-                        }
-                        keep[h] = f;
-                        idv[h] = id;
-                        first[pos] = f ? id : -1;
-                    }
-                    __syncwarp();
-                    nk = __popc(__ballot_sync(0xffffffffu, keep[0])) + __popc(__ballot_sync(0xffffffffu, keep[1]));
-                    if (nk > cap) {
-                        fb = 1;
-                    } else {
-                        for (int h = 0; h < 2; ++h) {
-                            if (!keep[h]) continue;
-                            int rank = 0;
-                            for (int j = 0; j < total; ++j) rank += first[j] >= 0 && first[j] < idv[h];
-                            cand_s[wid][rank] = idv[h];
-                        }
-                    }
-                }
-            }
-            if (!fb && nk == 0) {  // no term can contribute: an all-zero block
-                const int64_t bytes = (int64_t)npx * npx * 8;
-                char* ob = reinterpret_cast<char*>(out + (int64_t)blk * npx * npx);
-                const bool al16 = (reinterpret_cast<uintptr_t>(ob) & 15) == 0;
-                if (zero_mode == 0 && al16) {  // written by the TMA engine from the zero tile
-                    if (lane == 0) {
-                        int64_t o = 0;
-                        for (; o + BZ_DOUBLES * 8 <= bytes; o += BZ_DOUBLES * 8) bulk_store_s2g(ob + o, Z, BZ_DOUBLES * 8);
-                        const int64_t tail = (bytes - o) & ~(int64_t)15;
-                        if (tail > 0) bulk_store_s2g(ob + o, Z, (uint32_t)tail);
-                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                        if (bytes & 15) *reinterpret_cast<double*>(ob + bytes - 8) = 0.0;
-                        issued = true;
-                    }
-                } else if (zero_mode == 1 && al16) {  // 16-byte stores by the warp
-                    double2* o2 = reinterpret_cast<double2*>(ob);
-                    for (int64_t e = lane; e < bytes / 16; e += 32) o2[e] = make_double2(0.0, 0.0);
-                    if ((bytes & 15) && lane == 0) *reinterpret_cast<double*>(ob + bytes - 8) = 0.0;
-                } else if (zero_mode == 3) {  // listed for k_blocks_zero, which runs beside the gather
-                    if (lane == 0) zlist[atomicAdd(scr + 1, 1)] = blk;
-                } else if (zero_mode != 2) {
-                    double* od = reinterpret_cast<double*>(ob);
-                    for (int64_t e = lane; e < (int64_t)npx * npx; e += 32) od[e] = 0.0;
-                }  // zero_mode 2 / 4: the output is memset before / beside the launch
-            } else if (lane == 0) {  // list the block for the gather kernel, with its candidates
-                int32_t* cg = cand_g + (int64_t)blk * (cap + 1);
-                cg[0] = fb ? -1 : nk;
-                for (int c = 0; c < (fb ? 0 : nk); ++c) cg[1 + c] = cand_s[wid][c];
-                queue[atomicAdd(scr, 1)] = blk;
-            }
-        }
-    }
-    if (issued) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // Z read before the CTA exits
-}
-
-// zero_mode 3: the all-zero blocks listed by the classify pass, one warp per block, 16-byte stores
-// (runs on a second stream concurrently with k_blocks_gather: the two write disjoint blocks)
-__global__ void __launch_bounds__(256) k_blocks_zero(const int32_t* __restrict__ scr, int32_t nblk, int cap, int npx,
-                                                     double* __restrict__ out) {
-    const int lane = threadIdx.x & 31;
-    const int i = blockIdx.x * BC_WARPS + (threadIdx.x >> 5);
-    if (i >= scr[1]) return;
-    const int32_t* zlist = scr + 2 + nblk + (int64_t)nblk * (cap + 1);
-    const int blk = zlist[i];
-    const int64_t n2 = (int64_t)npx * npx;
-    double* ob = out + (int64_t)blk * n2;
-    if ((reinterpret_cast<uintptr_t>(ob) & 15) == 0) {
-        double2* o2 = reinterpret_cast<double2*>(ob);
-        for (int64_t e = lane; e < n2 / 2; e += 32) o2[e] = make_double2(0.0, 0.0);
-        if ((n2 & 1) && lane == 0) ob[n2 - 1] = 0.0;
-    } else {
-        for (int64_t e = lane; e < n2; e += 32) ob[e] = 0.0;
-    }
-}
-
-__global__ void __launch_bounds__(256) k_blocks_gather(EntryArgs a, const int64_t* __restrict__ t_origin,
-                                                       const int64_t* __restrict__ s_origin, int bs0, int bs1, int bs2,
-                                                       int cap, double* __restrict__ out, int32_t* bad,
-                                                       const int32_t* __restrict__ scr, int32_t nblk) {
-    extern __shared__ double sm[];
-    const int D = a.D;
-    const int bs[3] = {bs0, bs1, bs2};
-    int npx = 1, win = 1;
-    for (int i = 0; i < D; ++i) {
-        npx *= bs[i];
-        win *= 2 * bs[i] - 1;
-    }
-    const int tid = threadIdx.x;
-    const int32_t* queue = scr + 2;
-    const int32_t* cand_g = scr + 2 + nblk;
-    const int nwork = scr[0];
-    double* W = sm;               // [cap][npx]
-    double* PH = W + cap * npx;   // [cap][win]
-    int* offs = reinterpret_cast<int*>(PH + cap * win);              // [npx] window offset of a point
-    unsigned char* nzn = reinterpret_cast<unsigned char*>(offs + npx);  // [npx] nonzero-term count
-    unsigned char* nzc = nzn + npx;                                   // [npx][BT_NZ] their indices
-    __shared__ int s_nc, s_item;
-    __shared__ int s_cand[BT_CAP];
-    __shared__ int64_t s_t[3], s_s[3];
-    // the candidates' geometry (one parallel load per candidate instead of per staged element)
-    __shared__ int64_t c_woff[BT_CAP], c_poff[BT_CAP];
-    __shared__ int32_t c_xlo[BT_CAP][3], c_klo[BT_CAP][3], c_m[BT_CAP][3], c_kext[BT_CAP][3];
-    // per-point / per-window-offset coordinates (computed once per CTA; no divisions per element)
-    __shared__ int16_t pco[BT_PXMAX][3], wco[BT_WINMAX][3];
-    int centre = 0;
-    {
-        int mul = 1;
-        for (int d = D - 1; d >= 0; --d) {
-            centre += (bs[d] - 1) * mul;
-            mul *= 2 * bs[d] - 1;
-        }
-    }
-    for (int p = tid; p < npx; p += blockDim.x) {
-        int r = p, o = 0, mul = 1;
-        for (int d = D - 1; d >= 0; --d) {
-            o += (r % bs[d]) * mul;
-            mul *= 2 * bs[d] - 1;
-            pco[p][d] = (int16_t)(r % bs[d]);
-            r /= bs[d];
-        }
-        offs[p] = o;
-    }
-    for (int w = tid; w < win; w += blockDim.x) {
-        int r = w;
-        for (int d = D - 1; d >= 0; --d) {
-            const int wd = 2 * bs[d] - 1;
-            wco[w][d] = (int16_t)(r % wd - (bs[d] - 1));
-            r /= wd;
-        }
-    }
-    for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
-        if (tid == 0) {
-            const int item = queue[wi];
-            const int32_t* cg = cand_g + (int64_t)item * (cap + 1);
-            s_nc = cg[0];
-            for (int c = 0; c < s_nc; ++c) s_cand[c] = cg[1 + c];
-            for (int i = 0; i < 3; ++i) {
-                s_t[i] = i < D ? t_origin[(int64_t)item * D + i] : 0;
-                s_s[i] = i < D ? s_origin[(int64_t)item * D + i] : 0;
-            }
-            s_item = item;
-        }
-        __syncthreads();
-        const int blk = s_item;
-        const int nc = s_nc;
-        const int* cand = s_cand;
-        double* ob = out + (int64_t)blk * npx * npx;
-        if (nc < 0) {  // per-entry path (out-of-domain entries flag `bad`)
-            for (int e = tid; e < npx * npx; e += blockDim.x) {
-                int i = e / npx, j = e - (e / npx) * npx;
-                int64_t y[3], x[3];
-                for (int d = D - 1; d >= 0; --d) {
-                    y[d] = s_t[d] + i % bs[d];
-                    i /= bs[d];
-                    x[d] = s_s[d] + j % bs[d];
-                    j /= bs[d];
-                }
-                bool b = false;
-                ob[e] = entry_value(a, y, x, b);
-                if (b) atomicOr(bad, 1);
-            }
-            __syncthreads();
-            continue;
-        }
-        if (tid < nc) {  // candidate geometry relative to the block (32-bit: axes are < 2^20)
-            const TermDesc& t = a.terms[cand[tid]];
-            for (int d = 0; d < 3; ++d) {
-                c_xlo[tid][d] = d < D ? (int32_t)(t.x_lo[d] - s_s[d]) : 0;              // X_k.lo - S.lo
-                c_klo[tid][d] = d < D ? (int32_t)(t.k_lo[d] - (s_t[d] - s_s[d])) : 0;  // K_k.lo - (T - S).lo
-                c_m[tid][d] = t.m[d];
-                c_kext[tid][d] = t.k_ext[d];
-            }
-            c_woff[tid] = t.w_off;
-            c_poff[tid] = t.phi_off;
-        }
-        __syncthreads();
-#pragma unroll 4
-        for (int idx = tid; idx < nc * npx; idx += blockDim.x) {  // w_k on S (0 outside X_k)
-            const int c = idx / npx;
-            const int j = idx - c * npx;
-            bool in = true;
-            int wl = 0;
-            for (int d = 0; d < D; ++d) {
-                const int u = pco[j][d] - c_xlo[c][d];
-                in = in && u >= 0 && u < c_m[c][d];
-                wl = wl * c_m[c][d] + u;
-            }
-            W[idx] = in ? a.w_pool[c_woff[c] + wl] : 0.0;
-        }
-#pragma unroll 4
-        for (int idx = tid; idx < nc * win; idx += blockDim.x) {  // phi_k^E on the offsets T - S
-            const int c = idx / win;
-            const int w2 = idx - c * win;
-            bool in = true;
-            int zl = 0;
-            for (int d = 0; d < D; ++d) {
-                const int z = wco[w2][d] - c_klo[c][d];
-                in = in && z >= 0 && z < c_kext[c][d];
-                zl = zl * c_kext[c][d] + z;
-            }
-            PH[idx] = in ? a.phi_pool[c_poff[c] + zl] : 0.0;
-        }
-        __syncthreads();
-        for (int j = tid; j < npx; j += blockDim.x) {  // per source point: its terms with w != 0
-            int q = 0;
-            for (int c = 0; c < nc; ++c)
-                if (W[c * npx + j] != 0.0) {
-                    if (q < BT_NZ) nzc[j * BT_NZ + q] = (unsigned char)c;
-                    ++q;
-                }
-            nzn[j] = (unsigned char)(q <= BT_NZ ? q : 255);
-        }
-        __syncthreads();
-        // entry (i, j): window index T_off[i] - S_off[j] + centre (the per-axis offset is linear)
-        for (int e = tid; e < npx * npx; e += blockDim.x) {
-            const int i = e / npx, j = e - i * npx;
-            const int widx = offs[i] - offs[j] + centre;
-            double sum = 0.0;
-            const int q = nzn[j];
-            if (q != 255) {
-                for (int r = 0; r < q; ++r) {
-                    const int c = nzc[j * BT_NZ + r];
-                    sum = __dadd_rn(sum, __dmul_rn(W[c * npx + j], PH[c * win + widx]));
-                }
-            } else {
-                for (int c = 0; c < nc; ++c) {
-                    const double wv = W[c * npx + j];
-                    if (wv != 0.0) sum = __dadd_rn(sum, __dmul_rn(wv, PH[c * win + widx]));
-                }
-            }
-            ob[e] = sum;
-        }
-        __syncthreads();
-    }
-}
-
-
 // ---------------------------------------------------------------------------
-// Dense blocks, two independent passes (PCB_C5_ZERO = 5, the default; 6: on one stream):
+// Dense blocks, two independent passes (on two streams; PCB_BLOCKS_STREAMS=1: one after the other):
 //   * every block first takes a geometric test on its origins alone: if on some axis the offsets
 //     T - S = [t - s - (bs - 1), t - s + (bs - 1)] miss the union of all kernel boxes, every entry
 //     reads phi^E = 0 and the block is an exact zero (config 5: 3,9xx of 4096 blocks);
@@ -620,12 +266,13 @@ __global__ void __launch_bounds__(256) k_blocks_gather(EntryArgs a, const int64_
 //     evict-first): one load of the origins, then stores -- the write stream starts at once instead
 //     of after the candidate search (a chain of dependent loads through buckets and descriptors);
 //   * k_blocks_scan lists the others (one thread per block) and k_blocks_fused takes one listed
-//     block per CTA: warp 0 finds the block's candidate terms (classify_block, as
-//     k_blocks_classify), then the CTA stages their weights and phi^E windows and sums every entry
+//     block per CTA: warp 0 finds the block's candidate terms (classify_block), then the CTA stages
+//     their weights and phi^E windows ((2 bs - 1) offsets per axis) in shared memory and sums every entry
 //     in ascending k (bit-identical to entry_value), or writes zeros when no candidate is left.
 //     The two passes write disjoint blocks and need nothing from each other: two streams.
-// Measured at config 5 (us per call): classify + gather passes (mode 0) 58; this 33.1 (42.7 with 4 KiB
-// zero tiles); on one stream 54 (gather path 28, fill 29).  One launch with gather CTAs that scan the origins themselves: 65
+// Measured at config 5 (us per call): the round-2 design before it (a classify pass over every block
+// that also wrote the zero blocks, then a gather pass over the listed ones) 58; this 33.1 (42.7 with
+// 4 KiB zero tiles); on one stream 54 (gather path 28, fill 29).  One launch with gather CTAs that scan the origins themselves: 65
 // (every CTA re-reads all origins), and with the fill gated behind the gather CTAs' reads 81 -- a
 // read issued behind the saturating write stream takes ~10 us, so the passes gain nothing from
 // sharing a launch; the fill alone runs at 4.4 TB/s.
@@ -1005,15 +652,16 @@ cudaError_t launch_entries(const EntryArgs& a, int64_t cnt, const int64_t* y, co
     return cudaGetLastError();
 }
 
-int blocks_zero_mode() {
-    static const int mode = [] {
-        const char* e = getenv("PCB_C5_ZERO");
-        return e ? std::max(0, std::min(6, atoi(e))) : 5;
+bool blocks_two_streams() {
+    static const bool two = [] {
+        const char* e = getenv("PCB_BLOCKS_STREAMS");
+        return e ? atoi(e) != 1 : true;
     }();
-    return mode;
+    return two;
 }
 
-int64_t blocks_scratch_ints(int32_t nblk) { return 2 + (int64_t)nblk + (int64_t)nblk * (BT_CAP + 1) + nblk; }
+// int32 scratch: [0] the scan's counter, [4, 4 + 16 nblk) its records (BR_WORDS int64 per block)
+int64_t blocks_scratch_ints(int32_t nblk) { return 4 + 2 * (int64_t)BR_WORDS * nblk; }
 
 cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_origin, const int64_t* s_origin,
                           const int32_t* bshape_host, double* out, int32_t* bad, int32_t* scratch, int phase,
@@ -1028,15 +676,6 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
         const char* e = getenv("PCB_BLOCK_CAP");
         return e ? std::max(1, std::min(BT_CAP, atoi(e))) : 16;
     }();
-    // zero blocks (blocks_zero_mode, PCB_C5_ZERO): 0 = TMA bulk copies of a zero tile inside the
-    // classify pass, 1 = 16-byte stores there, 2 = one memset of the whole output before it, 3 =
-    // listed by the classify pass and written by k_blocks_zero on a second stream while the gather
-    // runs, 4 = the memset on a second stream while the classify pass runs, the gather after both.
-    // Measured at config 5 (4096 blocks, 4031 zero): modes 0/1/2/3/4 61.4 / 63.6 / 64.7 / 59.2 /
-    // 73.7 us -- the classify and gather passes are chains of dependent loads and slow down beside
-    // a concurrent zero stream (gather 24 -> 42 us in mode 3, classify 18 -> 54 us in mode 4), so the
-    // default (0) keeps the passes apart.
-    const int zero_mode = blocks_zero_mode();
     const size_t smem = sizeof(double) * (size_t)cap * (size_t)(npx + win) + sizeof(int) * (size_t)npx +
                         (size_t)npx * (1 + BT_NZ) + 16;
     const int bs1 = a.D > 1 ? bshape_host[1] : 1, bs2 = a.D > 2 ? bshape_host[2] : 1;
@@ -1045,64 +684,28 @@ cudaError_t launch_blocks(const EntryArgs& a, int32_t nblk, const int64_t* t_ori
         k_blocks<<<148 * 16, 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape_host[0], bs1, bs2, out, bad);
         return cudaGetLastError();
     }
-    if (zero_mode >= 5) {
-        // phase 0: the blocks that need terms (scan, then search + gather); phase 2: the zero fill (mode
-        // 5: on a second stream beside phase 0; mode 6: after it on the same stream)
-        if (phase == 1) return cudaSuccess;
+    if (phase == 1) {  // the zero fill
         static const int zvar = [] {  // zero_block variant (A/B)
             const char* e = getenv("PCB_C5_ZVAR");
             return e ? std::max(0, std::min(2, atoi(e))) : 0;
         }();
-        if (phase == 2) {
-            static const int zctas = [] {  // zero-fill CTAs per SM (0: one warp per block)
-                const char* e = getenv("PCB_C5_ZCTAS");
-                return e ? std::max(0, std::min(8, atoi(e))) : 0;
-            }();
-            const int64_t full = (nblk + BC_WARPS - 1) / BC_WARPS;
-            const unsigned zgrid = (unsigned)(zctas > 0 ? std::min<int64_t>(full, 148LL * zctas) : full);
-            k_blocks_zfill<<<zgrid, 32 * BC_WARPS, 0, st>>>(a, nblk, t_origin, s_origin, bshape_host[0], bs1, bs2, out,
-                                                           zvar);
-            return cudaGetLastError();
-        }
-        cudaError_t e = cudaMemsetAsync(scratch, 0, 2 * sizeof(int32_t), st);
-        if (e != cudaSuccess) return e;
-        int64_t* rec = reinterpret_cast<int64_t*>(scratch + 4);  // blocks_scratch_ints covers 4 + 16 nblk ints
-        k_blocks_scan<<<(unsigned)((nblk + 255) / 256), 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape_host[0], bs1,
-                                                                      bs2, scratch, rec);
-        if (smem > 36 * 1024) {  // (static shared memory takes ~11 KB of the default 48)
-            e = cudaFuncSetAttribute(k_blocks_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-        }
-        const int per_sm = std::max<int>(1, std::min<int>(6, (int)((220 * 1024) / (smem + 12 * 1024))));
-        const int grid = (int)std::min<int64_t>(nblk, 148LL * per_sm);
-        k_blocks_fused<<<grid, 256, smem, st>>>(a, nblk, bshape_host[0], bs1, bs2, cap, out, bad, scratch, rec);
+        const unsigned zgrid = (unsigned)((nblk + BC_WARPS - 1) / BC_WARPS);
+        k_blocks_zfill<<<zgrid, 32 * BC_WARPS, 0, st>>>(a, nblk, t_origin, s_origin, bshape_host[0], bs1, bs2, out, zvar);
         return cudaGetLastError();
     }
-    if (phase == 2) {  // the zero writes on a second stream: mode 4 the memset of the whole output
-                       // (beside phase 0), mode 3 the listed zero blocks (beside phase 1)
-        if (zero_mode == 4) return cudaMemsetAsync(out, 0, sizeof(double) * (size_t)nblk * (size_t)(npx * npx), st);
-        if (zero_mode != 3) return cudaSuccess;
-        k_blocks_zero<<<(unsigned)((nblk + BC_WARPS - 1) / BC_WARPS), 32 * BC_WARPS, 0, st>>>(scratch, nblk, cap, (int)npx,
-                                                                                          out);
-        return cudaGetLastError();
-    }
-    if (phase == 0) {  // classify (zero blocks written or listed here), listing the others for phase 1
-        cudaError_t e = cudaMemsetAsync(scratch, 0, 2 * sizeof(int32_t), st);
-        if (e == cudaSuccess && zero_mode == 2)  // (mode 4: phase 2 on the second stream)
-            e = cudaMemsetAsync(out, 0, sizeof(double) * (size_t)nblk * (size_t)(npx * npx), st);
-        if (e != cudaSuccess) return e;
-        k_blocks_classify<<<(unsigned)((nblk + BC_WARPS - 1) / BC_WARPS), 32 * BC_WARPS, 0, st>>>(
-            a, nblk, t_origin, s_origin, bshape_host[0], bs1, bs2, cap, out, scratch, zero_mode);
-        return cudaGetLastError();
-    }
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_blocks_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // phase 0: the blocks that need terms (scan, then search + gather)
+    cudaError_t e = cudaMemsetAsync(scratch, 0, 4 * sizeof(int32_t), st);
+    if (e != cudaSuccess) return e;
+    int64_t* rec = reinterpret_cast<int64_t*>(scratch + 4);
+    k_blocks_scan<<<(unsigned)((nblk + 255) / 256), 256, 0, st>>>(a, nblk, t_origin, s_origin, bshape_host[0], bs1, bs2,
+                                                                  scratch, rec);
+    if (smem > 36 * 1024) {  // (static shared memory takes ~11 KB of the default 48)
+        e = cudaFuncSetAttribute(k_blocks_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    const int per_sm = std::max<int>(1, (int)((220 * 1024) / (smem + 2048)));
-    const int grid = (int)std::min<int64_t>(nblk, 148LL * std::min(per_sm, 4));
-    k_blocks_gather<<<grid, 256, smem, st>>>(a, t_origin, s_origin, bshape_host[0], bs1, bs2, cap, out, bad, scratch,
-                                              nblk);
+    const int per_sm = std::max<int>(1, std::min<int>(6, (int)((220 * 1024) / (smem + 12 * 1024))));
+    const int grid = (int)std::min<int64_t>(nblk, 148LL * per_sm);
+    k_blocks_fused<<<grid, 256, smem, st>>>(a, nblk, bshape_host[0], bs1, bs2, cap, out, bad, scratch, rec);
     return cudaGetLastError();
 }
 

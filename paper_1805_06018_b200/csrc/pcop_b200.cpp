@@ -1691,6 +1691,18 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             if (!g.chains.empty()) g.chain_slots.upload(std::vector<int32_t>(g.chains.begin(), g.chains.end()));
     }
     op->a_pool.upload(apool.empty() ? std::vector<double>(1, 0.0) : apool);
+    // PCB_SLOT_FAM=1 (A/B): the column pass takes a group's terms family by family, so the members of
+    // a row family read their shared S rows within ~64 vectors of each other (L2 hits on the second
+    // read).  Measured: c3 cols 3.45 -> 3.42 ms, c4 / c2 unchanged (and streaming stores of T changed
+    // nothing): the pass is latency-bound, not bound by its 18% of excess DRAM reads.  Off by default.
+    if (const char* e = getenv("PCB_SLOT_FAM"))
+        if (atoi(e) != 0)
+            for (Group& g : op->groups)
+                std::stable_sort(g.terms.begin(), g.terms.end(), [&](int x, int y) {
+                    const int fx = op->term_fam[x] < 0 ? INT32_MAX : op->term_fam[x];
+                    const int fy = op->term_fam[y] < 0 ? INT32_MAX : op->term_fam[y];
+                    return fx < fy;
+                });
     for (Group& g : op->groups) g.slots.upload(std::vector<int32_t>(g.terms.begin(), g.terms.end()));
     // 1 / prod P per term (its group's FFT size); the last slot serves the global pseudo term
     std::vector<double> term_scale(op->terms.size() + 1, 1.0);
@@ -2841,33 +2853,22 @@ static void blocks_common(pcb_op* op, int32_t nblk, const int64_t* d_t, const in
     op->st_flag.ensure(1);
     op->st_blk.ensure((size_t)blocks_scratch_ints(nblk));
     PCB_CK(cudaMemsetAsync(op->st_flag.p, 0, 4, st));
-    // phase 0 classifies the blocks, phase 1 gathers the ones with candidate terms, phase 2 writes
-    // the all-zero ones on a second stream beside phase 0 (mode 4) or phase 1 (mode 3)
+    // phase 0: the blocks that need terms (scan, candidate search + gather); phase 1: the exact-zero
+    // blocks, independent of phase 0, on a second stream beside it
     auto phase = [&](int ph, cudaStream_t s2) {
         return launch_blocks(entry_args(op), nblk, d_t, d_s, bs, d_out, op->st_flag.p, op->st_blk.p, ph, s2);
     };
-    const int zm = blocks_zero_mode();
-    const bool aux = zm == 3 || zm == 4 || zm == 5;
-    if (aux && !op->s_aux) PCB_CK(cudaStreamCreateWithFlags(&op->s_aux, cudaStreamNonBlocking));
-    auto fork = [&] {
+    if (blocks_two_streams()) {
+        if (!op->s_aux) PCB_CK(cudaStreamCreateWithFlags(&op->s_aux, cudaStreamNonBlocking));
         PCB_CK(cudaEventRecord(op_event(op, 6), st));
         PCB_CK(cudaStreamWaitEvent(op->s_aux, op_event(op, 6), 0));
-        launch(op, op->s_aux, "blocks(zero)", [&] { return phase(2, op->s_aux); });
+        launch(op, op->s_aux, "blocks(zero)", [&] { return phase(1, op->s_aux); });
         PCB_CK(cudaEventRecord(op_event(op, 7), op->s_aux));
-    };
-    if (zm >= 5) {
-        // 5 (default): the zero fill on a second stream beside the blocks that need terms; 6: one stream
-        if (zm == 5) fork();
         launch(op, st, "blocks(gather)", [&] { return phase(0, st); });
-        if (zm == 5) PCB_CK(cudaStreamWaitEvent(st, op_event(op, 7), 0));
-        else launch(op, st, "blocks(zero)", [&] { return phase(2, st); });
+        PCB_CK(cudaStreamWaitEvent(st, op_event(op, 7), 0));
     } else {
-    if (zm == 4) fork();
-    launch(op, st, "blocks(classify)", [&] { return phase(0, st); });
-    if (zm == 3) fork();
-    if (zm == 4) PCB_CK(cudaStreamWaitEvent(st, op_event(op, 7), 0));  // the memset before the gather's writes
-    launch(op, st, "blocks(gather)", [&] { return phase(1, st); });
-    if (zm == 3) PCB_CK(cudaStreamWaitEvent(st, op_event(op, 7), 0));
+        launch(op, st, "blocks(gather)", [&] { return phase(0, st); });
+        launch(op, st, "blocks(zero)", [&] { return phase(1, st); });
     }
     if (host_check) {
         int32_t bad = 0;
