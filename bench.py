@@ -476,6 +476,16 @@ def main():
     e2e_value = e2e(Fh.numpy(), Gh.numpy(), reps)
     Gp = np.empty_like(F_host)
     e2e_pageable = e2e(F_host, Gp, max(2, reps // 2))
+    # the same caller-owned numpy buffers page-locked in place (pcb_host_register): what a binding that
+    # reuses its std::vector buffers gets; the registration itself is timed separately
+    t0 = time.perf_counter()
+    reg = lib.host_registered(F_host, Gp)
+    reg.__enter__()
+    reg_ms = (time.perf_counter() - t0) * 1e3
+    try:
+        e2e_registered = e2e(F_host, Gp, max(2, reps // 2))
+    finally:
+        reg.__exit__(None, None, None)
 
     # ---- secondary: shard-by-RHS weak scaling (every rank its own B vectors, no collective) ----
     rhs = None
@@ -517,7 +527,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(B * N * 8 * world),
                     "d2h_bytes_per_step": int(B * N * 8 * world),
                     "path": "pcb_apply_batch, pinned host buffers (H2D + kernels + reduce + D2H)",
-                    "pageable_value": e2e_pageable},
+                    "pageable_value": e2e_pageable, "registered_value": e2e_registered, "register_ms": reg_ms},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": dom_fam, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs, burst copy)",

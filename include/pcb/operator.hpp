@@ -63,6 +63,25 @@ struct pinned_allocator {
 };
 using pinned_vector = std::vector<double, pinned_allocator<double>>;
 
+// Page-locks a buffer the caller owns for the guard's lifetime (pcb_host_register): an ordinary
+// std::vector<double> that is applied many times then goes straight to the copy engines.
+class host_registration {
+  public:
+    host_registration(const double* p, size_t n) : p_(const_cast<double*>(p)) {
+        if (n == 0) p_ = nullptr;
+        else check(pcb_host_register(p_, static_cast<uint64_t>(n) * sizeof(double)));
+    }
+    explicit host_registration(const std::vector<double>& v) : host_registration(v.data(), v.size()) {}
+    ~host_registration() {
+        if (p_) pcb_host_unregister(p_);
+    }
+    host_registration(const host_registration&) = delete;
+    host_registration& operator=(const host_registration&) = delete;
+
+  private:
+    double* p_;
+};
+
 // A fresh 128-byte NCCL id for pcb_options.nccl_id (shard-by-k with the reduce inside the
 // library): create it on one rank and send it to the others (MPI_Bcast, a file, a socket ...).
 inline std::vector<unsigned char> comm_unique_id() {
@@ -135,6 +154,13 @@ class ProductConvolutionOperator {
         if (static_cast<int64_t>(F.size()) != N * B)
             throw std::invalid_argument(adjoint ? "PCOp::apply_adjoint: shape mismatch" : "PCOp::apply: shape mismatch");
         G.resize(F.size());
+        check(adjoint ? pcb_apply_adjoint_batch(op_, B, F.data(), G.data()) : pcb_apply_batch(op_, B, F.data(), G.data()));
+    }
+    // caller-owned output (G is not resized: buffers page-locked with host_registration stay put)
+    void apply_batch(const std::vector<double>& F, std::vector<double>& G, int32_t B, bool adjoint = false) const {
+        const int64_t N = domain_.num_points();
+        if (static_cast<int64_t>(F.size()) != N * B || G.size() != F.size())
+            throw std::invalid_argument(adjoint ? "PCOp::apply_adjoint: shape mismatch" : "PCOp::apply: shape mismatch");
         check(adjoint ? pcb_apply_adjoint_batch(op_, B, F.data(), G.data()) : pcb_apply_batch(op_, B, F.data(), G.data()));
     }
     std::vector<double> apply_adjoint_batch(const std::vector<double>& F, int32_t B) const {

@@ -320,6 +320,12 @@ PCB_API pcb_status pcb_debug_guard_check(int64_t* n_regions, int64_t* n_bad_byte
  * (operator.hpp) wraps these for std::vector. */
 PCB_API pcb_status pcb_host_alloc(uint64_t bytes, void** out);
 PCB_API pcb_status pcb_host_free(void* p);
+/* Page-lock a buffer the caller already owns (a std::vector the reference code passes to apply(),
+ * operators.cpp:39-49) so later host-buffer calls on it take the copy-engine path too.  Locking costs
+ * about as much as a few applies: register buffers that are reused, and unregister them before they
+ * are freed.  PCB_EINVAL if the range is already (or, for unregister, not) registered. */
+PCB_API pcb_status pcb_host_register(void* p, uint64_t bytes);
+PCB_API pcb_status pcb_host_unregister(void* p);
 
 /* Number of kernels this library has launched in the process (all handles). */
 PCB_API long long pcb_launch_count(void);

@@ -89,9 +89,12 @@ __global__ void k_block_direct(EntryArgs a, int32_t nblk, const int64_t* __restr
                                const int64_t* __restrict__ t_hi, const int64_t* __restrict__ s_lo,
                                const int64_t* __restrict__ s_hi, const int64_t* __restrict__ f_off,
                                const int64_t* __restrict__ g_off, const double* __restrict__ f,
-                               double* __restrict__ g, int adjoint, int32_t* bad) {
+                               double* __restrict__ g, int adjoint, int32_t* bad, int32_t blk0, uint32_t tiles) {
+    // 1-D grid: CTA = (block, tile of 256 outputs) -- batched H-matrix rounds pass more blocks than
+    // grid.y allows
     const int D = a.D;
-    const int blk = blockIdx.y;
+    const int blk = blk0 + (int)(blockIdx.x / tiles);
+    const uint32_t tile = blockIdx.x % tiles;
     if (blk >= nblk) return;
     int64_t text[3] = {1, 1, 1}, sext[3] = {1, 1, 1}, tcnt = 1, scnt = 1;
     for (int i = 0; i < D; ++i) {
@@ -100,7 +103,7 @@ __global__ void k_block_direct(EntryArgs a, int32_t nblk, const int64_t* __restr
         tcnt *= text[i];
         scnt *= sext[i];
     }
-    const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t o = (int64_t)tile * blockDim.x + threadIdx.x;
     int64_t pt[3] = {0, 0, 0};
     {
         int64_t r = o < tcnt ? o : 0;
@@ -727,9 +730,16 @@ cudaError_t launch_block_direct(const EntryArgs& a, int32_t nblk, int64_t max_t,
                                 const int64_t* g_off, const double* f, double* g, int adjoint, int32_t* bad,
                                 cudaStream_t st) {
     if (nblk <= 0) return cudaSuccess;
-    dim3 grid((unsigned)((max_t + 255) / 256), (unsigned)nblk);
-    k_block_direct<<<grid, 256, 0, st>>>(a, nblk, t_lo, t_hi, s_lo, s_hi, f_off, g_off, f, g, adjoint, bad);
-    return cudaGetLastError();
+    const int64_t tiles = std::max<int64_t>(1, (max_t + 255) / 256);
+    const int64_t per = std::max<int64_t>(1, ((1LL << 31) - 1) / tiles);  // blocks per launch (grid.x limit)
+    for (int64_t b0 = 0; b0 < nblk; b0 += per) {
+        const int64_t nb = std::min<int64_t>(per, nblk - b0);
+        k_block_direct<<<(unsigned)(nb * tiles), 256, 0, st>>>(a, nblk, t_lo, t_hi, s_lo, s_hi, f_off, g_off, f, g, adjoint,
+                                                               bad, (int32_t)b0, (uint32_t)tiles);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 int64_t probe_sums_scratch(int D, const int32_t* n, int32_t q) {

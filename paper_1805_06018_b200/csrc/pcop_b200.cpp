@@ -2084,6 +2084,31 @@ PCB_API pcb_status pcb_host_free(void* p) {
     return PCB_OK;
 }
 
+PCB_API pcb_status pcb_host_register(void* p, uint64_t bytes) {
+    if (!p || bytes == 0) {
+        set_err("pcb_host_register: null buffer");
+        return PCB_EINVAL;
+    }
+    const cudaError_t e = cudaHostRegister(p, (size_t)bytes, cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        set_err(std::string("cudaHostRegister failed: ") + cudaGetErrorString(e));
+        return e == cudaErrorMemoryAllocation ? PCB_ENOMEM : e == cudaErrorHostMemoryAlreadyRegistered ? PCB_EINVAL : PCB_ECUDA;
+    }
+    return PCB_OK;
+}
+
+PCB_API pcb_status pcb_host_unregister(void* p) {
+    if (!p) return PCB_OK;
+    const cudaError_t e = cudaHostUnregister(p);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        set_err(std::string("cudaHostUnregister failed: ") + cudaGetErrorString(e));
+        return e == cudaErrorHostMemoryNotRegistered ? PCB_EINVAL : PCB_ECUDA;
+    }
+    return PCB_OK;
+}
+
 PCB_API pcb_status pcb_comm_unique_id(void* id128) {
     if (!id128) {
         set_err("pcb_comm_unique_id: null output");

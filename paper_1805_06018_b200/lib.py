@@ -35,7 +35,7 @@ EXPORTS = ["pcb_default_options", "pcb_last_error", "pcb_create", "pcb_destroy",
            "pcb_hmatrix_destroy", "pcb_hmatrix_get_info", "pcb_hmatrix_tree", "pcb_hmatrix_block",
            "pcb_hmatrix_admissible", "pcb_hmatrix_matvec", "pcb_hmatrix_save", "pcb_hmatrix_load",
            "pcb_comm_unique_id", "pcb_plan_shards", "pcb_debug_guard_check", "pcb_estimator_create_ex",
-           "pcb_host_alloc", "pcb_host_free", "pcb_create_multi"]
+           "pcb_host_alloc", "pcb_host_free", "pcb_create_multi", "pcb_host_register", "pcb_host_unregister"]
 RNG = {"mt19937": 0, "philox": 1}
 REDUCE = {"none": 0, "all": 1, "root": 2}
 PARTITION = {"cost": 0, "count": 1}
@@ -155,6 +155,8 @@ def load():
     L.pcb_debug_guard_check.argtypes = [P_i64, P_i64]
     L.pcb_host_alloc.argtypes = [ctypes.c_uint64, ctypes.POINTER(vp)]
     L.pcb_host_free.argtypes = [vp]
+    L.pcb_host_register.argtypes = [vp, ctypes.c_uint64]
+    L.pcb_host_unregister.argtypes = [vp]
     L.pcb_plan_shards.argtypes = [i32, P_i64, P_i64, i32, P_i64, P_i64, ctypes.POINTER(vp), P_i64, P_i64,
                                   ctypes.POINTER(vp), i32, i32, vp, vp]
     for n in EXPORTS:
@@ -189,6 +191,27 @@ def comm_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     check(load().pcb_comm_unique_id(buf))
     return buf.raw
+
+
+class host_registered:
+    """Context manager: page-lock numpy arrays the caller owns (pcb_host_register) so the host-buffer
+    calls on them take the copy-engine path; unregistered on exit."""
+
+    def __init__(self, *arrays):
+        self._arrays = [a for a in arrays if a.size]
+        self._done = []
+
+    def __enter__(self):
+        for a in self._arrays:
+            check(load().pcb_host_register(a.ctypes.data, a.nbytes))
+            self._done.append(a)
+        return self
+
+    def __exit__(self, *exc):
+        for a in reversed(self._done):
+            load().pcb_host_unregister(a.ctypes.data)
+        self._done = []
+        return False
 
 
 def guard_check():

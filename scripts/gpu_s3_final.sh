@@ -11,10 +11,10 @@ for cfg in c3 c4; do
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
       --log-file $O/launches_$cfg.csv $CMD > $O/ncu_launch_$cfg.log 2>&1
   echo "launch list $cfg rc=$?"
-  python scripts/launch_share.py $O/launches_$cfg.csv 2 > $O/${cfg}_launches_share.txt
+  python scripts/launch_share.py $O/launches_$cfg.csv 5 > $O/${cfg}_launches_share.txt
 done
-python scripts/traffic_json.py $O/launches_c3.csv 2 $O/traffic_c3_local.json 64
-python scripts/traffic_json.py $O/launches_c4.csv 2 $O/traffic_c4_local.json 8
+python scripts/traffic_json.py $O/launches_c3.csv 5 $O/traffic_c3_local.json 64
+python scripts/traffic_json.py $O/launches_c4.csv 5 $O/traffic_c4_local.json 8
 cp $O/traffic_c3_local.json $O/traffic_c4_local.json profiles/   # bench reads profiles/traffic_*.json
 CMD="python bench.py --config c3 --profile-only --steps 1 --warmup 3"
 cap() { # tag regex

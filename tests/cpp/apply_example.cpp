@@ -81,6 +81,15 @@ int main() {
             for (int i = 0; i < n * n; ++i)
                 if (pg[i] != ref[i]) return 5;
             std::printf("pinned_vector apply: bitwise equal to the pageable path\n");
+            // an ordinary std::vector page-locked in place for the guard's lifetime
+            std::vector<double> rf(f), rg(f.size());
+            {
+                pcb::host_registration lf(rf), lg(rg);
+                pop.apply_batch(rf, rg, 1);
+            }
+            for (int i = 0; i < n * n; ++i)
+                if (rg[i] != ref[i]) return 6;
+            std::printf("host_registration apply: bitwise equal\n");
         }
         // reference error behaviour
         pcb::ProductConvolutionOperator op(dom, w, phi);

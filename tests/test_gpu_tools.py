@@ -116,6 +116,15 @@ def test_host_pipeline_many_sub_batches(gpu, cfg, B):
         # repeated calls replay the cached graphs (same keys every call)
         again = op.apply_adjoint_batch(F) if adj else op.apply_batch(F)
         assert np.array_equal(again, want)
+        # caller-owned buffers page-locked in place (pcb_host_register): the copy-engine path
+        G = np.empty_like(F)
+        with lib.host_registered(F, G):
+            lib.check(fn(op._h, B, F.ctypes.data, G.ctypes.data))
+            with pytest.raises(lib.PcbError):  # already registered
+                lib.check(lib.load().pcb_host_register(F.ctypes.data, F.nbytes))
+        assert np.array_equal(G, want)
+        with pytest.raises(lib.PcbError):  # not registered any more
+            lib.check(lib.load().pcb_host_unregister(F.ctypes.data))
     op.close()
 
 
