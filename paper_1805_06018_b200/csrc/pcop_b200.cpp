@@ -16,6 +16,7 @@
 //   LOCAL:  per-term grid P_k >= ext(X_k) + ext(K_k) + 1 (the reference's own
 //           padding rule on the trimmed boxes), s_k = X_k.lo + K_k.lo; each
 //           term's cropped output is gathered into Omega in ascending k.
+#include <emmintrin.h>
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -316,6 +317,7 @@ struct pcb_op {
     cudaEvent_t ev_x[8] = {};       // bridging / completion events (op_event)
     cudaEvent_t ev_io[8] = {};      // host pipeline
     double host_sub_mb = 16.0;
+    double host_sub_mb_pg = 32.0;  // ... when a caller buffer is pageable (bounce copies by host threads)
     double* bounce = nullptr;       // pinned bounce slots for pageable host buffers (2 in, 2 out)
     size_t bounce_n = 0;
     // shard-by-k communicator (comm.cpp): the partial outputs are summed inside every apply
@@ -2199,6 +2201,12 @@ PCB_API pcb_status pcb_create(int32_t dim, const int64_t* dom_lo, const int64_t*
 
         op->host_sub_mb = opt.host_sub_mb > 0 ? (double)opt.host_sub_mb : 16.0;
         if (const char* e = getenv("PCB_SUB_MB")) op->host_sub_mb = std::max(1.0, atof(e));
+        // pageable buffers (bounce copies by the host pool): measured with the non-temporal copies
+        // (scripts/pageable_sub.py; ms per batch at c3 / c4): 8 MiB 23.6 / 9.6, 16 MiB 24.5 / 9.6,
+        // 32 MiB 22.5 / 9.6, 64 MiB 23.1 / 10.2, 128 MiB 23.8 / 15.7 (c4: one unpipelined sub-batch).
+        // With ordinary stores 16 MiB took 53 ms at c3 and 128 MiB 32 ms (scripts/pageable_sweep.py).
+        op->host_sub_mb_pg = opt.host_sub_mb > 0 ? (double)opt.host_sub_mb : std::max(32.0, op->host_sub_mb);
+        if (const char* e = getenv("PCB_SUB_MB_PAGEABLE")) op->host_sub_mb_pg = std::max(1.0, atof(e));
         if (const char* e = getenv("PCB_COMM_CHUNKS")) op->comm_chunks = std::max(1, atoi(e));
         if (opt.reduce < PCB_REDUCE_NONE || opt.reduce > PCB_REDUCE_ROOT) fail(PCB_EINVAL, "pcb_create: bad reduce");
         if (opt.partition != PCB_PARTITION_COST && opt.partition != PCB_PARTITION_COUNT)
@@ -2299,6 +2307,7 @@ PCB_API pcb_status pcb_create_multi(int32_t dim, const int64_t* dom_lo, const in
         op->r = s0->r;
         op->mode = s0->mode;
         op->host_sub_mb = s0->host_sub_mb;
+        op->host_sub_mb_pg = s0->host_sub_mb_pg;
         op->sbuf.resize(ndev);
         op->d_parts_s.assign(ndev, nullptr);
         for (int s2 = 0; s2 < ndev; ++s2) {
@@ -2650,6 +2659,32 @@ struct HostCopy {
     size_t bytes;
 };
 
+// memcpy with non-temporal stores (SSE2 movntpd): the bounce copies stream 1 GiB per c3 step through
+// host DRAM, and ordinary stores read every destination line first (write-allocate) -- a quarter of
+// the traffic of a path that is host-DRAM-bound.  PCB_HOST_NT=0: plain memcpy.
+static void host_copy_piece(void* dst, const void* src, size_t bytes) {
+    static const bool nt = [] {
+        const char* e = std::getenv("PCB_HOST_NT");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    if (!nt || (reinterpret_cast<uintptr_t>(dst) & 15) != 0 || bytes < 4096) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    double* d = static_cast<double*>(dst);
+    const double* s = static_cast<const double*>(src);
+    const size_t n64 = bytes / 64;
+    for (size_t i = 0; i < n64; ++i, d += 8, s += 8) {
+        const __m128d a = _mm_loadu_pd(s), b = _mm_loadu_pd(s + 2), c = _mm_loadu_pd(s + 4), e = _mm_loadu_pd(s + 6);
+        _mm_stream_pd(d, a);
+        _mm_stream_pd(d + 2, b);
+        _mm_stream_pd(d + 4, c);
+        _mm_stream_pd(d + 6, e);
+    }
+    _mm_sfence();
+    if (bytes % 64) std::memcpy(d, s, bytes % 64);
+}
+
 class HostPool {
   public:
     static HostPool& get() {
@@ -2669,7 +2704,7 @@ class HostPool {
             HostCopy c = q_.back();
             q_.pop_back();
             lk.unlock();
-            std::memcpy(c.dst, c.src, c.bytes);
+            host_copy_piece(c.dst, c.src, c.bytes);
             lk.lock();
             --pending_;
         }
@@ -2698,7 +2733,7 @@ class HostPool {
             HostCopy c = q_.back();
             q_.pop_back();
             lk.unlock();
-            std::memcpy(c.dst, c.src, c.bytes);
+            host_copy_piece(c.dst, c.src, c.bytes);
             lk.lock();
             if (--pending_ == 0) done_.notify_all();
         }
@@ -2739,7 +2774,9 @@ static pcb_status apply_host_common(pcb_op* op, bool adjoint, int32_t B, const d
         // kernel batch; the first and the last are half size so the unoverlapped fill (first H2D) and
         // drain (last D2H) stay short
         const double vec_mb = (double)op->N * 8.0 / (1 << 20);
-        const int per = (int)std::max(2.0, std::floor(op->host_sub_mb / vec_mb));
+        const bool pin_f = host_pinned(F), pin_g = host_pinned(G);
+        const double sub_mb = pin_f && pin_g ? op->host_sub_mb : op->host_sub_mb_pg;
+        const int per = (int)std::max(2.0, std::floor(sub_mb / vec_mb));
         std::vector<int> sizes;
         if (B <= per) {
             sizes.push_back(B);
@@ -2758,7 +2795,6 @@ static pcb_status apply_host_common(pcb_op* op, bool adjoint, int32_t B, const d
         const size_t slot = (size_t)mx * (size_t)op->N;
         op->st_in.ensure(2 * slot);
         op->st_out.ensure(2 * slot);
-        const bool pin_f = host_pinned(F), pin_g = host_pinned(G);
         if ((!pin_f || !pin_g) && op->bounce_n < 4 * slot) {
             if (op->bounce) cudaFreeHost(op->bounce);
             op->bounce = nullptr;
