@@ -12,6 +12,12 @@
 //   * the per-block Gaussian probes are the reference's own streams (mt19937_64 seeded by the block
 //     position, std::normal_distribution), so the sampled ranges are the reference's.
 // Householder QR and one-sided Jacobi SVD are written here (the reference uses Eigen's).
+#include <exception>
+#include <thread>
+#include <atomic>
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -221,6 +227,15 @@ int64_t box_index(const pcb_hmatrix* h, const CNode& n, const int64_t* p) {
 
 // block_apply (hmatrix.cpp:116-136), batched: job j applies the (t_j, s_j) block (or its adjoint)
 // to x_j given in cluster order; returns each output in cluster order.
+// PCB_HM_TIMING=1: wall-clock split of an assembly, printed by pcb_hmatrix_assemble (stderr)
+struct HmTimes {
+    double pack = 0, gpu = 0, unpack = 0, qr = 0, svd = 0, probes = 0, form = 0, entries = 0, aca_host = 0;
+};
+HmTimes g_hm_times;
+inline double hm_now() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 struct ApplyJob {
     int32_t t, s;
     bool adjoint;
@@ -251,6 +266,7 @@ std::vector<std::vector<double>> block_apply_batch(pcb_op* op, const pcb_hmatrix
             shi.insert(shi.end(), in_n.hi, in_n.hi + h->D);
             ++j1;
         }
+        const double t_pack0 = hm_now();
         std::vector<double> f((size_t)fcnt, 0.0), g((size_t)gcnt, 0.0);
         int64_t fo = 0;
         int64_t p[3];
@@ -263,8 +279,12 @@ std::vector<std::vector<double>> block_apply_batch(pcb_op* op, const pcb_hmatrix
             }
             fo += box_points(h, in_n);
         }
+        const double t_gpu0 = hm_now();
         ck(pcb_apply_block(op, (int32_t)(j1 - j0), tlo.data(), thi.data(), slo.data(), shi.data(), f.data(), g.data(),
                            jobs[j0].adjoint ? 1 : 0));
+        const double t_gpu1 = hm_now();
+        g_hm_times.pack += t_gpu0 - t_pack0;
+        g_hm_times.gpu += t_gpu1 - t_gpu0;
         int64_t go = 0;
         for (size_t j = j0; j < j1; ++j) {
             const ApplyJob& jb = jobs[j];
@@ -276,6 +296,7 @@ std::vector<std::vector<double>> block_apply_batch(pcb_op* op, const pcb_hmatrix
             }
             go += box_points(h, out_n);
         }
+        g_hm_times.unpack += hm_now() - t_gpu1;
         j0 = j1;
     }
     return out;
@@ -390,6 +411,89 @@ void jacobi_svd(std::vector<double> A, int64_t m, int64_t n, std::vector<double>
         for (int64_t i = 0; i < n; ++i) V2[(size_t)(jj * n + i)] = V[(size_t)(j * n + i)];
     }
     V = std::move(V2);
+}
+
+// SVD of a tall A (m x n, m >= n) through its QR factorization: A = Q R (Householder), R = Ur S V^T
+// (one-sided Jacobi on the n x n triangle), U = Q Ur.  The Jacobi sweeps then cost O(n^3) instead of
+// O(m n^2) each -- the randomized route's SVDs were 93% of an assembly (21.4 of 23.0 s at N = 9,216,
+// PCB_HM_TIMING=1) with the sweeps on the tall matrix.
+void tall_svd(std::vector<double> A, int64_t m, int64_t n, std::vector<double>& U, std::vector<double>& sv,
+              std::vector<double>& V) {
+    if (m < 2 * n || n < 2) {
+        jacobi_svd(std::move(A), m, n, U, sv, V);
+        return;
+    }
+    // Householder QR in place: R in the upper triangle, reflectors kept to form Q Ur afterwards
+    std::vector<std::vector<double>> vs((size_t)n);
+    std::vector<double> betas((size_t)n, 0.0);
+    for (int64_t j = 0; j < n; ++j) {
+        double* col = &A[(size_t)(j * m)];
+        double nrm2 = 0.0;
+        for (int64_t i = j; i < m; ++i) nrm2 += col[i] * col[i];
+        const double nrm = std::sqrt(nrm2);
+        if (nrm == 0.0) continue;
+        const double alpha = col[j] >= 0.0 ? -nrm : nrm;
+        std::vector<double> v(col + j, col + m);
+        v[0] -= alpha;
+        const double vn2 = dot(v.data(), v.data(), m - j);
+        if (vn2 == 0.0) continue;
+        const double beta = 2.0 / vn2;
+        for (int64_t c = j; c < n; ++c) {
+            double* yc = &A[(size_t)(c * m)];
+            const double sc = beta * dot(v.data(), yc + j, m - j);
+            for (int64_t i = j; i < m; ++i) yc[i] -= sc * v[(size_t)(i - j)];
+        }
+        vs[(size_t)j] = std::move(v);
+        betas[(size_t)j] = beta;
+    }
+    std::vector<double> Rm((size_t)(n * n), 0.0);
+    for (int64_t c = 0; c < n; ++c)
+        for (int64_t i = 0; i <= c; ++i) Rm[(size_t)(c * n + i)] = A[(size_t)(c * m + i)];
+    std::vector<double> Ur;
+    jacobi_svd(std::move(Rm), n, n, Ur, sv, V);
+    // U = Q [Ur; 0]: apply the reflectors in reverse order to the embedded columns
+    U.assign((size_t)(m * n), 0.0);
+    for (int64_t c = 0; c < n; ++c) std::copy(Ur.begin() + c * n, Ur.begin() + (c + 1) * n, U.begin() + c * m);
+    for (int64_t j = n - 1; j >= 0; --j) {
+        const double beta = betas[(size_t)j];
+        if (beta == 0.0) continue;
+        const std::vector<double>& v = vs[(size_t)j];
+        for (int64_t c = 0; c < n; ++c) {
+            double* uc = &U[(size_t)(c * m)];
+            const double sc = beta * dot(v.data(), uc + j, m - j);
+            for (int64_t i = j; i < m; ++i) uc[i] -= sc * v[(size_t)(i - j)];
+        }
+    }
+}
+
+// fn(i) for i in [0, n) on the host's cores (the per-block factorizations are independent)
+template <typename F>
+void parallel_for(size_t n, F fn) {
+    static const int nthreads = [] {
+        int t = (int)std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
+        if (const char* e = std::getenv("PCB_HOST_THREADS")) t = std::max(1, std::atoi(e));
+        return t;
+    }();
+    if (n < 2 || nthreads < 2) {
+        for (size_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::atomic<size_t> next{0};
+    std::exception_ptr err;
+    std::mutex mu;
+    auto work = [&] {
+        try {
+            for (size_t i; (i = next.fetch_add(1)) < n;) fn(i);
+        } catch (...) {
+            std::lock_guard<std::mutex> lk(mu);
+            if (!err) err = std::current_exception();
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nthreads && (size_t)t < n; ++t) th.emplace_back(work);
+    work();
+    for (auto& t : th) t.join();
+    if (err) std::rethrow_exception(err);
 }
 
 // ---- compression ------------------------------------------------------------------------------
@@ -563,6 +667,7 @@ void compress_randomized_batch(pcb_op* op, const pcb_hmatrix* h, std::vector<HBl
     }
     const int s_probes = 4;
     for (;;) {
+        const double t_round = hm_now();
         std::vector<ApplyJob> jobs;
         std::vector<size_t> who;
         std::vector<int> nprobe;
@@ -580,6 +685,7 @@ void compress_randomized_batch(pcb_op* op, const pcb_hmatrix* h, std::vector<HBl
             nprobe.push_back((int)cnt);
         }
         if (who.empty()) break;
+        g_hm_times.probes += hm_now() - t_round;
         const std::vector<std::vector<double>> ys = block_apply_batch(op, h, jobs);
         size_t o = 0;
         for (size_t w = 0; w < who.size(); ++w) {
@@ -599,7 +705,9 @@ void compress_randomized_batch(pcb_op* op, const pcb_hmatrix* h, std::vector<HBl
                 o += (size_t)nprobe[w];
                 continue;
             }
+            const double t_qr = hm_now();
             r.Q = householder_q(Y, r.nt, r.l);
+            g_hm_times.qr += hm_now() - t_qr;
             r.qc = std::min(r.nt, r.l);
             if (!resid) {
                 r.active = false;
@@ -633,22 +741,31 @@ void compress_randomized_batch(pcb_op* op, const pcb_hmatrix* h, std::vector<HBl
                                     std::vector<double>(r.Q.begin() + k * r.nt, r.Q.begin() + (k + 1) * r.nt)});
     }
     const std::vector<std::vector<double>> bt = block_apply_batch(op, h, jobs);
-    size_t o = 0;
-    for (R& r : rs) {
+    std::vector<size_t> off(rs.size(), 0);  // first adjoint sample of each block
+    {
+        size_t o = 0;
+        for (size_t i = 0; i < rs.size(); ++i) {
+            off[i] = o;
+            if (!rs[i].zero) o += (size_t)rs[i].qc;
+        }
+    }
+    const double t_svd = hm_now();
+    parallel_for(rs.size(), [&](size_t bi) {
+        R& r = rs[bi];
+        const size_t o = off[bi];
         HBlock& b = *r.b;
         if (r.zero) {
             b.B = Mat(r.nt, 0);
             b.C = Mat(0, r.ns);
             b.capped = false;
-            continue;
+            return;
         }
         // A := Bt (ns x qc, column-major) = B^T;  Bt = U S V^T  =>  B = V S U^T
         std::vector<double> At((size_t)(r.ns * r.qc));
         for (int64_t k = 0; k < r.qc; ++k) std::copy(bt[o + (size_t)k].begin(), bt[o + (size_t)k].end(), At.begin() + k * r.ns);
-        o += (size_t)r.qc;
         // qc <= max_rank <= ns, so Bt is tall
         std::vector<double> U, sv, V;
-        jacobi_svd(At, r.ns, r.qc, U, sv, V);
+        tall_svd(std::move(At), r.ns, r.qc, U, sv, V);
         // B = Vb S Ub^T with Vb (qc x n) = V, Ub (ns x n) = U
         const int64_t ns_sv = (int64_t)sv.size();
         int64_t rank;
@@ -681,7 +798,8 @@ void compress_randomized_batch(pcb_op* op, const pcb_hmatrix* h, std::vector<HBl
             for (int64_t j = 0; j < r.ns; ++j) b.C(k, j) = U[(size_t)(k * r.ns + j)];
         }
         b.capped = capped;
-    }
+    });
+    g_hm_times.svd += hm_now() - t_svd;
 }
 
 void compress(pcb_op* op, pcb_hmatrix* h, std::vector<HBlock*>& blks) {
@@ -827,8 +945,19 @@ PCB_API pcb_status pcb_hmatrix_assemble(pcb_op* op, double tol, int32_t leaf_cap
         rec(0, 0);
         std::vector<HBlock*> lr, dn;
         for (HBlock& b : h->blocks) (b.low_rank ? lr : dn).push_back(&b);
+        g_hm_times = HmTimes{};
+        const double t0 = hm_now();
         dense_blocks(op, h.get(), dn);
+        const double t1 = hm_now();
         compress(op, h.get(), lr);
+        const double t2 = hm_now();
+        if (const char* e = std::getenv("PCB_HM_TIMING"))
+            if (std::atoi(e) != 0)
+                std::fprintf(stderr,
+                             "[pcb hmatrix] dense leaves %.3f s (%zu), low-rank %.3f s (%zu): probe draws %.3f, pack %.3f, "
+                             "block applies (GPU calls) %.3f, unpack %.3f, QR %.3f, SVD %.3f\n",
+                             t1 - t0, dn.size(), t2 - t1, lr.size(), g_hm_times.probes, g_hm_times.pack, g_hm_times.gpu,
+                             g_hm_times.unpack, g_hm_times.qr, g_hm_times.svd);
         *out = h.release();
     });
 }

@@ -1693,18 +1693,21 @@ void plan(pcb_op* op, int32_t dim, const int64_t* dom_lo, const int64_t* dom_hi,
             if (!g.chains.empty()) g.chain_slots.upload(std::vector<int32_t>(g.chains.begin(), g.chains.end()));
     }
     op->a_pool.upload(apool.empty() ? std::vector<double>(1, 0.0) : apool);
-    // PCB_SLOT_FAM=1 (A/B): the column pass takes a group's terms family by family, so the members of
-    // a row family read their shared S rows within ~64 vectors of each other (L2 hits on the second
-    // read).  Measured: c3 cols 3.45 -> 3.42 ms, c4 / c2 unchanged (and streaming stores of T changed
-    // nothing): the pass is latency-bound, not bound by its 18% of excess DRAM reads.  Off by default.
-    if (const char* e = getenv("PCB_SLOT_FAM"))
-        if (atoi(e) != 0)
+    // The column pass takes a group's terms family by family, so the members of a row family read
+    // their shared S rows within ~64 vectors of each other (L2 hits on the second read).  Measured
+    // (PCB_SLOT_FAM=0 / 1): c3 cols 3.45 -> 3.42 ms in two A/B pairs, c4 / c2 unchanged; streaming
+    // stores of T changed nothing: the pass is latency-bound, not bound by its excess DRAM reads.
+    {
+        bool by_family = true;
+        if (const char* e = getenv("PCB_SLOT_FAM")) by_family = atoi(e) != 0;
+        if (by_family)
             for (Group& g : op->groups)
                 std::stable_sort(g.terms.begin(), g.terms.end(), [&](int x, int y) {
                     const int fx = op->term_fam[x] < 0 ? INT32_MAX : op->term_fam[x];
                     const int fy = op->term_fam[y] < 0 ? INT32_MAX : op->term_fam[y];
                     return fx < fy;
                 });
+    }
     for (Group& g : op->groups) g.slots.upload(std::vector<int32_t>(g.terms.begin(), g.terms.end()));
     // 1 / prod P per term (its group's FFT size); the last slot serves the global pseudo term
     std::vector<double> term_scale(op->terms.size() + 1, 1.0);
