@@ -316,7 +316,7 @@ PCB_API pcb_status pcb_debug_guard_check(int64_t* n_regions, int64_t* n_bad_byte
 
 /* Page-locked host memory for the host-buffer calls: F and G in pinned memory go straight to the
  * copy engines (c3: 5.5k vectors/s end to end), pageable buffers are staged through the handle's
- * pinned bounce slots by host threads (~1.2k vectors/s, host-memory-bound).  pcb::pinned_allocator
+ * pinned bounce slots by host threads (~2.8k vectors/s, host-memory-bound).  pcb::pinned_allocator
  * (operator.hpp) wraps these for std::vector. */
 PCB_API pcb_status pcb_host_alloc(uint64_t bytes, void** out);
 PCB_API pcb_status pcb_host_free(void* p);
