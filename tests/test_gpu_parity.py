@@ -176,6 +176,54 @@ def test_edge_cases(gpu):
     assert op.apply_batch(np.zeros((0, 256))).shape == (0, 256)
 
 
+BLOCK_CASES = {
+    "1d": (lambda: inputs.small_lattice(n=50, dim=1, m=5, sigma=2.0), (5,)),
+    "2d_rect": (lambda: inputs.small_lattice(n=24, dim=2, m=3, sigma=1.7), (3, 5)),
+    "3d": (lambda: inputs.small_lattice(n=12, dim=3, m=2, sigma=1.1), (2, 3, 2)),
+    "2d_odd": (lambda: inputs.small_lattice(n=24, dim=2, m=3, sigma=1.7), (3, 3)),  # 81 entries: odd block size
+    "c1_large": (lambda: inputs.make_config("c1"), (16, 16)),  # 256 points: the staged path's upper end
+    "c1_huge": (lambda: inputs.make_config("c1"), (20, 20)),   # too large to stage: the per-entry kernel
+}
+
+
+@pytest.mark.parametrize("name", list(BLOCK_CASES))
+@pytest.mark.parametrize("streams", ["2", "1"])
+def test_blocks_match_entries(gpu, name, streams, monkeypatch):
+    """Dense blocks of every dimension and shape -- near-diagonal ones (terms contribute), far ones
+    (the zero test / zero fill), coincident origins, blocks at the domain edge -- equal the per-entry
+    gather bit for bit (entry() is pinned to the reference), on two streams and on one."""
+    monkeypatch.setenv("PCB_BLOCKS_STREAMS", streams)
+    make, bs = BLOCK_CASES[name]
+    inp = make()
+    op = ProductConvolutionOperator.from_inputs(inp)
+    d = inp.dim
+    n = np.array(inp.shape)
+    bsz = np.array(bs)
+    rng = np.random.default_rng(7)
+    nb = 40 if name.startswith("c1") else 150
+    t = np.stack([rng.integers(0, n[a] - bsz[a] + 1, nb) for a in range(d)], 1)
+    s = t + rng.integers(-4, 5, (nb, d))  # near the diagonal
+    far = rng.random(nb) < 0.4
+    s[far] = np.stack([rng.integers(0, n[a] - bsz[a] + 1, int(far.sum())) for a in range(d)], 1)
+    s = np.clip(s, 0, n - bsz)
+    t[0] = 0  # corners of the domain
+    s[0] = 0
+    t[1] = n - bsz
+    s[1] = n - bsz
+    out = op.blocks(t, s, bs)
+    off = np.array(list(np.ndindex(*bs)))
+    npx = len(off)
+    for b in range(nb):
+        yy = np.repeat(t[b] + off, npx, axis=0)
+        xx = np.tile(s[b] + off, (npx, 1))
+        assert np.array_equal(op.entries(yy, xx).reshape(npx, npx), out[b]), (name, b)
+    assert any(out[b].any() for b in range(nb)) and any(not out[b].any() for b in range(nb))
+    bad_t = t.copy()
+    bad_t[3] = n - bsz + 1  # one block leaves the domain
+    with pytest.raises(ValueError, match="index outside the domain"):
+        op.blocks(bad_t, s, bs)
+
+
 def test_errors_mirror_reference(gpu):
     op = ProductConvolutionOperator.from_inputs(inputs.small_lattice(n=12, dim=2, m=2, sigma=1.0))
     with pytest.raises(ValueError, match="PCOp::apply: shape mismatch"):
