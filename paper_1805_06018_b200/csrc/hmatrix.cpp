@@ -99,6 +99,7 @@ struct pcb_hmatrix {
     int64_t N = 0;
     int32_t leaf_cap = 32;
     std::vector<int64_t> perm;
+    std::vector<int64_t> pts;  // coordinates of the point at each permuted position (N x D; point_of)
     std::vector<CNode> nodes;
     double tol = 0.0;
     int32_t fixed_rank = 0;
@@ -191,11 +192,34 @@ bool admissible(const pcb_hmatrix* h, int32_t t, int32_t s) {
     return distance(h, a, b) >= std::min(diameter(h, a), diameter(h, b));
 }
 
-void point_of(const pcb_hmatrix* h, int64_t perm_pos, int64_t* p) { delin(h, h->perm[(size_t)perm_pos], p); }
+void point_of(const pcb_hmatrix* h, int64_t perm_pos, int64_t* p) {
+    if (!h->pts.empty()) {  // table built by the assembly (no index arithmetic per requested entry)
+        for (int a = 0; a < h->D; ++a) p[a] = h->pts[(size_t)(perm_pos * h->D + a)];
+        return;
+    }
+    delin(h, h->perm[(size_t)perm_pos], p);
+}
+void build_point_table(pcb_hmatrix* h) {
+    h->pts.resize((size_t)(h->N * h->D));
+    int64_t p[3];
+    for (int64_t i = 0; i < h->N; ++i) {
+        delin(h, h->perm[(size_t)i], p);
+        for (int a = 0; a < h->D; ++a) h->pts[(size_t)(i * h->D + a)] = p[a];
+    }
+}
 
 // ---- batched operator access ----------------------------------------------------------------
 
 // (y, x) coordinate lists for pcb_entries
+// PCB_HM_TIMING=1: wall-clock split of an assembly, printed by pcb_hmatrix_assemble (stderr)
+struct HmTimes {
+    double pack = 0, gpu = 0, unpack = 0, qr = 0, svd = 0, probes = 0, form = 0, entries = 0, aca_host = 0;
+};
+HmTimes g_hm_times;
+inline double hm_now() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 struct EntryBatch {
     std::vector<int64_t> y, x;
     void add(const pcb_hmatrix* h, int64_t ypos, int64_t xpos) {
@@ -205,10 +229,20 @@ struct EntryBatch {
         point_of(h, xpos, p);
         x.insert(x.end(), p, p + h->D);
     }
+    void resize(const pcb_hmatrix* h, int64_t n) {
+        y.resize((size_t)(n * h->D));
+        x.resize((size_t)(n * h->D));
+    }
+    void set(const pcb_hmatrix* h, int64_t i, int64_t ypos, int64_t xpos) {  // slot i of a resized batch
+        point_of(h, ypos, &y[(size_t)(i * h->D)]);
+        point_of(h, xpos, &x[(size_t)(i * h->D)]);
+    }
     int64_t size(int D) const { return (int64_t)y.size() / D; }
     std::vector<double> run(pcb_op* op, int D) const {
         std::vector<double> out((size_t)size(D));
+        const double t0 = hm_now();
         if (!out.empty()) ck(pcb_entries(op, size(D), y.data(), x.data(), out.data()));
+        g_hm_times.entries += hm_now() - t0;
         return out;
     }
 };
@@ -227,15 +261,6 @@ int64_t box_index(const pcb_hmatrix* h, const CNode& n, const int64_t* p) {
 
 // block_apply (hmatrix.cpp:116-136), batched: job j applies the (t_j, s_j) block (or its adjoint)
 // to x_j given in cluster order; returns each output in cluster order.
-// PCB_HM_TIMING=1: wall-clock split of an assembly, printed by pcb_hmatrix_assemble (stderr)
-struct HmTimes {
-    double pack = 0, gpu = 0, unpack = 0, qr = 0, svd = 0, probes = 0, form = 0, entries = 0, aca_host = 0;
-};
-HmTimes g_hm_times;
-inline double hm_now() {
-    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
-}
-
 struct ApplyJob {
     int32_t t, s;
     bool adjoint;
@@ -524,25 +549,31 @@ void compress_cur_batch(pcb_op* op, const pcb_hmatrix* h, std::vector<HBlock*>& 
         as.push_back(std::move(a));
     }
     for (;;) {
-        // rows
+        // rows (the requests are filled and the residuals updated block by block on the host's cores)
         EntryBatch rq;
         std::vector<size_t> who;
+        std::vector<int64_t> offs;
+        int64_t tot = 0;
         for (size_t i = 0; i < as.size(); ++i) {
-            A& a = as[i];
-            if (a.st != NEED_ROW) continue;
-            const CNode& tn = h->nodes[(size_t)a.b->t];
-            const CNode& sn = h->nodes[(size_t)a.b->s];
-            for (int64_t j = 0; j < a.ns; ++j) rq.add(h, tn.begin + a.next_row, sn.begin + j);
+            if (as[i].st != NEED_ROW) continue;
             who.push_back(i);
+            offs.push_back(tot);
+            tot += as[i].ns;
         }
         bool any = !who.empty();
         if (any) {
+            rq.resize(h, tot);
+            parallel_for(who.size(), [&](size_t w) {
+                const A& a = as[who[w]];
+                const CNode& tn = h->nodes[(size_t)a.b->t];
+                const CNode& sn = h->nodes[(size_t)a.b->s];
+                for (int64_t j = 0; j < a.ns; ++j) rq.set(h, offs[w] + j, tn.begin + a.next_row, sn.begin + j);
+            });
             const std::vector<double> vals = rq.run(op, h->D);
-            size_t off = 0;
-            for (size_t i : who) {
-                A& a = as[i];
+            parallel_for(who.size(), [&](size_t w) {
+                A& a = as[who[w]];
+                const size_t off = (size_t)offs[w];
                 std::vector<double> r(vals.begin() + (int64_t)off, vals.begin() + (int64_t)(off + a.ns));
-                off += (size_t)a.ns;
                 for (size_t k = 0; k < a.us.size(); ++k) {
                     const double c = a.us[k][(size_t)a.next_row];
                     for (int64_t j = 0; j < a.ns; ++j) r[(size_t)j] -= c * a.vs[k][(size_t)j];
@@ -564,34 +595,40 @@ void compress_cur_batch(pcb_op* op, const pcb_hmatrix* h, std::vector<HBlock*>& 
                         }
                     if (cand < 0) a.st = DONE;
                     else a.next_row = cand;
-                    continue;
+                    return;
                 }
                 a.v.resize((size_t)a.ns);
                 const double piv = r[(size_t)jp];
                 for (int64_t j = 0; j < a.ns; ++j) a.v[(size_t)j] = r[(size_t)j] / piv;
                 a.jpiv = jp;
                 a.st = NEED_COL;
-            }
+            });
         }
         // columns
         EntryBatch cq;
         who.clear();
+        offs.clear();
+        tot = 0;
         for (size_t i = 0; i < as.size(); ++i) {
-            A& a = as[i];
-            if (a.st != NEED_COL) continue;
-            const CNode& tn = h->nodes[(size_t)a.b->t];
-            const CNode& sn = h->nodes[(size_t)a.b->s];
-            for (int64_t q = 0; q < a.nt; ++q) cq.add(h, tn.begin + q, sn.begin + a.jpiv);
+            if (as[i].st != NEED_COL) continue;
             who.push_back(i);
+            offs.push_back(tot);
+            tot += as[i].nt;
         }
         any = any || !who.empty();
         if (!who.empty()) {
+            cq.resize(h, tot);
+            parallel_for(who.size(), [&](size_t w) {
+                const A& a = as[who[w]];
+                const CNode& tn = h->nodes[(size_t)a.b->t];
+                const CNode& sn = h->nodes[(size_t)a.b->s];
+                for (int64_t q = 0; q < a.nt; ++q) cq.set(h, offs[w] + q, tn.begin + q, sn.begin + a.jpiv);
+            });
             const std::vector<double> vals = cq.run(op, h->D);
-            size_t off = 0;
-            for (size_t i : who) {
-                A& a = as[i];
+            parallel_for(who.size(), [&](size_t w) {
+                A& a = as[who[w]];
+                const size_t off = (size_t)offs[w];
                 std::vector<double> u(vals.begin() + (int64_t)off, vals.begin() + (int64_t)(off + a.nt));
-                off += (size_t)a.nt;
                 for (size_t k = 0; k < a.us.size(); ++k) {
                     const double c = a.vs[k][(size_t)a.jpiv];
                     for (int64_t q = 0; q < a.nt; ++q) u[(size_t)q] -= c * a.us[k][(size_t)q];
@@ -623,7 +660,7 @@ void compress_cur_batch(pcb_op* op, const pcb_hmatrix* h, std::vector<HBlock*>& 
                     }
                 }
                 if (a.st != DONE && (int64_t)a.us.size() >= a.max_rank) a.st = DONE;
-            }
+            });
         }
         if (!any) break;
     }
@@ -671,25 +708,37 @@ void compress_randomized_batch(pcb_op* op, const pcb_hmatrix* h, std::vector<HBl
         std::vector<ApplyJob> jobs;
         std::vector<size_t> who;
         std::vector<int> nprobe;
+        std::vector<size_t> job0;
+        size_t njobs = 0;
         for (size_t i = 0; i < rs.size(); ++i) {
             R& r = rs[i];
             if (!r.active) continue;
             const bool resid = !(fixed_rank > 0 || r.l >= r.max_rank);
             const int64_t cnt = r.l + (resid ? s_probes : 0);
-            for (int64_t j = 0; j < cnt; ++j) {
-                ApplyJob jb{r.b->t, r.b->s, false, std::vector<double>((size_t)r.ns)};
-                for (int64_t q = 0; q < r.ns; ++q) jb.x[(size_t)q] = r.gauss(r.rng);
-                jobs.push_back(std::move(jb));
-            }
             who.push_back(i);
             nprobe.push_back((int)cnt);
+            job0.push_back(njobs);
+            njobs += (size_t)cnt;
         }
         if (who.empty()) break;
+        jobs.resize(njobs);
+        parallel_for(who.size(), [&](size_t w) {  // every block draws from its own stream
+            R& r = rs[who[w]];
+            for (int j = 0; j < nprobe[w]; ++j) {
+                ApplyJob& jb = jobs[job0[w] + (size_t)j];
+                jb.t = r.b->t;
+                jb.s = r.b->s;
+                jb.adjoint = false;
+                jb.x.resize((size_t)r.ns);
+                for (int64_t q = 0; q < r.ns; ++q) jb.x[(size_t)q] = r.gauss(r.rng);
+            }
+        });
         g_hm_times.probes += hm_now() - t_round;
         const std::vector<std::vector<double>> ys = block_apply_batch(op, h, jobs);
-        size_t o = 0;
-        for (size_t w = 0; w < who.size(); ++w) {
+        const double t_qr = hm_now();
+        parallel_for(who.size(), [&](size_t w) {
             R& r = rs[who[w]];
+            const size_t o = job0[w];
             const bool resid = nprobe[w] > r.l;
             std::vector<double> Y((size_t)(r.nt * r.l));
             double y_fro2 = 0.0;
@@ -702,17 +751,13 @@ void compress_randomized_batch(pcb_op* op, const pcb_hmatrix* h, std::vector<HBl
             if (scale == 0.0) {
                 r.zero = true;
                 r.active = false;
-                o += (size_t)nprobe[w];
-                continue;
+                return;
             }
-            const double t_qr = hm_now();
             r.Q = householder_q(Y, r.nt, r.l);
-            g_hm_times.qr += hm_now() - t_qr;
             r.qc = std::min(r.nt, r.l);
             if (!resid) {
                 r.active = false;
-                o += (size_t)nprobe[w];
-                continue;
+                return;
             }
             double r2 = 0.0;
             std::vector<double> c((size_t)r.qc);
@@ -729,8 +774,8 @@ void compress_randomized_batch(pcb_op* op, const pcb_hmatrix* h, std::vector<HBl
             const double res = std::sqrt(r2 / s_probes);
             if (res <= 0.25 * tol * scale) r.active = false;
             else r.l = std::min(r.max_rank, 2 * r.l);
-            o += (size_t)nprobe[w];
-        }
+        });
+        g_hm_times.qr += hm_now() - t_qr;
     }
     // adjoint pass: B = Q^T A = (A^* Q)^T
     std::vector<ApplyJob> jobs;
@@ -892,6 +937,7 @@ PCB_API pcb_status pcb_cluster_tree(int32_t dim, const int64_t* dom_lo, const in
         init_domain(h.get(), dim, dom_lo, dom_hi);
         h->leaf_cap = leaf_cap;
         build_tree(h.get());
+        build_point_table(h.get());
         *out = h.release();
     });
 }
@@ -918,6 +964,7 @@ PCB_API pcb_status pcb_hmatrix_assemble(pcb_op* op, double tol, int32_t leaf_cap
         h->fixed_rank = fixed_rank;
         h->method = method;
         build_tree(h.get());
+        build_point_table(h.get());
         // block partition, preorder (assemble_hmatrix, hmatrix.cpp:345-375)
         std::function<void(int32_t, int32_t)> rec = [&](int32_t t, int32_t s) {
             const CNode& tn = h->nodes[(size_t)t];
@@ -955,9 +1002,10 @@ PCB_API pcb_status pcb_hmatrix_assemble(pcb_op* op, double tol, int32_t leaf_cap
             if (std::atoi(e) != 0)
                 std::fprintf(stderr,
                              "[pcb hmatrix] dense leaves %.3f s (%zu), low-rank %.3f s (%zu): probe draws %.3f, pack %.3f, "
-                             "block applies (GPU calls) %.3f, unpack %.3f, QR %.3f, SVD %.3f\n",
+                             "block applies (GPU calls) %.3f, unpack %.3f, QR %.3f, SVD %.3f; entry requests (pcb_entries calls, "
+                             "dense + ACA) %.3f\n",
                              t1 - t0, dn.size(), t2 - t1, lr.size(), g_hm_times.probes, g_hm_times.pack, g_hm_times.gpu,
-                             g_hm_times.unpack, g_hm_times.qr, g_hm_times.svd);
+                             g_hm_times.unpack, g_hm_times.qr, g_hm_times.svd, g_hm_times.entries);
         *out = h.release();
     });
 }
