@@ -110,3 +110,26 @@ def test_hmatrix_vs_live_reference(gpu, method, tmp_path):
     R2 = ref_lib.RefHMatrix.load(path, inp.n_points)
     assert R2.info()["n_blocks"] == h.info["n_blocks"]
     assert np.allclose(R2.matvec(f), h.matvec(f), rtol=0, atol=1e-13 * np.abs(g_ref).max())
+
+
+@pytest.mark.parametrize("method", ["randomized", "cur"])
+def test_hmatrix_vs_live_reference_larger(gpu, method, tmp_path):
+    """The same comparison on a 48 x 48 domain (N = 2,304, leaf 32: ~3,800 blocks, ranks up to ~36):
+    the sizes where the block factorizations run on several host threads and the tall SVDs go
+    through QR.  File-level comparison (tree, partition, dense leaves, ranks, factors) and matvec."""
+    from oracle import ref_lib
+
+    if not ref_lib.available():
+        pytest.skip("reference build (oracle/_ref) not shipped with this copy")
+    inp = inputs.small_lattice(n=48, dim=2, m=3, sigma=2.0)
+    op = ProductConvolutionOperator.from_inputs(inp)
+    h = HMatrix.assemble(op, TOL, 32, method)
+    path = str(tmp_path / f"ours48_{method}.pchm")
+    h.save(path)
+    R = ref_lib.RefHMatrix.assemble(ref_lib.RefOperator(inp), TOL, 32, method)
+    ref_path = str(tmp_path / f"live48_{method}.pchm")
+    R.save(ref_path)
+    compare_files(path, ref_path, method)
+    f = normal_vectors(33, 1, inp.n_points)[0]
+    g_ref = R.matvec(f)
+    assert np.linalg.norm(h.matvec(f) - g_ref) <= FACTOR_TOL[method] * np.linalg.norm(g_ref)
