@@ -58,9 +58,17 @@ def compare_files(path_ours, path_ref, method):
     assert tree_bytes(a) == tree_bytes(b)
     da, db = HO.read_pchm(path_ours), HO.read_pchm(path_ref)
     assert [(t, s, lr) for t, s, lr, *_ in da["blocks"]] == [(t, s, lr) for t, s, lr, *_ in db["blocks"]]
+    # the scale of the matrix: an admissible block whose entries are all exactly zero (beyond every
+    # kernel's truncation radius) is a rank-0 block here (the block applies use the exact entry
+    # gather), while the reference's FFT-based apply_block returns rounding noise (~1e-17) for it and
+    # its range finder "compresses" that noise to some rank: such blocks must be negligible
+    big = max([np.linalg.norm(Br @ Cr) for _, _, lr, Br, Cr, _ in db["blocks"] if lr and Br.shape[1]] + [1e-300])
     for (t, s, lr, B, C, D), (_, _, _, Br, Cr, Dr) in zip(da["blocks"], db["blocks"]):
         if not lr:
             assert np.array_equal(D, Dr), (t, s)  # dense leaves: reference entry(), bitwise
+            continue
+        if method == "randomized" and B.shape[1] == 0 and Br.shape[1] > 0:
+            assert np.linalg.norm(Br @ Cr) <= 1e-13 * big, (t, s, np.linalg.norm(Br @ Cr), big)
             continue
         assert B.shape[1] == Br.shape[1], (method, t, s, B.shape, Br.shape)  # same rank
         if B.shape[1] == 0:
