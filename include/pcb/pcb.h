@@ -264,7 +264,7 @@ PCB_API pcb_status pcb_get_domain(const pcb_op* op, int64_t* dom_lo, int64_t* do
  *                           approximation over batched GPU entries (:236-318)
  *   pcb_hmatrix_compress    compress_block (:320-336) for listed (t, s) node pairs, appended as
  *                           low-rank blocks
- *   pcb_hmatrix_matvec      HMatrix::matvec (:379-400), host
+ *   pcb_hmatrix_matvec      HMatrix::matvec (:379-400), host; pcb_hmatrix_matvec_batch: on the GPU
  *   pcb_hmatrix_save/_load  the little-endian "PCHM" v1 container, byte-compatible with the
  *                           reference's save_hmatrix / load_hmatrix (:433-526)
  *   pcb_hmatrix_tree / _block / _admissible / _get_info   inspection */
@@ -305,6 +305,10 @@ PCB_API pcb_status pcb_hmatrix_block(pcb_hmatrix* h, int64_t i, int32_t* t_s_kin
 PCB_API pcb_status pcb_hmatrix_admissible(pcb_hmatrix* h, int32_t t, int32_t s, int32_t* adm, double* dist,
                                           double* diam_t, double* diam_s);
 PCB_API pcb_status pcb_hmatrix_matvec(pcb_hmatrix* h, const double* f, double* g);
+/* The same product for B vectors (B x N, vector-major) on GPU `device`: the blocks are copied to the
+ * device on the first call; every row's dot product and the sum over the blocks covering a row keep
+ * the host loop's order (IEEE mul / add), so each vector equals pcb_hmatrix_matvec bit for bit. */
+PCB_API pcb_status pcb_hmatrix_matvec_batch(pcb_hmatrix* h, int32_t device, int32_t B, const double* F, double* G);
 PCB_API pcb_status pcb_hmatrix_save(pcb_hmatrix* h, const char* path);
 PCB_API pcb_status pcb_hmatrix_load(const char* path, pcb_hmatrix** out);
 

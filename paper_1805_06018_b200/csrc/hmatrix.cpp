@@ -31,6 +31,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "pcb/pcb.h"
 
 void pcb_detail_set_error(const std::string& m);
@@ -106,6 +108,35 @@ struct pcb_hmatrix {
     int32_t method = PCB_HM_RANDOMIZED;
     std::vector<HBlock> blocks;
     bool any_capped = false;
+    // device copy for pcb_hmatrix_matvec_batch (built on first use, freed by destroy)
+    struct Dev {
+        int device = -1;
+        double* vals = nullptr;      // every block's dense / B / C values, row-major
+        int64_t* perm = nullptr;
+        void* items_a = nullptr;     // GemvItem lists: pass A (t = C x), pass B (y = D x | B t)
+        void* items_b = nullptr;
+        int64_t n_a = 0, n_b = 0;
+        int64_t* row_ptr = nullptr;  // per permuted row position: its slots of the y buffer, block order
+        int64_t* row_idx = nullptr;
+        int64_t y_total = 0, t_total = 0;
+        double *F = nullptr, *G = nullptr, *Y = nullptr, *T = nullptr;
+        int64_t cap_vec = 0;
+    } dev;
+    ~pcb_hmatrix() {
+        if (dev.device >= 0) {
+            cudaSetDevice(dev.device);
+            cudaFree(dev.vals);
+            cudaFree(dev.perm);
+            cudaFree(dev.items_a);
+            cudaFree(dev.items_b);
+            cudaFree(dev.row_ptr);
+            cudaFree(dev.row_idx);
+            cudaFree(dev.F);
+            cudaFree(dev.G);
+            cudaFree(dev.Y);
+            cudaFree(dev.T);
+        }
+    }
 };
 
 namespace {
@@ -920,6 +951,134 @@ Mat rd_mat(std::istream& is) {
     return m;
 }
 
+// ---- GPU matvec (HMatrix::matvec, hmatrix.cpp:379-400, for B vectors at once) -----------------
+// Three passes: A) t = C x_S for every low-rank block, B) y = D x_S (dense) or y = B t (low rank)
+// into a per-block slot of a y buffer, C) g[perm[p]] = sum of the slots covering row p in block
+// order.  Every row's dot product runs over its columns in ascending order with IEEE mul / add, and
+// the rows' contributions are added in block order: the result is bit-identical to the host
+// matvec (and to the reference's loop order).
+struct GemvItem {
+    int64_t a_off;   // row-major rows x cols values at vals + a_off (lda = cols)
+    int64_t x_off;   // x: gathered from f through perm[x_off + j] (x_perm) or read from the t buffer at x_off
+    int64_t out_off; // y / t buffer offset of row 0 of the tile
+    int32_t rows, cols;
+    int32_t row0;    // first row of this tile within the block
+    int32_t x_perm;
+};
+constexpr int HM_TR = 128, HM_TC = 32;  // tile: 128 rows (one per thread) x 32 columns staged in shared memory
+
+__global__ void __launch_bounds__(HM_TR) k_hm_gemv(const GemvItem* __restrict__ items, const double* __restrict__ vals,
+                                                   const int64_t* __restrict__ perm, const double* __restrict__ f,
+                                                   int64_t f_vst, const double* __restrict__ xbuf, int64_t x_vst,
+                                                   double* __restrict__ out, int64_t out_vst) {
+    __shared__ double tile[HM_TR][HM_TC + 1];
+    __shared__ double xs[HM_TC];
+    const GemvItem it = items[blockIdx.x];
+    const int vec = blockIdx.y;
+    const int tid = threadIdx.x;
+    const int nrow = min(HM_TR, it.rows - it.row0);
+    const double* A = vals + it.a_off + (int64_t)it.row0 * it.cols;
+    double sum = 0.0;
+    for (int c0 = 0; c0 < it.cols; c0 += HM_TC) {
+        const int nc = min(HM_TC, it.cols - c0);
+        __syncthreads();
+        if (tid < nc)
+            xs[tid] = it.x_perm ? f[(int64_t)vec * f_vst + perm[it.x_off + c0 + tid]]
+                                : xbuf[(int64_t)vec * x_vst + it.x_off + c0 + tid];
+        for (int e = tid; e < nrow * nc; e += HM_TR) {  // coalesced along the columns
+            const int r = e / nc, c = e - r * nc;
+            tile[r][c] = A[(int64_t)r * it.cols + c0 + c];
+        }
+        __syncthreads();
+        if (tid < nrow)
+            for (int c = 0; c < nc; ++c) sum = __dadd_rn(sum, __dmul_rn(tile[tid][c], xs[c]));
+    }
+    if (tid < nrow) out[(int64_t)vec * out_vst + it.out_off + tid] = sum;
+}
+
+__global__ void k_hm_gather(int64_t n, const int64_t* __restrict__ perm, const int64_t* __restrict__ row_ptr,
+                            const int64_t* __restrict__ row_idx, const double* __restrict__ Y, int64_t y_vst,
+                            double* __restrict__ g, int64_t g_vst) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int vec = blockIdx.y;
+    double sum = 0.0;
+    for (int64_t e = row_ptr[p]; e < row_ptr[p + 1]; ++e) sum = __dadd_rn(sum, Y[(int64_t)vec * y_vst + row_idx[e]]);
+    g[(int64_t)vec * g_vst + perm[p]] = sum;
+}
+
+void cu(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        hfail(e == cudaErrorMemoryAllocation ? PCB_ENOMEM : PCB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+template <typename T>
+T* dev_upload(const std::vector<T>& v, const char* what) {
+    T* p = nullptr;
+    cu(cudaMalloc((void**)&p, std::max<size_t>(v.size(), 1) * sizeof(T)), what);
+    if (!v.empty()) cu(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), what);
+    return p;
+}
+
+void build_device_copy(pcb_hmatrix* h, int device) {
+    pcb_hmatrix::Dev& d = h->dev;
+    cu(cudaSetDevice(device), "cudaSetDevice");
+    std::vector<double> vals;
+    std::vector<GemvItem> ia, ib;
+    std::vector<std::vector<int64_t>> rows((size_t)h->N);
+    int64_t y_off = 0, t_off = 0;
+    auto tiles = [](std::vector<GemvItem>& dst, GemvItem it) {
+        for (int32_t r0 = 0; r0 < it.rows; r0 += HM_TR) {
+            it.row0 = r0;
+            GemvItem t = it;
+            t.out_off = it.out_off + r0;
+            dst.push_back(t);
+        }
+    };
+    for (const HBlock& b : h->blocks) {
+        const CNode& tn = h->nodes[(size_t)b.t];
+        const CNode& sn = h->nodes[(size_t)b.s];
+        if (b.low_rank) {
+            const int64_t rk = b.C.r;
+            if (rk > 0) {
+                GemvItem a{(int64_t)vals.size(), sn.begin, t_off, (int32_t)rk, (int32_t)b.C.c, 0, 1};
+                vals.insert(vals.end(), b.C.v.begin(), b.C.v.end());
+                tiles(ia, a);
+            }
+            // rank 0: y = 0 (a tile with no columns)
+            GemvItem y{(int64_t)vals.size(), t_off, y_off, (int32_t)b.B.r, (int32_t)rk, 0, 0};
+            vals.insert(vals.end(), b.B.v.begin(), b.B.v.end());
+            tiles(ib, y);
+            t_off += rk;
+        } else {
+            GemvItem y{(int64_t)vals.size(), sn.begin, y_off, (int32_t)b.dense.r, (int32_t)b.dense.c, 0, 1};
+            vals.insert(vals.end(), b.dense.v.begin(), b.dense.v.end());
+            tiles(ib, y);
+        }
+        for (int64_t i = 0; i < tn.size(); ++i) rows[(size_t)(tn.begin + i)].push_back(y_off + i);
+        y_off += tn.size();
+    }
+    std::vector<int64_t> rp((size_t)h->N + 1, 0), ri;
+    ri.reserve((size_t)y_off);
+    for (int64_t p = 0; p < h->N; ++p) {
+        rp[(size_t)p] = (int64_t)ri.size();
+        ri.insert(ri.end(), rows[(size_t)p].begin(), rows[(size_t)p].end());
+    }
+    rp[(size_t)h->N] = (int64_t)ri.size();
+    d.device = device;
+    d.vals = dev_upload(vals, "H-matrix values");
+    d.perm = dev_upload(h->perm, "H-matrix permutation");
+    d.items_a = dev_upload(ia, "H-matrix items");
+    d.items_b = dev_upload(ib, "H-matrix items");
+    d.n_a = (int64_t)ia.size();
+    d.n_b = (int64_t)ib.size();
+    d.row_ptr = dev_upload(rp, "H-matrix row lists");
+    d.row_idx = dev_upload(ri, "H-matrix row lists");
+    d.y_total = y_off;
+    d.t_total = t_off;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1184,6 +1343,47 @@ PCB_API pcb_status pcb_hmatrix_matvec(pcb_hmatrix* h, const double* f, double* g
             }
             for (int64_t i = 0; i < tn.size(); ++i) g[h->perm[(size_t)(tn.begin + i)]] += y[(size_t)i];
         }
+    });
+}
+
+PCB_API pcb_status pcb_hmatrix_matvec_batch(pcb_hmatrix* h, int32_t device, int32_t B, const double* F, double* G) {
+    if (!h || !F || !G) {
+        pcb_detail_set_error("null argument");
+        return PCB_EINVAL;
+    }
+    std::lock_guard<std::mutex> lk(h->mu);
+    return hguard([&] {
+        if (B < 0 || B > 65535) hfail(PCB_EINVAL, "pcb_hmatrix_matvec_batch: 0 <= B <= 65535 required");
+        if (B == 0) return;
+        pcb_hmatrix::Dev& d = h->dev;
+        if (d.device >= 0 && d.device != device) hfail(PCB_EINVAL, "pcb_hmatrix_matvec_batch: the H-matrix lives on another device");
+        if (d.device < 0) build_device_copy(h, device);
+        cu(cudaSetDevice(device), "cudaSetDevice");
+        if (d.cap_vec < B) {
+            cudaFree(d.F);
+            cudaFree(d.G);
+            cudaFree(d.Y);
+            cudaFree(d.T);
+            d.F = d.G = d.Y = d.T = nullptr;
+            d.cap_vec = 0;
+            cu(cudaMalloc((void**)&d.F, (size_t)B * h->N * 8), "matvec buffers");
+            cu(cudaMalloc((void**)&d.G, (size_t)B * h->N * 8), "matvec buffers");
+            cu(cudaMalloc((void**)&d.Y, std::max<size_t>((size_t)B * d.y_total, 1) * 8), "matvec buffers");
+            cu(cudaMalloc((void**)&d.T, std::max<size_t>((size_t)B * d.t_total, 1) * 8), "matvec buffers");
+            d.cap_vec = B;
+        }
+        cu(cudaMemcpy(d.F, F, (size_t)B * h->N * 8, cudaMemcpyHostToDevice), "H2D");
+        const GemvItem* ia = static_cast<const GemvItem*>(d.items_a);
+        const GemvItem* ib = static_cast<const GemvItem*>(d.items_b);
+        if (d.n_a > 0)
+            k_hm_gemv<<<dim3((unsigned)d.n_a, (unsigned)B), HM_TR>>>(ia, d.vals, d.perm, d.F, h->N, nullptr, 0, d.T, d.t_total);
+        if (d.n_b > 0)
+            k_hm_gemv<<<dim3((unsigned)d.n_b, (unsigned)B), HM_TR>>>(ib, d.vals, d.perm, d.F, h->N, d.T, d.t_total, d.Y,
+                                                                  d.y_total);
+        k_hm_gather<<<dim3((unsigned)((h->N + 255) / 256), (unsigned)B), 256>>>(h->N, d.perm, d.row_ptr, d.row_idx, d.Y,
+                                                                             d.y_total, d.G, h->N);
+        cu(cudaGetLastError(), "H-matrix matvec kernels");
+        cu(cudaMemcpy(G, d.G, (size_t)B * h->N * 8, cudaMemcpyDeviceToHost), "D2H");
     });
 }
 

@@ -168,3 +168,12 @@ class HMatrix:
         g = np.empty_like(f)
         _rc(_L.load().pcb_hmatrix_matvec(self._h, f.ctypes.data, g.ctypes.data))
         return g
+
+    def matvec_batch(self, F: np.ndarray, device: int = 0) -> np.ndarray:
+        """B products at once on the GPU (pcb_hmatrix_matvec_batch): bit-identical to matvec per vector."""
+        F = np.ascontiguousarray(F, dtype=np.float64)
+        if F.ndim != 2 or F.shape[1] != self.n_points:
+            raise ValueError("HMatrix::matvec: size mismatch")
+        G = np.empty_like(F)
+        _rc(_L.load().pcb_hmatrix_matvec_batch(self._h, int(device), F.shape[0], F.ctypes.data, G.ctypes.data))
+        return G

@@ -35,7 +35,7 @@ EXPORTS = ["pcb_default_options", "pcb_last_error", "pcb_create", "pcb_destroy",
            "pcb_hmatrix_destroy", "pcb_hmatrix_get_info", "pcb_hmatrix_tree", "pcb_hmatrix_block",
            "pcb_hmatrix_admissible", "pcb_hmatrix_matvec", "pcb_hmatrix_save", "pcb_hmatrix_load",
            "pcb_comm_unique_id", "pcb_plan_shards", "pcb_debug_guard_check", "pcb_estimator_create_ex",
-           "pcb_host_alloc", "pcb_host_free", "pcb_create_multi", "pcb_host_register", "pcb_host_unregister"]
+           "pcb_host_alloc", "pcb_host_free", "pcb_create_multi", "pcb_host_register", "pcb_host_unregister", "pcb_hmatrix_matvec_batch"]
 RNG = {"mt19937": 0, "philox": 1}
 REDUCE = {"none": 0, "all": 1, "root": 2}
 PARTITION = {"cost": 0, "count": 1}
@@ -149,6 +149,7 @@ def load():
     L.pcb_hmatrix_block.argtypes = [vp, i64, vp, vp, vp, vp, vp]
     L.pcb_hmatrix_admissible.argtypes = [vp, i32, i32, vp, vp, vp, vp]
     L.pcb_hmatrix_matvec.argtypes = [vp, vp, vp]
+    L.pcb_hmatrix_matvec_batch.argtypes = [vp, i32, i32, vp, vp]
     L.pcb_hmatrix_save.argtypes = [vp, ctypes.c_char_p]
     L.pcb_hmatrix_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
     L.pcb_comm_unique_id.argtypes = [vp]
