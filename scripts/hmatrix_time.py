@@ -29,9 +29,18 @@ for case in CASES:
         t0 = time.perf_counter()
         h = HMatrix.assemble(op, 1e-8, leaf, method)
         t_gpu = time.perf_counter() - t0
+        t0 = time.perf_counter()
         g = h.matvec(f)
+        t_host_mv = time.perf_counter() - t0
+        Fb = normal_vectors(6, 32, inp.n_points)
+        h.matvec_batch(Fb)  # first call copies the blocks to the device
+        t0 = time.perf_counter()
+        Gb = h.matvec_batch(Fb)
+        t_gpu_mv = time.perf_counter() - t0
         r = {"gpu_assemble_s": t_gpu, "blocks": len(h.blocks()),
-             "matvec_vs_apply_rel": float(np.linalg.norm(g - g_op) / np.linalg.norm(g_op))}
+             "matvec_vs_apply_rel": float(np.linalg.norm(g - g_op) / np.linalg.norm(g_op)),
+             "host_matvec_ms_per_vector": t_host_mv * 1e3, "gpu_matvec_batch32_ms": t_gpu_mv * 1e3,
+             "gpu_matvec_equals_host": bool(np.array_equal(Gb[0], h.matvec(Fb[0])))}
         try:
             from oracle import ref_lib  # reported baseline only
             if ref_lib.available():
@@ -40,7 +49,9 @@ for case in CASES:
                 hr = ref_lib.RefHMatrix.assemble(rop, 1e-8, leaf, method)
                 r["reference_assemble_s"] = time.perf_counter() - t0
                 r["reference_threads"] = 1
+                t0 = time.perf_counter()
                 gr = hr.matvec(f)
+                r["reference_matvec_ms_per_vector"] = (time.perf_counter() - t0) * 1e3
                 r["matvec_vs_reference_rel"] = float(np.linalg.norm(g - gr) / np.linalg.norm(gr))
                 r["speedup"] = r["reference_assemble_s"] / t_gpu
         except Exception as ex:  # reported, never fatal
